@@ -1,0 +1,216 @@
+/*
+ * damf_gpu.h — C ABI of the B200-native DAMF hot path.
+ *
+ * This is the drop-in boundary. The reference (arxiv 2306.08967, DAMF) is a
+ * C++ library whose hot path is reached through damf::Engine
+ * (/root/reference/proj/include/damf/engine.hpp:26-61). It has no FFI, so
+ * every entry point below names the reference member function it replaces;
+ * the header-only C++ facade (paper_2306_08967_b200/csrc/damf_engine.hpp)
+ * restores the Engine API on top of it, and INTEGRATION.md shows the
+ * ctypes / pybind binding a maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no CUDA or torch types cross the ABI.
+ *    Buffers named *_host are host memory; *_dev are device pointers.
+ *  - Every call returns a status: 0 = ok, otherwise damf::Error::Kind
+ *    ordinal + 1 (types.hpp:21-41), so DAMF_E_UNKNOWN_NODE == 2, etc.
+ *    DAMF_E_CUDA / DAMF_E_UNSUPPORTED are ABI-specific. No exception ever
+ *    crosses the ABI; damf_gpu_last_error() returns the message.
+ *  - One CUDA stream per handle; calls on one handle are externally
+ *    serialised (single writer).
+ *  - Node ids are dense int64 in [0, n); AddNode ids are implicit (= n).
+ */
+#ifndef DAMF_GPU_H_
+#define DAMF_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: Error::Kind ordinal + 1 (types.hpp:21-41) ----------- */
+enum {
+  DAMF_OK = 0,
+  DAMF_E_PARSE = 1,
+  DAMF_E_UNKNOWN_NODE = 2,
+  DAMF_E_DUPLICATE_EDGE = 3,
+  DAMF_E_MISSING_EDGE = 4,
+  DAMF_E_SHAPE_MISMATCH = 5,
+  DAMF_E_ZERO_MATRIX = 6,
+  DAMF_E_NON_FINITE = 7,
+  DAMF_E_SINGULAR_PROJECTION = 8,
+  DAMF_E_NON_CONVERGENCE = 9,
+  DAMF_E_DEGENERATE_LABELS = 10,
+  DAMF_E_K_TOO_LARGE = 11,
+  DAMF_E_GRAPH_TOO_SMALL = 12,
+  DAMF_E_TOO_LARGE = 13,
+  DAMF_E_IO = 14,
+  DAMF_E_CUDA = 100,
+  DAMF_E_UNSUPPORTED = 101
+};
+
+/* GraphEvent::Kind order (graph.hpp:17). */
+enum { DAMF_ADD_NODE = 0, DAMF_ADD_EDGE = 1, DAMF_REMOVE_EDGE = 2 };
+
+/* Matrices addressable by the query / state calls. */
+enum {
+  DAMF_XB = 0,     /* base context rows  X_b  (n x k, fp32)  factor_state.hpp:68 */
+  DAMF_YB = 1,     /* base content rows  Y_b  (n x k, fp32)                      */
+  DAMF_PX = 2,     /* projection P_X (k x k, fp64)           factor_state.hpp:69 */
+  DAMF_PY = 3,     /* projection P_Y (k x k, fp64)                               */
+  DAMF_SIGMA = 4,  /* spectrum (k, fp64)                     factor_state.hpp:70 */
+  DAMF_ZB = 5,     /* enhancer Z_b (n x k, fp32)             enhancer.hpp:67     */
+  DAMF_RB = 6,     /* enhancer r_b (n x k, fp32)                                 */
+  DAMF_X = 7,      /* current X = X_b P_X  (query_all / query_context)           */
+  DAMF_Y = 8,      /* current Y = Y_b P_Y  (query_all / query_content)           */
+  DAMF_Z = 9,      /* enhanced Z = Z_b P_X (query_enhanced)                      */
+  DAMF_QX = 10,    /* maintained inverse P_X^{-1} (k x k, fp64; GPU-only state)  */
+  DAMF_QY = 11
+};
+
+/* RunConfig (engine.hpp:13-21) plus device sizing. */
+typedef struct damf_config {
+  int64_t d;             /* target rank                                   */
+  double alpha;          /* PPR restart (enhancer.hpp:14-17)              */
+  double eps;            /* PPR push threshold                            */
+  uint64_t seed;         /* init sketch seed                              */
+  double rebase_cond;    /* rebase when cond(P_X) exceeds this (1e8)      */
+  int64_t rebase_every;  /* rebase every this many events (50000)         */
+  int32_t undirected;    /* DynamicGraph(n, undirected)                   */
+  int32_t flags;         /* reserved, 0                                   */
+  int64_t node_capacity; /* rows to reserve beyond n for AddNode (0=auto) */
+  int64_t arc_capacity;  /* arc slots to reserve beyond arcs (0=auto)     */
+} damf_config;
+
+/* Out-adjacency in CSR form (host memory). weights may be NULL (all 1.0). */
+typedef struct damf_csr {
+  int64_t n;
+  int64_t arcs;
+  const int64_t* offsets; /* n+1 */
+  const int32_t* targets; /* arcs */
+  const double* weights;  /* arcs or NULL */
+} damf_csr;
+
+/* A batch of GraphEvents (graph.hpp:14-47), applied SEQUENTIALLY exactly as
+ * `for (e : batch) engine.apply(e)`. AddNode neighbour lists use offsets
+ * into flat arrays (in_off/out_off have count+1 entries; NULL if unused).
+ * All pointers are host memory; w / in_w / out_w may be NULL (1.0). */
+typedef struct damf_event_batch {
+  int64_t count;
+  const int32_t* kind;
+  const int64_t* u;
+  const int64_t* v;
+  const double* w;
+  const int64_t* in_off;
+  const int64_t* in_ids;
+  const double* in_w;
+  const int64_t* out_off;
+  const int64_t* out_ids;
+  const double* out_w;
+} damf_event_batch;
+
+/* Apply modes (bit flags). The default (0) is Engine::apply. */
+enum {
+  DAMF_APPLY_GRAPH_AND_PPR_ONLY = 1, /* structure-only events: graph mutation
+                                        + absorb_structure_delta + push, no
+                                        factor update   */
+  DAMF_APPLY_DEFER_PUSH = 2,         /* absorb only; caller pushes later   */
+  DAMF_APPLY_TIME_EVENTS = 4         /* record per-event device latency    */
+};
+
+typedef struct damf_apply_stats {
+  int64_t applied;       /* events fully applied                          */
+  int64_t failed_index;  /* index of the failing event, or -1             */
+  int64_t rank1_updates; /* space-projection steps run                    */
+  int64_t rebases;       /* rebases triggered inside this call            */
+  int64_t eager_folds;   /* rank change / ill-conditioned folds           */
+  int64_t push_rounds;   /* frontier rounds of the PPR push               */
+  int64_t pushes;        /* rows pushed                                   */
+} damf_apply_stats;
+
+typedef struct damf_diag {
+  int64_t n, k, d, arcs;
+  int64_t events_applied, events_since_rebase;
+  double cond_estimate;   /* factor_state.cpp:224-249 (estimator differs) */
+  double proj_row_bound;  /* factor_state.cpp:251-259                      */
+  int64_t total_pushes;   /* enhancer.hpp:41                               */
+  int64_t device_bytes;   /* HBM held by the handle                        */
+} damf_diag;
+
+typedef struct damf_gpu damf_gpu; /* opaque handle: owns all device memory */
+
+/* Engine(g, fs, es, cfg, 0, 0) with fs = FactorState(xb, yb, px, py, sigma, d)
+ * (factor_state.hpp:22-23, engine.hpp:32-34) followed by
+ * EnhancerState::init_propagate (enhancer.cpp:26-47). xb/yb: n x k fp32
+ * row-major host arrays; px/py: k x k fp64; sigma: k fp64, nonincreasing. */
+int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int64_t k,
+                                 const float* xb_host, const float* yb_host,
+                                 const double* px_host, const double* py_host,
+                                 const double* sigma_host, damf_gpu** out);
+
+/* Engine(g, cfg) (engine.cpp:5-10): randomized t-SVD init on device.
+ * Not yet implemented on the GPU: returns DAMF_E_UNSUPPORTED. */
+int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out);
+
+void damf_gpu_destroy(damf_gpu* h);
+const char* damf_gpu_last_error(const damf_gpu* h);
+int damf_gpu_sync(damf_gpu* h);
+
+/* Engine::apply (engine.cpp:22-41) over a batch, sequentially. On error the
+ * failing index is reported and earlier events stay applied, as with the
+ * reference's per-event throw. stats may be NULL. */
+int damf_gpu_apply(damf_gpu* h, const damf_event_batch* batch, int32_t mode,
+                   damf_apply_stats* stats);
+
+/* Per-event device latency (microseconds) of the last apply with
+ * DAMF_APPLY_TIME_EVENTS: fills min(max, count) values, returns count. */
+int64_t damf_gpu_event_latencies(damf_gpu* h, double* out_us_host, int64_t max);
+
+/* Engine::context/content/enhanced (engine.hpp:45-47) for m rows:
+ * out_host[m x k] fp32 (which = DAMF_X, DAMF_Y or DAMF_Z). */
+int damf_gpu_query_rows(damf_gpu* h, int32_t which, const int64_t* ids_host, int64_t m,
+                        float* out_host);
+
+/* Engine::score (engine.cpp:49-52). */
+int damf_gpu_score(damf_gpu* h, int64_t u, int64_t v, int32_t enhanced, double* out);
+
+/* FactorState::query_all (factor_state.cpp:120-123) / full Z = Z_b P_X:
+ * dst = base(which) * P into a caller buffer of n x k fp32, device or host. */
+int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_device);
+
+/* Raw state download for parity checks (DAMF_XB..DAMF_QY), host buffer of
+ * the natural size/type (fp32 for row matrices, fp64 for P/Q/sigma). */
+int damf_gpu_get_state(damf_gpu* h, int32_t which, void* out_host);
+
+/* Sorted out-neighbour sets and weighted out-degrees (graph.cpp bookkeeping):
+ * offsets_host[n+1], targets_host[arcs] (sorted per row), degree_host[n]. */
+int damf_gpu_get_graph(damf_gpu* h, int64_t* offsets_host, int32_t* targets_host,
+                       double* degree_host);
+
+/* EnhancerState::init_propagate / push_to_tolerance (enhancer.cpp:26-47,
+ * 98-157). init_propagate resets Z_b = 0, r_b = alpha X_b and pushes. */
+int damf_gpu_ppr_init(damf_gpu* h, damf_apply_stats* stats);
+int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats);
+
+/* Engine::rebase (engine.cpp:43-47). */
+int damf_gpu_rebase(damf_gpu* h);
+
+int damf_gpu_diagnostics(damf_gpu* h, damf_diag* out);
+
+/* Standalone materialisation kernel, Z = X * F (cfg 4): x_dev/z_dev are
+ * n x d fp32 device buffers (may alias for in-place), f_host is d x d fp64.
+ * stream is a cudaStream_t passed as void* (NULL = default stream). The
+ * returned kernel time (ms, CUDA events on that stream) is written to
+ * *ms_out when non-NULL. */
+int damf_materialize_dev(const float* x_dev, int64_t n, int64_t d, const double* f_host,
+                         float* z_dev, void* stream, float* ms_out);
+
+/* Library build info: "sm_100a <git> <flags>". */
+const char* damf_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DAMF_GPU_H_ */

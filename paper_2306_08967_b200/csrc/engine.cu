@@ -1,0 +1,1132 @@
+// Host orchestration of the B200 DAMF hot path behind the C ABI in
+// include/damf_gpu.h. Mirrors damf::Engine (engine.cpp:5-52): graph deltas
+// -> space-projection updates -> enhancer absorb + push -> rebase policy,
+// with all state device-resident and the per-event work in the cluster
+// kernel (event_kernel.cu) and the PPR kernels (ppr.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/damf_gpu.h"
+#include "common.cuh"
+#include "event_kernel.cuh"
+#include "materialize.cuh"
+#include "ppr.cuh"
+
+using namespace dgpu;
+
+namespace {
+
+#define CK(expr)                                                                       \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess) return cuda_fail(h, _e, #expr, __LINE__);                   \
+  } while (0)
+
+template <class T>
+struct Staged {
+  T* h = nullptr;
+  T* d = nullptr;
+  size_t cap = 0;
+  size_t n = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= cap) return cudaSuccess;
+    const size_t nc = std::max<size_t>(want, cap * 2 + 64);
+    T* nh = nullptr;
+    T* nd = nullptr;
+    cudaError_t e = cudaMallocHost(&nh, nc * sizeof(T));
+    if (e != cudaSuccess) return e;
+    e = cudaMalloc(&nd, nc * sizeof(T));
+    if (e != cudaSuccess) return e;
+    if (h && n) std::memcpy(nh, h, n * sizeof(T));  // keep staged content
+    if (h) cudaFreeHost(h);
+    if (d) cudaFree(d);
+    h = nh;
+    d = nd;
+    cap = nc;
+    return cudaSuccess;
+  }
+  void push(const T& v) { h[n++] = v; }
+  cudaError_t upload(cudaStream_t s) {
+    return n ? cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s) : cudaSuccess;
+  }
+  void release() {
+    if (h) cudaFreeHost(h);
+    if (d) cudaFree(d);
+    h = nullptr;
+    d = nullptr;
+  }
+};
+
+// ---- small device kernels ------------------------------------------------
+__global__ void csr_expand_kernel(int64_t n, const int64_t* coff, const int32_t* cids,
+                                  const double* cw, const int64_t* noff, int32_t* nids,
+                                  double* nw, int32_t* cnt, int32_t* cap, int64_t* off) {
+  const int64_t u = (int64_t)blockIdx.x;
+  for (int64_t r = u; r < n; r += gridDim.x) {
+    const int64_t a = coff[r], b = coff[r + 1], o = noff[r];
+    for (int64_t p = a + threadIdx.x; p < b; p += blockDim.x) {
+      nids[o + (p - a)] = cids[p];
+      if (nw) nw[o + (p - a)] = cw ? cw[p] : 1.0;
+    }
+    if (threadIdx.x == 0) {
+      cnt[r] = (int32_t)(b - a);
+      cap[r] = (int32_t)(noff[r + 1] - o);
+      off[r] = o;
+    }
+  }
+}
+
+__global__ void degree_kernel(int64_t n, DevCSR g, double* deg) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0;
+    const int64_t o = g.off[u];
+    const int c = g.cnt[u];
+    if (g.wts)
+      for (int p = 0; p < c; ++p) s += g.wts[o + p];
+    else
+      s = (double)c;
+    deg[u] = s;
+  }
+}
+
+// In-place Gauss-Jordan inverse with partial pivoting of a k x k fp64
+// matrix (ld), one CTA; used once at creation for P^-1.
+__global__ void gj_inverse_kernel(double* A, double* Inv, int k, int ld, int* singular) {
+  __shared__ int piv;
+  __shared__ double pval;
+  for (int x = threadIdx.x; x < k * k; x += blockDim.x) {
+    const int i = x / k, j = x % k;
+    Inv[(int64_t)i * ld + j] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int c = 0; c < k; ++c) {
+    if (threadIdx.x == 0) {
+      int p = c;
+      double best = fabs(A[(int64_t)c * ld + c]);
+      for (int r = c + 1; r < k; ++r)
+        if (fabs(A[(int64_t)r * ld + c]) > best) {
+          best = fabs(A[(int64_t)r * ld + c]);
+          p = r;
+        }
+      piv = p;
+      pval = A[(int64_t)p * ld + c];
+      if (best == 0.0) *singular = 1;
+    }
+    __syncthreads();
+    if (pval == 0.0) return;
+    if (piv != c)
+      for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        double t = A[(int64_t)c * ld + j];
+        A[(int64_t)c * ld + j] = A[(int64_t)piv * ld + j];
+        A[(int64_t)piv * ld + j] = t;
+        t = Inv[(int64_t)c * ld + j];
+        Inv[(int64_t)c * ld + j] = Inv[(int64_t)piv * ld + j];
+        Inv[(int64_t)piv * ld + j] = t;
+      }
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      A[(int64_t)c * ld + j] /= pval;
+      Inv[(int64_t)c * ld + j] /= pval;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < k * k; x += blockDim.x) {
+      const int r = x / k, j = x % k;
+      if (r == c) continue;
+      const double f = A[(int64_t)r * ld + c];
+      if (j != c) A[(int64_t)r * ld + j] -= f * A[(int64_t)c * ld + j];
+      Inv[(int64_t)r * ld + j] -= f * Inv[(int64_t)c * ld + j];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < k; r += blockDim.x)
+      if (r != c) A[(int64_t)r * ld + c] = 0.0;
+    __syncthreads();
+  }
+}
+
+__global__ void transpose_kernel(const double* A, double* B, int k, int ld) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < k * k; x += gridDim.x * blockDim.x) {
+    const int i = x / k, j = x % k;
+    B[(int64_t)j * ld + i] = A[(int64_t)i * ld + j];
+  }
+}
+
+__global__ void identity_kernel(double* A, int k, int ld) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < k * ld; x += gridDim.x * blockDim.x) {
+    const int i = x / ld, j = x % ld;
+    A[x] = (i == j && j < k) ? 1.0 : 0.0;
+  }
+}
+
+// out[q][j] = sum_i base[ids[q]][i] * P[i][j] (P given as PT), fp64 accumulation.
+__global__ void query_rows_kernel(const float* base, int d, const double* PT, int ld, int k,
+                                  const int64_t* ids, int64_t m, float* out, double* out64) {
+  for (int64_t q = blockIdx.x; q < m; q += gridDim.x) {
+    const int64_t r = ids[q];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      double s = 0;
+      for (int i = 0; i < k; ++i) s += (double)base[r * d + i] * PT[(int64_t)j * ld + i];
+      if (out) out[q * k + j] = (float)s;
+      if (out64) out64[q * k + j] = s;
+    }
+  }
+}
+
+__global__ void pack_rows_kernel(const float* base, int64_t n, int d, int k, float* out) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n * k;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = x / k;
+    const int j = (int)(x % k);
+    out[x] = base[r * d + j];
+  }
+}
+
+
+}  // namespace
+
+struct damf_gpu {
+  damf_config cfg{};
+  int d = 0, ld = 0, k = 0;
+  int64_t n = 0, n_cap = 0, arcs = 0;
+  bool alpha1 = false, directed = false;
+  cudaStream_t st = nullptr;
+  int nsm = 148;
+  DevCtl* ctl = nullptr;
+  DevCtl* h_ctl = nullptr;  // pinned
+  float *Xb = nullptr, *Yb = nullptr, *Zb = nullptr, *rb = nullptr, *delta = nullptr,
+        *key = nullptr;
+  int *stamp = nullptr, *mark = nullptr, *listF = nullptr, *listL = nullptr, *blk = nullptr;
+  double* PT[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  double* Q[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  double* sigma = nullptr;
+  DevCSR out{}, in{};
+  double* deg = nullptr;
+  double* ws = nullptr;
+  double* smax = nullptr;
+  long long* pstats = nullptr;  // pushes, rounds, round base
+  long long* h_pstats = nullptr;
+  Staged<EventDesc> ev;
+  Staged<StepDesc> steps;
+  Staged<int64_t> sp_rows, nb_ids, touched;
+  Staged<double> sp_vals, nb_w;
+  unsigned long long *t_begin = nullptr, *t_end = nullptr;
+  size_t t_cap = 0;
+  std::vector<double> lat_us;
+  uint64_t events_applied = 0;
+  int64_t since_rebase = 0;
+  int64_t total_pushes = 0;
+  int round_base = 0;
+  size_t bytes = 0;
+  std::string err;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int cuda_fail(damf_gpu* h, cudaError_t e, const char* what, int line) {
+  if (h) h->err = std::string("CUDA error ") + cudaGetErrorString(e) + " at engine.cu:" +
+                  std::to_string(line) + " (" + what + ")";
+  return DAMF_E_CUDA;
+}
+
+template <class T>
+cudaError_t dalloc(damf_gpu* h, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e == cudaSuccess) {
+    h->allocs.push_back(*p);
+    h->bytes += count * sizeof(T);
+  }
+  return e;
+}
+
+int fail(damf_gpu* h, int code, const std::string& msg) {
+  h->err = msg;
+  return code;
+}
+
+EventKernelArgs event_args(damf_gpu* h) {
+  EventKernelArgs a{};
+  a.ev = h->ev.d;
+  a.steps = h->steps.d;
+  a.sp_rows = h->sp_rows.d;
+  a.sp_vals = h->sp_vals.d;
+  a.nb_ids = h->nb_ids.d;
+  a.nb_w = h->nb_w.d;
+  a.ctl = h->ctl;
+  a.d = h->d;
+  a.ld = h->ld;
+  a.Xb = h->Xb;
+  a.Yb = h->Yb;
+  a.Zb = h->Zb;
+  a.rb = h->rb;
+  a.alpha_is_one = h->alpha1;
+  a.key = h->key;
+  for (int s = 0; s < 2; ++s)
+    for (int p = 0; p < 2; ++p) {
+      a.PT[s][p] = h->PT[s][p];
+      a.Q[s][p] = h->Q[s][p];
+    }
+  a.sigma = h->sigma;
+  a.rebase_cond = h->cfg.rebase_cond;
+  a.out = h->out;
+  a.in = h->in;
+  a.directed = h->directed;
+  a.undirected = h->cfg.undirected;
+  a.deg = h->deg;
+  const size_t m = (size_t)h->ld * h->ld;
+  a.ws_Q1T = h->ws;
+  a.ws_Q2T = h->ws + m;
+  a.ws_ET = h->ws + 2 * m;
+  a.ws_HT = h->ws + 3 * m;
+  a.ws_FT = h->ws + 4 * m;
+  a.ws_GT = h->ws + 5 * m;
+  a.ws_Fi = h->ws + 6 * m;
+  a.ws_Gi = h->ws + 7 * m;
+  return a;
+}
+
+PprArgs ppr_args(damf_gpu* h) {
+  PprArgs a{};
+  a.n = h->n;
+  a.d = h->d;
+  a.k = h->k;
+  a.Xb = h->Xb;
+  a.Zb = h->Zb;
+  a.rb = h->rb;
+  a.delta = h->delta;
+  a.key = h->key;
+  a.stamp = h->stamp;
+  a.mark = h->mark;
+  a.listF = h->listF;
+  a.listL = h->listL;
+  a.blk = h->blk;
+  a.out = h->out;
+  a.in = h->in;
+  a.directed = h->directed;
+  a.deg = h->deg;
+  a.alpha = h->cfg.alpha;
+  a.alpha_eps = h->cfg.alpha * h->cfg.eps;
+  a.smax = h->smax;
+  a.round_base = h->round_base;
+  a.cand = nullptr;
+  a.ncand = -1;
+  a.push_guard = 1000000000LL;  // enhancer.cpp:8
+  a.stats = h->pstats;
+  a.ctl = h->ctl;
+  return a;
+}
+
+int sync_ctl(damf_gpu* h) {
+  CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(h->h_pstats, h->pstats, 3 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->k = h->h_ctl->k;
+  h->round_base = (int)h->h_pstats[2];
+  return 0;
+}
+
+double* live_PT(damf_gpu* h, int side) { return h->PT[side][h->h_ctl->pp[side]]; }
+double* live_Q(damf_gpu* h, int side) { return h->Q[side][h->h_ctl->pp[side]]; }
+
+// PPR push with the current s_max (computed and consumed on the device: no
+// host round trip per event); grid sized to the expected work.
+int run_push(damf_gpu* h, int grid, unsigned long long* t_end) {
+  CK(launch_smax(h->PT[0][0], h->PT[0][1], h->ctl, h->ld, h->smax, h->st));
+  PprArgs a = ppr_args(h);
+  a.t_end = t_end;
+  const int gmax = ppr_push_max_grid(h->nsm);
+  CK(launch_ppr_push(a, std::min(grid, gmax), h->st));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* damf_gpu_version(void) { return "damf_gpu sm_100a (cluster update, SIMT materialise, pull PPR)"; }
+
+const char* damf_gpu_last_error(const damf_gpu* h) { return h ? h->err.c_str() : "null handle"; }
+
+int damf_gpu_sync(damf_gpu* h) {
+  CK(cudaStreamSynchronize(h->st));
+  return 0;
+}
+
+void damf_gpu_destroy(damf_gpu* h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->st);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->h_ctl) cudaFreeHost(h->h_ctl);
+  if (h->h_pstats) cudaFreeHost(h->h_pstats);
+  h->ev.release();
+  h->steps.release();
+  h->sp_rows.release();
+  h->nb_ids.release();
+  h->touched.release();
+  h->sp_vals.release();
+  h->nb_w.release();
+  if (h->t_begin) cudaFree(h->t_begin);
+  if (h->t_end) cudaFree(h->t_end);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out) {
+  (void)g;
+  (void)cfg;
+  *out = nullptr;
+  return DAMF_E_UNSUPPORTED;  // device randomized t-SVD init: SURVEY 8(f)#1
+}
+
+int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int64_t k,
+                                 const float* xb, const float* yb, const double* px,
+                                 const double* py, const double* sigma, damf_gpu** outp) {
+  *outp = nullptr;
+  auto* h = new damf_gpu();
+  h->cfg = *cfg;
+  if (cfg->d < 1 || cfg->d > kMaxD || k < 1 || k > cfg->d) {
+    int r = fail(h, DAMF_E_K_TOO_LARGE, "d must be in [1,256] and 1 <= k <= d");
+    delete h;
+    return r;
+  }
+  h->d = (int)cfg->d;
+  h->ld = ((h->d + 1) + 3) & ~3;
+  h->k = (int)k;
+  h->n = g->n;
+  h->arcs = g->arcs;
+  h->alpha1 = cfg->alpha == 1.0;
+  h->directed = !cfg->undirected;
+  const int64_t extra = cfg->node_capacity > 0 ? cfg->node_capacity
+                                               : std::max<int64_t>(1024, g->n / 16);
+  h->n_cap = g->n + extra;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev);
+  CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+  CK(cudaMallocHost(&h->h_ctl, sizeof(DevCtl)));
+  CK(cudaMallocHost(&h->h_pstats, 4 * sizeof(long long)));
+  const int64_t n = g->n, ncap = h->n_cap, d = h->d, ld = h->ld;
+  // ---- factor state
+  CK(dalloc(h, &h->ctl, 1));
+  CK(dalloc(h, &h->Xb, (size_t)ncap * d));
+  CK(dalloc(h, &h->Yb, (size_t)ncap * d));
+  CK(cudaMemsetAsync(h->Xb, 0, (size_t)ncap * d * 4, h->st));
+  CK(cudaMemsetAsync(h->Yb, 0, (size_t)ncap * d * 4, h->st));
+  CK(cudaMemcpy2DAsync(h->Xb, d * 4, xb, k * 4, k * 4, n, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpy2DAsync(h->Yb, d * 4, yb, k * 4, k * 4, n, cudaMemcpyHostToDevice, h->st));
+  for (int s = 0; s < 2; ++s)
+    for (int p = 0; p < 2; ++p) {
+      CK(dalloc(h, &h->PT[s][p], (size_t)ld * ld));
+      CK(dalloc(h, &h->Q[s][p], (size_t)ld * ld));
+      CK(cudaMemsetAsync(h->PT[s][p], 0, (size_t)ld * ld * 8, h->st));
+      CK(cudaMemsetAsync(h->Q[s][p], 0, (size_t)ld * ld * 8, h->st));
+    }
+  CK(dalloc(h, &h->sigma, (size_t)ld));
+  CK(cudaMemsetAsync(h->sigma, 0, (size_t)ld * 8, h->st));
+  CK(cudaMemcpyAsync(h->sigma, sigma, k * 8, cudaMemcpyHostToDevice, h->st));
+  CK(dalloc(h, &h->ws, (size_t)8 * ld * ld));
+  CK(dalloc(h, &h->smax, 1));
+  CK(dalloc(h, &h->pstats, 4));
+  CK(cudaMemsetAsync(h->pstats, 0, 4 * sizeof(long long), h->st));
+  {
+    // P (row-major k x k on host) -> device, transpose into PT, invert into Q.
+    double* tmp = nullptr;
+    double* tmp2 = nullptr;
+    int* sing = nullptr;
+    CK(cudaMalloc(&tmp, (size_t)ld * ld * 8));
+    CK(cudaMalloc(&tmp2, (size_t)ld * ld * 8));
+    CK(cudaMalloc(&sing, sizeof(int)));
+    for (int s = 0; s < 2; ++s) {
+      const double* p = s == 0 ? px : py;
+      CK(cudaMemsetAsync(sing, 0, sizeof(int), h->st));
+      CK(cudaMemcpy2DAsync(tmp, ld * 8, p, k * 8, k * 8, k, cudaMemcpyHostToDevice, h->st));
+      transpose_kernel<<<64, 256, 0, h->st>>>(tmp, h->PT[s][0], (int)k, (int)ld);
+      CK(cudaMemcpyAsync(tmp2, tmp, (size_t)ld * ld * 8, cudaMemcpyDeviceToDevice, h->st));
+      gj_inverse_kernel<<<1, 256, 0, h->st>>>(tmp2, h->Q[s][0], (int)k, (int)ld, sing);
+      int hs = 0;
+      CK(cudaMemcpyAsync(&hs, sing, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      if (hs) {
+        cudaFree(tmp);
+        cudaFree(tmp2);
+        cudaFree(sing);
+        int r = fail(h, DAMF_E_SINGULAR_PROJECTION, "initial projection matrix is singular");
+        damf_gpu_destroy(h);
+        return r;
+      }
+    }
+    cudaFree(tmp);
+    cudaFree(tmp2);
+    cudaFree(sing);
+  }
+  DevCtl c0{};
+  c0.k = (int)k;
+  c0.rows_x = n;
+  c0.rows_y = n;
+  c0.cond_est = 1.0;
+  *h->h_ctl = c0;
+  CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, h->st));
+  // ---- graph (slack CSR)
+  {
+    const int64_t arcs = g->arcs;
+    std::vector<int64_t> noff(n + 1);
+    int64_t pos = 0;
+    for (int64_t u = 0; u < n; ++u) {
+      noff[u] = pos;
+      const int64_t c = g->offsets[u + 1] - g->offsets[u];
+      pos += c + std::max<int64_t>(4, c >> 3);
+    }
+    noff[n] = pos;
+    const int64_t reserve = cfg->arc_capacity > 0 ? cfg->arc_capacity
+                                                  : std::max<int64_t>(1 << 20, arcs / 4) + 64 * extra;
+    const bool weighted = g->weights != nullptr;
+    for (int side = 0; side < (h->directed ? 2 : 1); ++side) {
+      DevCSR& c = side == 0 ? h->out : h->in;
+      c.pool_size = pos + reserve;
+      CK(dalloc(h, &c.off, (size_t)ncap));
+      CK(dalloc(h, &c.cnt, (size_t)ncap));
+      CK(dalloc(h, &c.cap, (size_t)ncap));
+      CK(dalloc(h, &c.ids, (size_t)c.pool_size));
+      if (weighted) CK(dalloc(h, &c.wts, (size_t)c.pool_size));
+      CK(dalloc(h, &c.pool_top, 1));
+      CK(cudaMemsetAsync(c.cnt, 0, (size_t)ncap * 4, h->st));
+      CK(cudaMemsetAsync(c.cap, 0, (size_t)ncap * 4, h->st));
+    }
+    // out-CSR: compact upload + device expansion into the slack layout
+    auto build = [&](DevCSR& c, const std::vector<int64_t>& coff, const int32_t* cids,
+                     const double* cw, const std::vector<int64_t>& slack_off) -> int {
+      int64_t *d_coff = nullptr, *d_noff = nullptr;
+      int32_t* d_cids = nullptr;
+      double* d_cw = nullptr;
+      CK(cudaMalloc(&d_coff, (n + 1) * 8));
+      CK(cudaMalloc(&d_noff, (n + 1) * 8));
+      CK(cudaMalloc(&d_cids, std::max<int64_t>(arcs, 1) * 4));
+      if (cw) CK(cudaMalloc(&d_cw, std::max<int64_t>(arcs, 1) * 8));
+      CK(cudaMemcpyAsync(d_coff, coff.data(), (n + 1) * 8, cudaMemcpyHostToDevice, h->st));
+      CK(cudaMemcpyAsync(d_noff, slack_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, h->st));
+      if (arcs) CK(cudaMemcpyAsync(d_cids, cids, arcs * 4, cudaMemcpyHostToDevice, h->st));
+      if (cw && arcs) CK(cudaMemcpyAsync(d_cw, cw, arcs * 8, cudaMemcpyHostToDevice, h->st));
+      if (n > 0)
+        csr_expand_kernel<<<(int)std::min<int64_t>(n, 65535), 128, 0, h->st>>>(
+            n, d_coff, d_cids, d_cw, d_noff, c.ids, c.wts, c.cnt, c.cap, c.off);
+      CK(cudaGetLastError());
+      int64_t top = slack_off[n];
+      CK(cudaMemcpyAsync(c.pool_top, &top, 8, cudaMemcpyHostToDevice, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      cudaFree(d_coff);
+      cudaFree(d_noff);
+      cudaFree(d_cids);
+      if (d_cw) cudaFree(d_cw);
+      return 0;
+    };
+    std::vector<int64_t> coff(g->offsets, g->offsets + n + 1);
+    if (int r = build(h->out, coff, g->targets, g->weights, noff)) return r;
+    if (h->directed) {
+      // in-CSR by counting transpose (host; directed graphs are the small
+      // reference-test configurations)
+      std::vector<int64_t> ioff(n + 1, 0);
+      for (int64_t p = 0; p < arcs; ++p) ioff[g->targets[p] + 1]++;
+      for (int64_t u = 0; u < n; ++u) ioff[u + 1] += ioff[u];
+      std::vector<int32_t> iids(std::max<int64_t>(arcs, 1));
+      std::vector<double> iw(weighted ? std::max<int64_t>(arcs, 1) : 0);
+      std::vector<int64_t> fill(ioff.begin(), ioff.end() - 1);
+      for (int64_t u = 0; u < n; ++u)
+        for (int64_t p = g->offsets[u]; p < g->offsets[u + 1]; ++p) {
+          const int64_t at = fill[g->targets[p]]++;
+          iids[at] = (int32_t)u;
+          if (weighted) iw[at] = g->weights[p];
+        }
+      std::vector<int64_t> inoff(n + 1);
+      int64_t ip = 0;
+      for (int64_t u = 0; u < n; ++u) {
+        inoff[u] = ip;
+        const int64_t c = ioff[u + 1] - ioff[u];
+        ip += c + std::max<int64_t>(4, c >> 3);
+      }
+      inoff[n] = ip;
+      if (int r = build(h->in, ioff, iids.data(), weighted ? iw.data() : nullptr, inoff)) return r;
+    } else {
+      h->in = h->out;
+    }
+    CK(dalloc(h, &h->deg, (size_t)ncap));
+    CK(cudaMemsetAsync(h->deg, 0, (size_t)ncap * 8, h->st));
+    degree_kernel<<<h->nsm * 4, 256, 0, h->st>>>(n, h->out, h->deg);
+    CK(cudaGetLastError());
+  }
+  // ---- enhancer (enhancer.cpp:26-47)
+  if (h->alpha1) {
+    h->Zb = h->Xb;  // Z_b mirrors X_b bit for bit
+  } else {
+    CK(dalloc(h, &h->Zb, (size_t)ncap * d));
+    CK(dalloc(h, &h->rb, (size_t)ncap * d));
+    CK(dalloc(h, &h->delta, (size_t)ncap * d));
+    CK(dalloc(h, &h->key, (size_t)ncap));
+    CK(dalloc(h, &h->stamp, (size_t)ncap));
+    CK(dalloc(h, &h->mark, (size_t)ncap));
+    CK(dalloc(h, &h->listF, (size_t)ncap));
+    CK(dalloc(h, &h->listL, (size_t)ncap));
+    CK(dalloc(h, &h->blk, (size_t)4096));
+    CK(cudaMemsetAsync(h->Zb, 0, (size_t)ncap * d * 4, h->st));
+    CK(cudaMemsetAsync(h->rb, 0, (size_t)ncap * d * 4, h->st));
+    CK(cudaMemsetAsync(h->key, 0, (size_t)ncap * 4, h->st));
+    CK(cudaMemsetAsync(h->stamp, 0, (size_t)ncap * 4, h->st));
+    CK(cudaMemsetAsync(h->mark, 0, (size_t)ncap * 4, h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+  *outp = h;
+  if (!h->alpha1) {
+    damf_apply_stats s{};
+    int r = damf_gpu_ppr_init(h, &s);
+    if (r) {
+      *outp = nullptr;
+      damf_gpu_destroy(h);
+      return r;
+    }
+  }
+  return 0;
+}
+
+int damf_gpu_ppr_init(damf_gpu* h, damf_apply_stats* stats) {
+  if (h->alpha1) return 0;
+  if (int r = sync_ctl(h)) return r;
+  PprArgs a = ppr_args(h);
+  CK(launch_ppr_init(a, h->nsm, h->st));
+  CK(launch_ppr_keys(a, h->nsm, h->st));
+  const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
+  if (int r = run_push(h, 1 << 20, nullptr)) return r;
+  if (int r = sync_ctl(h)) return r;
+  if (h->h_ctl->err) return fail(h, h->h_ctl->err, "push_to_tolerance: push budget exceeded");
+  if (stats) {
+    stats->pushes = h->h_pstats[0] - p0;
+    stats->push_rounds = h->h_pstats[1] - r0;
+  }
+  return 0;
+}
+
+int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
+  if (h->alpha1) return 0;
+  if (int r = sync_ctl(h)) return r;
+  const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
+  if (int r = run_push(h, 1 << 20, nullptr)) return r;
+  if (int r = sync_ctl(h)) return r;
+  if (h->h_ctl->err) return fail(h, h->h_ctl->err, "push_to_tolerance: push budget exceeded");
+  if (stats) {
+    stats->pushes = h->h_pstats[0] - p0;
+    stats->push_rounds = h->h_pstats[1] - r0;
+  }
+  return 0;
+}
+
+int damf_gpu_rebase(damf_gpu* h) {
+  if (int r = sync_ctl(h)) return r;
+  const int k = h->k, d = h->d, ld = h->ld;
+  float* tmp = nullptr;
+  if (k > 128) CK(cudaMalloc(&tmp, (size_t)h->n * d * 4));
+  auto fold = [&](float* base, const double* PT) -> int {
+    if (!tmp) {
+      CK(launch_materialize(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
+    } else {
+      CK(launch_materialize(base, h->n, k, d, PT, ld, k, tmp, d, h->st, h->nsm));
+      CK(cudaMemcpyAsync(base, tmp, (size_t)h->n * d * 4, cudaMemcpyDeviceToDevice, h->st));
+    }
+    return 0;
+  };
+  if (int r = fold(h->Xb, live_PT(h, 0))) return r;
+  if (int r = fold(h->Yb, live_PT(h, 1))) return r;
+  if (!h->alpha1) {
+    if (int r = fold(h->Zb, live_PT(h, 0))) return r;
+    if (int r = fold(h->rb, live_PT(h, 0))) return r;
+  }
+  for (int s = 0; s < 2; ++s) {
+    identity_kernel<<<64, 256, 0, h->st>>>(live_PT(h, s), k, ld);
+    identity_kernel<<<64, 256, 0, h->st>>>(live_Q(h, s), k, ld);
+  }
+  CK(cudaGetLastError());
+  if (!h->alpha1) CK(launch_ppr_keys(ppr_args(h), h->nsm, h->st));
+  h->h_ctl->cond_est = 1.0;
+  h->h_ctl->need_rebase = 0;
+  CK(cudaMemcpyAsync(&h->ctl->cond_est, &h->h_ctl->cond_est, sizeof(double), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(&h->ctl->need_rebase, &h->h_ctl->need_rebase, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (tmp) cudaFree(tmp);
+  h->since_rebase = 0;
+  return 0;
+}
+
+int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_apply_stats* stats) {
+  damf_apply_stats s{};
+  s.failed_index = -1;
+  const int64_t count = b->count;
+  // ---- host validation and descriptor build (graph.cpp:83-207 semantics)
+  CK(h->ev.ensure(count + 1));
+  CK(h->steps.ensure(2 * count + 2));
+  h->ev.n = h->steps.n = h->sp_rows.n = h->sp_vals.n = h->nb_ids.n = h->nb_w.n = h->touched.n = 0;
+  int64_t nn = h->n;
+  int64_t ok_count = count;
+  int vstatus = 0;
+  std::string vmsg;
+  std::vector<std::pair<int64_t, double>> inl, outl;
+  for (int64_t i = 0; i < count && !vstatus; ++i) {
+    const int kind = b->kind[i];
+    EventDesc e{};
+    e.kind = kind;
+    e.step0 = (int64_t)h->steps.n;
+    e.touched_off = (int64_t)h->touched.n;
+    auto need = [&](size_t rows, size_t nbs, size_t tch) -> cudaError_t {
+      cudaError_t x = h->sp_rows.ensure(h->sp_rows.n + rows + 2);
+      if (x == cudaSuccess) x = h->sp_vals.ensure(h->sp_vals.n + rows + 2);
+      if (x == cudaSuccess) x = h->nb_ids.ensure(h->nb_ids.n + nbs + 2);
+      if (x == cudaSuccess) x = h->nb_w.ensure(h->nb_w.n + nbs + 2);
+      if (x == cudaSuccess) x = h->touched.ensure(h->touched.n + tch + 2);
+      return x;
+    };
+    if (kind == DAMF_ADD_EDGE || kind == DAMF_REMOVE_EDGE) {
+      const int64_t u = b->u[i], v = b->v[i];
+      const double w = (kind == DAMF_ADD_EDGE && b->w) ? b->w[i] : 1.0;
+      if (u < 0 || u >= nn || v < 0 || v >= nn) {
+        vstatus = DAMF_E_UNKNOWN_NODE;
+        vmsg = "unknown node " + std::to_string(u < 0 || u >= nn ? u : v);
+        ok_count = i;
+        break;
+      }
+      if (kind == DAMF_ADD_EDGE && !(w > 0.0)) {
+        vstatus = DAMF_E_PARSE;
+        vmsg = "AddEdge: weight must be > 0";
+        ok_count = i;
+        break;
+      }
+      CK(need(2, 0, 2));
+      const bool two = h->cfg.undirected && u != v;
+      e.u = u;
+      e.v = v;
+      e.w = w;
+      e.nsteps = two ? 2 : 1;
+      const double cv = kind == DAMF_ADD_EDGE ? w : -1.0;  // removal weight patched on device
+      for (int q = 0; q < e.nsteps; ++q) {
+        StepDesc sd{};
+        sd.kind = kStepEdge;
+        sd.nb = 1;
+        sd.b_off = (int64_t)h->sp_rows.n;
+        h->sp_rows.push(q == 0 ? u : v);
+        h->sp_vals.push(1.0);
+        sd.c_row = q == 0 ? v : u;
+        sd.c_val = cv;
+        sd.n_a = nn;
+        sd.n_b = nn;
+        sd.bnorm2 = 1.0;
+        h->steps.push(sd);
+      }
+      h->touched.push(u);
+      if (two) h->touched.push(v);
+    } else if (kind == DAMF_ADD_NODE) {
+      inl.clear();
+      outl.clear();
+      if (b->in_off)
+        for (int64_t t = b->in_off[i]; t < b->in_off[i + 1]; ++t)
+          inl.emplace_back(b->in_ids[t], b->in_w ? b->in_w[t] : 1.0);
+      if (b->out_off)
+        for (int64_t t = b->out_off[i]; t < b->out_off[i + 1]; ++t)
+          outl.emplace_back(b->out_ids[t], b->out_w ? b->out_w[t] : 1.0);
+      // touched_by (graph.cpp:199-204): in sources (+ out targets), new id last
+      std::vector<int64_t> tch;
+      auto addt = [&](int64_t x) {
+        if (std::find(tch.begin(), tch.end(), x) == tch.end()) tch.push_back(x);
+      };
+      for (auto& p : inl) addt(p.first);
+      if (h->cfg.undirected)
+        for (auto& p : outl) addt(p.first);
+      addt(nn);
+      if (h->cfg.undirected) {  // graph.cpp:137-141
+        for (auto& p : outl) inl.push_back(p);
+        outl = inl;
+      }
+      for (auto& p : inl)
+        if (p.first < 0 || p.first >= nn || !(p.second > 0.0)) {
+          vstatus = (p.first < 0 || p.first >= nn) ? DAMF_E_UNKNOWN_NODE : DAMF_E_PARSE;
+          vmsg = "AddNode: bad neighbour";
+        }
+      for (auto& p : outl)
+        if (p.first < 0 || p.first >= nn || !(p.second > 0.0)) {
+          vstatus = (p.first < 0 || p.first >= nn) ? DAMF_E_UNKNOWN_NODE : DAMF_E_PARSE;
+          vmsg = "AddNode: bad neighbour";
+        }
+      if (nn + 1 > h->n_cap) {
+        vstatus = DAMF_E_TOO_LARGE;
+        vmsg = "node capacity exhausted (damf_config.node_capacity)";
+      }
+      if (vstatus) {
+        ok_count = i;
+        break;
+      }
+      CK(need(inl.size() + outl.size(), inl.size() + outl.size(), tch.size()));
+      e.u = nn;
+      e.in_off = (int64_t)h->nb_ids.n;
+      e.in_cnt = (int64_t)inl.size();
+      for (auto& p : inl) {
+        h->nb_ids.push(p.first);
+        h->nb_w.push(p.second);
+      }
+      e.out_off = (int64_t)h->nb_ids.n;
+      e.out_cnt = (int64_t)outl.size();
+      for (auto& p : outl) {
+        h->nb_ids.push(p.first);
+        h->nb_w.push(p.second);
+      }
+      auto sorted_in = inl, sorted_out = outl;
+      std::sort(sorted_in.begin(), sorted_in.end());
+      std::sort(sorted_out.begin(), sorted_out.end());
+      // column step (update_embedding_n, u_is_x = true)
+      StepDesc c{};
+      c.kind = kStepNodeCol;
+      c.nb = (int32_t)sorted_in.size();
+      c.b_off = (int64_t)h->sp_rows.n;
+      double b2 = 0;
+      for (auto& p : sorted_in) {
+        h->sp_rows.push(p.first);
+        h->sp_vals.push(p.second);
+        b2 += p.second * p.second;
+      }
+      c.bnorm2 = b2;
+      c.c_row = nn;  // new Y row
+      c.n_a = nn;
+      c.n_b = nn;
+      h->steps.push(c);
+      // row step (u_is_x = false): b over Y rows (now nn + 1)
+      StepDesc r{};
+      r.kind = kStepNodeRow;
+      r.nb = (int32_t)sorted_out.size();
+      r.b_off = (int64_t)h->sp_rows.n;
+      b2 = 0;
+      for (auto& p : sorted_out) {
+        h->sp_rows.push(p.first);
+        h->sp_vals.push(p.second);
+        b2 += p.second * p.second;
+      }
+      r.bnorm2 = b2;
+      r.c_row = nn;  // new X row
+      r.n_a = nn + 1;
+      r.n_b = nn;
+      h->steps.push(r);
+      e.nsteps = 2;
+      for (int64_t x : tch) h->touched.push(x);
+      ++nn;
+    } else {
+      vstatus = DAMF_E_PARSE;
+      vmsg = "unknown event kind";
+      ok_count = i;
+      break;
+    }
+    e.touched_cnt = (int64_t)h->touched.n - e.touched_off;
+    h->ev.push(e);
+  }
+  // ---- upload
+  CK(h->ev.upload(h->st));
+  CK(h->steps.upload(h->st));
+  CK(h->sp_rows.upload(h->st));
+  CK(h->sp_vals.upload(h->st));
+  CK(h->nb_ids.upload(h->st));
+  CK(h->nb_w.upload(h->st));
+  CK(h->touched.upload(h->st));
+  const bool timing = mode & DAMF_APPLY_TIME_EVENTS;
+  if (timing && (size_t)ok_count > h->t_cap) {
+    if (h->t_begin) cudaFree(h->t_begin);
+    if (h->t_end) cudaFree(h->t_end);
+    h->t_cap = (size_t)ok_count + 1024;
+    CK(cudaMalloc(&h->t_begin, h->t_cap * 8));
+    CK(cudaMalloc(&h->t_end, h->t_cap * 8));
+  }
+  if (int r = sync_ctl(h)) return r;
+  const long long rank1_0 = h->h_ctl->rank1, folds0 = h->h_ctl->folds;
+  const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
+  EventKernelArgs ea = event_args(h);
+  ea.mode = mode;
+  ea.t_begin = timing ? h->t_begin : nullptr;
+  ea.t_end = timing ? h->t_end : nullptr;
+  const bool ppr = !h->alpha1;
+  const bool push_each = ppr && !(mode & DAMF_APPLY_DEFER_PUSH);
+  int64_t rebases = 0;
+  int64_t i = 0;
+  int64_t n_before = h->n;
+  while (i < ok_count) {
+    // events up to the next rebase_every boundary (engine.cpp:37-40)
+    int64_t j = ok_count;
+    if (h->cfg.rebase_every > 0) j = std::min<int64_t>(j, i + (h->cfg.rebase_every - h->since_rebase));
+    if (!ppr) {
+      ea.e_begin = i;
+      ea.e_end = j;
+      CK(launch_event_kernel(ea, h->st));
+    } else {
+      for (int64_t e = i; e < j; ++e) {
+        ea.e_begin = e;
+        ea.e_end = e + 1;
+        CK(launch_event_kernel(ea, h->st));
+        // rows appended by AddNode are visible to the enhancer from here
+        const EventDesc& ed = h->ev.h[e];
+        if (ed.kind == DAMF_ADD_NODE) h->n = ed.u + 1;
+        PprArgs pa = ppr_args(h);
+        pa.k = h->k;
+        CK(launch_ppr_absorb(pa, h->touched.d + ed.touched_off, (int)ed.touched_cnt, h->st));
+        if (push_each) {
+          if (int r = run_push(h, 8 * h->nsm, timing ? h->t_end + e : nullptr)) return r;
+        }
+      }
+    }
+    for (int64_t e = i; e < j; ++e)
+      if (h->ev.h[e].kind == DAMF_ADD_NODE) h->n = h->ev.h[e].u + 1;
+    if (int r = sync_ctl(h)) return r;
+    if (h->h_ctl->err) break;
+    h->events_applied += (uint64_t)(j - i);
+    h->since_rebase += (j - i);
+    if (h->cfg.rebase_every > 0 && h->since_rebase >= h->cfg.rebase_every) {
+      if (int r = damf_gpu_rebase(h)) return r;
+      ++rebases;
+    }
+    i = j;
+  }
+  if (int r = sync_ctl(h)) return r;
+  int status = 0;
+  if (h->h_ctl->err) {
+    const int64_t fe = h->h_ctl->err_event;
+    status = h->h_ctl->err;
+    s.failed_index = fe;
+    // events before fe were applied; rewind the node count to the device view
+    h->n = n_before;
+    for (int64_t e = 0; e < fe; ++e)
+      if (h->ev.h[e].kind == DAMF_ADD_NODE) h->n = h->ev.h[e].u + 1;
+    h->err = status == DAMF_E_DUPLICATE_EDGE ? "AddEdge: edge already present"
+             : status == DAMF_E_MISSING_EDGE ? "RemoveEdge: edge not present"
+             : status == DAMF_E_NON_CONVERGENCE ? "push_to_tolerance: push budget exceeded"
+                                                : "event failed on device";
+    for (int64_t e2 = 0; e2 < fe; ++e2) (void)e2;
+    h->events_applied += (uint64_t)std::max<int64_t>(0, fe - i);
+    h->since_rebase += std::max<int64_t>(0, fe - i);
+    // clear the device error for subsequent calls
+    h->h_ctl->err = 0;
+    CK(cudaMemcpyAsync(&h->ctl->err, &h->h_ctl->err, sizeof(int), cudaMemcpyHostToDevice, h->st));
+    s.applied = fe;
+  } else {
+    s.applied = ok_count;
+    if (vstatus) {
+      status = vstatus;
+      s.failed_index = ok_count;
+      h->err = vmsg;
+    }
+  }
+  // deferred cond-triggered rebase (engine.cpp:38-40; query-transparent)
+  if (!status && h->h_ctl->need_rebase) {
+    if (int r = damf_gpu_rebase(h)) return r;
+    ++rebases;
+  }
+  if (timing) {
+    const int64_t m = s.applied;
+    std::vector<unsigned long long> tb(m), te(m);
+    if (m) {
+      CK(cudaMemcpy(tb.data(), h->t_begin, m * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(te.data(), h->t_end, m * 8, cudaMemcpyDeviceToHost));
+    }
+    h->lat_us.resize(m);
+    for (int64_t e = 0; e < m; ++e) h->lat_us[e] = (double)(te[e] - tb[e]) * 1e-3;
+  }
+  s.rank1_updates = h->h_ctl->rank1 - rank1_0;
+  s.eager_folds = h->h_ctl->folds - folds0;
+  s.rebases = rebases;
+  s.pushes = h->h_pstats[0] - p0;
+  s.push_rounds = h->h_pstats[1] - r0;
+  h->total_pushes = h->h_pstats[0];
+  if (stats) *stats = s;
+  return status;
+}
+
+int64_t damf_gpu_event_latencies(damf_gpu* h, double* out, int64_t max) {
+  const int64_t m = (int64_t)h->lat_us.size();
+  for (int64_t i = 0; i < std::min(m, max); ++i) out[i] = h->lat_us[i];
+  return m;
+}
+
+int damf_gpu_query_rows(damf_gpu* h, int32_t which, const int64_t* ids, int64_t m, float* out) {
+  if (int r = sync_ctl(h)) return r;
+  for (int64_t q = 0; q < m; ++q)
+    if (ids[q] < 0 || ids[q] >= h->n) return fail(h, DAMF_E_UNKNOWN_NODE, "query: unknown node " + std::to_string(ids[q]));
+  const float* base = which == DAMF_Y ? h->Yb : which == DAMF_Z ? h->Zb : h->Xb;
+  const double* PT = live_PT(h, which == DAMF_Y ? 1 : 0);
+  int64_t* dids = nullptr;
+  float* dout = nullptr;
+  CK(cudaMalloc(&dids, std::max<int64_t>(m, 1) * 8));
+  CK(cudaMalloc(&dout, std::max<int64_t>(m, 1) * h->k * 4));
+  CK(cudaMemcpyAsync(dids, ids, m * 8, cudaMemcpyHostToDevice, h->st));
+  query_rows_kernel<<<(int)std::min<int64_t>(std::max<int64_t>(m, 1), 4096), 128, 0, h->st>>>(
+      base, h->d, PT, h->ld, h->k, dids, m, dout, nullptr);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, dout, m * h->k * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(dids);
+  cudaFree(dout);
+  return 0;
+}
+
+int damf_gpu_score(damf_gpu* h, int64_t u, int64_t v, int32_t enhanced, double* out) {
+  if (int r = sync_ctl(h)) return r;
+  if (u < 0 || u >= h->n || v < 0 || v >= h->n) return fail(h, DAMF_E_UNKNOWN_NODE, "score: unknown node");
+  int64_t ids[2] = {u, v};
+  int64_t* dids = nullptr;
+  double* dout = nullptr;
+  CK(cudaMalloc(&dids, 16));
+  CK(cudaMalloc(&dout, 2 * h->k * 8));
+  CK(cudaMemcpyAsync(dids, ids, 16, cudaMemcpyHostToDevice, h->st));
+  query_rows_kernel<<<1, 128, 0, h->st>>>(enhanced ? h->Zb : h->Xb, h->d, live_PT(h, 0), h->ld, h->k,
+                                          dids, 1, nullptr, dout);
+  query_rows_kernel<<<1, 128, 0, h->st>>>(h->Yb, h->d, live_PT(h, 1), h->ld, h->k, dids + 1, 1,
+                                          nullptr, dout + h->k);
+  CK(cudaGetLastError());
+  std::vector<double> hv(2 * h->k);
+  CK(cudaMemcpyAsync(hv.data(), dout, 2 * h->k * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  double s = 0;
+  for (int j = 0; j < h->k; ++j) s += hv[j] * hv[h->k + j];
+  *out = s;
+  cudaFree(dids);
+  cudaFree(dout);
+  return 0;
+}
+
+int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_device) {
+  if (int r = sync_ctl(h)) return r;
+  const float* base = which == DAMF_Y ? h->Yb : which == DAMF_Z ? h->Zb : h->Xb;
+  const double* PT = live_PT(h, which == DAMF_Y ? 1 : 0);
+  float* out = dst;
+  if (!dst_is_device) CK(cudaMalloc(&out, (size_t)std::max<int64_t>(h->n, 1) * h->k * 4));
+  CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
+  if (!dst_is_device) {
+    CK(cudaMemcpyAsync(dst, out, (size_t)h->n * h->k * 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    cudaFree(out);
+  }
+  CK(cudaStreamSynchronize(h->st));
+  return 0;
+}
+
+int damf_gpu_get_state(damf_gpu* h, int32_t which, void* out) {
+  if (int r = sync_ctl(h)) return r;
+  const int k = h->k, d = h->d, ld = h->ld;
+  switch (which) {
+    case DAMF_XB:
+    case DAMF_YB:
+    case DAMF_ZB:
+    case DAMF_RB: {
+      const float* base = which == DAMF_XB ? h->Xb : which == DAMF_YB ? h->Yb
+                          : which == DAMF_ZB ? h->Zb : h->rb;
+      if (!base) return fail(h, DAMF_E_SHAPE_MISMATCH, "matrix not allocated (alpha == 1)");
+      CK(cudaMemcpy2D(out, k * 4, base, d * 4, k * 4, h->n, cudaMemcpyDeviceToHost));
+      return 0;
+    }
+    case DAMF_PX:
+    case DAMF_PY: {
+      std::vector<double> t((size_t)k * ld);
+      CK(cudaMemcpy(t.data(), live_PT(h, which == DAMF_PY), (size_t)k * ld * 8, cudaMemcpyDeviceToHost));
+      double* o = static_cast<double*>(out);
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) o[i * k + j] = t[(size_t)j * ld + i];
+      return 0;
+    }
+    case DAMF_QX:
+    case DAMF_QY:
+      CK(cudaMemcpy2D(out, k * 8, live_Q(h, which == DAMF_QY), ld * 8, k * 8, k, cudaMemcpyDeviceToHost));
+      return 0;
+    case DAMF_SIGMA:
+      CK(cudaMemcpy(out, h->sigma, k * 8, cudaMemcpyDeviceToHost));
+      return 0;
+    case DAMF_X:
+    case DAMF_Y:
+    case DAMF_Z:
+      return damf_gpu_materialize(h, which, static_cast<float*>(out), 0);
+  }
+  return fail(h, DAMF_E_SHAPE_MISMATCH, "unknown matrix id");
+}
+
+int damf_gpu_get_graph(damf_gpu* h, int64_t* offsets, int32_t* targets, double* degree) {
+  if (int r = sync_ctl(h)) return r;
+  const int64_t n = h->n;
+  std::vector<int64_t> off(n);
+  std::vector<int32_t> cnt(n);
+  CK(cudaMemcpy(off.data(), h->out.off, n * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cnt.data(), h->out.cnt, n * 4, cudaMemcpyDeviceToHost));
+  if (degree) CK(cudaMemcpy(degree, h->deg, n * 8, cudaMemcpyDeviceToHost));
+  int64_t top = 0;
+  CK(cudaMemcpy(&top, h->out.pool_top, 8, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> ids(std::max<int64_t>(top, 1));
+  CK(cudaMemcpy(ids.data(), h->out.ids, top * 4, cudaMemcpyDeviceToHost));
+  int64_t pos = 0;
+  for (int64_t u = 0; u < n; ++u) {
+    if (offsets) offsets[u] = pos;
+    if (targets) {
+      std::copy(ids.begin() + off[u], ids.begin() + off[u] + cnt[u], targets + pos);
+      std::sort(targets + pos, targets + pos + cnt[u]);
+    }
+    pos += cnt[u];
+  }
+  if (offsets) offsets[n] = pos;
+  return 0;
+}
+
+int damf_gpu_diagnostics(damf_gpu* h, damf_diag* o) {
+  if (int r = sync_ctl(h)) return r;
+  o->n = h->n;
+  o->k = h->k;
+  o->d = h->d;
+  int64_t arcs = 0;
+  {
+    std::vector<int32_t> cnt(h->n);
+    CK(cudaMemcpy(cnt.data(), h->out.cnt, h->n * 4, cudaMemcpyDeviceToHost));
+    for (auto c : cnt) arcs += c;
+  }
+  o->arcs = arcs;
+  o->events_applied = (int64_t)h->events_applied;
+  o->events_since_rebase = h->since_rebase;
+  o->cond_estimate = h->h_ctl->cond_est;
+  CK(launch_smax(h->PT[0][0], h->PT[0][1], h->ctl, h->ld, h->smax, h->st));
+  double sm = 0;
+  CK(cudaMemcpy(&sm, h->smax, 8, cudaMemcpyDeviceToHost));
+  o->proj_row_bound = sm;
+  o->total_pushes = h->h_pstats[0];
+  o->device_bytes = (int64_t)h->bytes;
+  return 0;
+}
+
+int damf_materialize_dev(const float* x, int64_t n, int64_t d, const double* f_host, float* z,
+                         void* stream, float* ms_out) {
+  damf_gpu* h = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int ld = (int)d;
+  double* FT = nullptr;
+  std::vector<double> ft((size_t)d * d);
+  for (int64_t i = 0; i < d; ++i)
+    for (int64_t j = 0; j < d; ++j) ft[j * d + i] = f_host[i * d + j];
+  CK(cudaMalloc(&FT, (size_t)d * d * 8));
+  CK(cudaMemcpyAsync(FT, ft.data(), (size_t)d * d * 8, cudaMemcpyHostToDevice, s));
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  CK(launch_materialize(x, n, (int)d, (int)d, FT, ld, (int)d, z, (int)d, s, nsm));
+  cudaEventRecord(e1, s);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  if (ms_out) *ms_out = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(FT);
+  return 0;
+}
+
+}  // extern "C"

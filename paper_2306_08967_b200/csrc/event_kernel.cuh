@@ -1,0 +1,54 @@
+// Host-visible interface of the per-event cluster kernel (event_kernel.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace dgpu {
+
+constexpr int kEventThreads = 256;
+
+struct EventKernelArgs {
+  // batch
+  const EventDesc* ev;
+  int64_t e_begin, e_end;
+  StepDesc* steps;
+  const int64_t* sp_rows;   // sparse b rows
+  const double* sp_vals;    // sparse b values
+  const int64_t* nb_ids;    // AddNode neighbour ids (flat)
+  const double* nb_w;       // AddNode neighbour weights
+  unsigned long long* t_begin;  // per-event %globaltimer stamps (or null)
+  unsigned long long* t_end;
+  int mode;                 // DAMF_APPLY_* bits
+  // factor state
+  DevCtl* ctl;
+  int d, ld;
+  float* Xb;
+  float* Yb;
+  float* Zb;
+  float* rb;
+  float* key;  // enhancer residual keys (refreshed on folds)
+  int alpha_is_one;
+  double* PT[2][2];  // [side X/Y][ping-pong]  P transposed
+  double* Q[2][2];   // [side][ping-pong]      P^-1
+  double* sigma;
+  double rebase_cond;
+  // graph
+  DevCSR out, in;
+  int directed, undirected;
+  double* deg;
+  // workspace (fp64, ld x ld each)
+  double* ws_Q1T;
+  double* ws_Q2T;
+  double* ws_ET;
+  double* ws_HT;
+  double* ws_FT;
+  double* ws_GT;
+  double* ws_Fi;
+  double* ws_Gi;
+};
+
+cudaError_t launch_event_kernel(const EventKernelArgs& a, cudaStream_t s);
+int event_cluster_size();
+size_t event_kernel_smem(int C);
+
+}  // namespace dgpu

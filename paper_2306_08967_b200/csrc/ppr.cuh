@@ -1,0 +1,42 @@
+#pragma once
+#include "common.cuh"
+
+namespace dgpu {
+
+struct PprArgs {
+  int64_t n;
+  int d, k;
+  const float* Xb;
+  float* Zb;
+  float* rb;
+  float* delta;
+  float* key;
+  int* stamp;
+  int* mark;
+  int* listF;
+  int* listL;
+  int* blk;
+  DevCSR out, in;
+  int directed;
+  double* deg;
+  double alpha;
+  double alpha_eps;   // alpha*eps (enhancer.cpp:104)
+  const double* smax; // device s_max = proj_row_bound(P_X); push when key > alpha_eps/s_max
+  int round_base;
+  const int* cand;    // candidate rows for the first frontier (ncand >= 0)
+  int ncand;          // -1: scan all rows
+  long long push_guard;
+  long long* stats;   // [pushes, rounds, next round base]
+  unsigned long long* t_end;
+  DevCtl* ctl;
+};
+
+cudaError_t launch_ppr_push(const PprArgs& a, int grid, cudaStream_t s);
+int ppr_push_max_grid(int nsm);
+cudaError_t launch_ppr_absorb(const PprArgs& a, const int64_t* rows, int nrows, cudaStream_t s);
+cudaError_t launch_ppr_keys(const PprArgs& a, int nsm, cudaStream_t s);
+cudaError_t launch_ppr_init(const PprArgs& a, int nsm, cudaStream_t s);
+cudaError_t launch_smax(const double* PT0, const double* PT1, const DevCtl* ctl, int ld,
+                        double* out, cudaStream_t s);
+
+}  // namespace dgpu

@@ -1,0 +1,275 @@
+"""Python binding of the B200 DAMF hot path (ctypes over include/damf_gpu.h).
+
+`Engine` mirrors damf::Engine (/root/reference/proj/include/damf/engine.hpp:
+26-61): apply(events), context/content/enhanced(u), score(u, v), rebase(),
+plus query_all-style materialisation and the PPR entry points. Everything
+runs in libdamf_gpu.so on the GPU; there is no CPU fallback — importing this
+module on a machine without the built library or without a GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdamf_gpu.so")
+
+i64p = C.POINTER(C.c_int64)
+i32p = C.POINTER(C.c_int32)
+f64p = C.POINTER(C.c_double)
+f32p = C.POINTER(C.c_float)
+
+# status codes: damf::Error::Kind ordinal + 1 (types.hpp:21-41)
+ERROR_KINDS = ["ParseError", "UnknownNode", "DuplicateEdge", "MissingEdge", "ShapeMismatch",
+               "ZeroMatrix", "NonFinite", "SingularProjection", "NonConvergence",
+               "DegenerateLabels", "KTooLarge", "GraphTooSmall", "TooLarge", "IoError"]
+ADD_NODE, ADD_EDGE, REMOVE_EDGE = 0, 1, 2
+XB, YB, PX, PY, SIGMA, ZB, RB, X, Y, Z, QX, QY = range(12)
+APPLY_GRAPH_AND_PPR_ONLY, APPLY_DEFER_PUSH, APPLY_TIME_EVENTS = 1, 2, 4
+
+
+class DamfError(RuntimeError):
+    """Carries the reference's Error::Kind (types.hpp:21-41)."""
+
+    def __init__(self, status, msg, index=-1):
+        kind = ERROR_KINDS[status - 1] if 1 <= status <= len(ERROR_KINDS) else (
+            "CudaError" if status == 100 else "Unsupported" if status == 101 else str(status))
+        super().__init__(f"{kind}: {msg}" + (f" (event {index})" if index >= 0 else ""))
+        self.status = status
+        self.kind = kind
+        self.index = index
+
+
+class Config(C.Structure):
+    _fields_ = [("d", C.c_int64), ("alpha", C.c_double), ("eps", C.c_double),
+                ("seed", C.c_uint64), ("rebase_cond", C.c_double), ("rebase_every", C.c_int64),
+                ("undirected", C.c_int32), ("flags", C.c_int32), ("node_capacity", C.c_int64),
+                ("arc_capacity", C.c_int64)]
+
+
+class Csr(C.Structure):
+    _fields_ = [("n", C.c_int64), ("arcs", C.c_int64), ("offsets", i64p), ("targets", i32p),
+                ("weights", f64p)]
+
+
+class EventBatch(C.Structure):
+    _fields_ = [("count", C.c_int64), ("kind", i32p), ("u", i64p), ("v", i64p), ("w", f64p),
+                ("in_off", i64p), ("in_ids", i64p), ("in_w", f64p), ("out_off", i64p),
+                ("out_ids", i64p), ("out_w", f64p)]
+
+
+class ApplyStats(C.Structure):
+    _fields_ = [("applied", C.c_int64), ("failed_index", C.c_int64),
+                ("rank1_updates", C.c_int64), ("rebases", C.c_int64), ("eager_folds", C.c_int64),
+                ("push_rounds", C.c_int64), ("pushes", C.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Diag(C.Structure):
+    _fields_ = [("n", C.c_int64), ("k", C.c_int64), ("d", C.c_int64), ("arcs", C.c_int64),
+                ("events_applied", C.c_int64), ("events_since_rebase", C.c_int64),
+                ("cond_estimate", C.c_double), ("proj_row_bound", C.c_double),
+                ("total_pushes", C.c_int64), ("device_bytes", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdamf_gpu.so; fails loudly when it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built (run `make` or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.damf_gpu_last_error.restype = C.c_char_p
+        L.damf_gpu_last_error.argtypes = [vp]
+        L.damf_gpu_version.restype = C.c_char_p
+        L.damf_gpu_create_from_factors.argtypes = [C.POINTER(Csr), C.POINTER(Config), C.c_int64,
+                                                   f32p, f32p, f64p, f64p, f64p, C.POINTER(vp)]
+        L.damf_gpu_create.argtypes = [C.POINTER(Csr), C.POINTER(Config), C.POINTER(vp)]
+        L.damf_gpu_destroy.argtypes = [vp]
+        L.damf_gpu_sync.argtypes = [vp]
+        L.damf_gpu_apply.argtypes = [vp, C.POINTER(EventBatch), C.c_int32, C.POINTER(ApplyStats)]
+        L.damf_gpu_event_latencies.argtypes = [vp, f64p, C.c_int64]
+        L.damf_gpu_event_latencies.restype = C.c_int64
+        L.damf_gpu_query_rows.argtypes = [vp, C.c_int32, i64p, C.c_int64, f32p]
+        L.damf_gpu_score.argtypes = [vp, C.c_int64, C.c_int64, C.c_int32, f64p]
+        L.damf_gpu_materialize.argtypes = [vp, C.c_int32, vp, C.c_int32]
+        L.damf_gpu_get_state.argtypes = [vp, C.c_int32, vp]
+        L.damf_gpu_get_graph.argtypes = [vp, i64p, i32p, f64p]
+        L.damf_gpu_ppr_init.argtypes = [vp, C.POINTER(ApplyStats)]
+        L.damf_gpu_ppr_push.argtypes = [vp, C.POINTER(ApplyStats)]
+        L.damf_gpu_rebase.argtypes = [vp]
+        L.damf_gpu_diagnostics.argtypes = [vp, C.POINTER(Diag)]
+        L.damf_materialize_dev.argtypes = [vp, C.c_int64, C.c_int64, f64p, vp, vp, f32p]
+        _lib = L
+    return _lib
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+def make_batch(ev):
+    """Build a damf_event_batch from an object with kind/u/v/w/in_*/out_* arrays."""
+    arrs = dict(kind=np.ascontiguousarray(ev.kind, np.int32),
+                u=np.ascontiguousarray(ev.u, np.int64), v=np.ascontiguousarray(ev.v, np.int64),
+                w=np.ascontiguousarray(ev.w, np.float64),
+                in_off=np.ascontiguousarray(ev.in_off, np.int64),
+                in_ids=np.ascontiguousarray(ev.in_ids, np.int64),
+                in_w=np.ascontiguousarray(ev.in_w, np.float64),
+                out_off=np.ascontiguousarray(ev.out_off, np.int64),
+                out_ids=np.ascontiguousarray(ev.out_ids, np.int64),
+                out_w=np.ascontiguousarray(ev.out_w, np.float64))
+    b = EventBatch(len(arrs["kind"]), _p(arrs["kind"], i32p), _p(arrs["u"], i64p),
+                   _p(arrs["v"], i64p), _p(arrs["w"], f64p), _p(arrs["in_off"], i64p),
+                   _p(arrs["in_ids"], i64p), _p(arrs["in_w"], f64p), _p(arrs["out_off"], i64p),
+                   _p(arrs["out_ids"], i64p), _p(arrs["out_w"], f64p))
+    return b, arrs  # keep arrs alive while b is used
+
+
+class Engine:
+    """damf::Engine on one B200. Construct from explicit factors
+    (FactorState(xb, yb, px, py, sigma, d), factor_state.hpp:22-23)."""
+
+    def __init__(self, n, offsets, targets, weights, d, k, xb, yb, px, py, sigma, alpha=0.3,
+                 eps=1e-5, undirected=False, rebase_cond=1e8, rebase_every=50000, seed=0,
+                 node_capacity=0, arc_capacity=0):
+        L = lib()
+        self._offsets = np.ascontiguousarray(offsets, np.int64)
+        self._targets = np.ascontiguousarray(targets, np.int32)
+        self._weights = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        csr = Csr(n, len(self._targets), _p(self._offsets, i64p), _p(self._targets, i32p),
+                  _p(self._weights, f64p))
+        cfg = Config(d, alpha, eps, seed, rebase_cond, rebase_every, int(undirected), 0,
+                     node_capacity, arc_capacity)
+        xb = np.ascontiguousarray(xb, np.float32)
+        yb = np.ascontiguousarray(yb, np.float32)
+        px = np.ascontiguousarray(px, np.float64)
+        py = np.ascontiguousarray(py, np.float64)
+        sigma = np.ascontiguousarray(sigma, np.float64)
+        self.h = C.c_void_p()
+        st = L.damf_gpu_create_from_factors(C.byref(csr), C.byref(cfg), k, _p(xb, f32p),
+                                            _p(yb, f32p), _p(px, f64p), _p(py, f64p),
+                                            _p(sigma, f64p), C.byref(self.h))
+        del self._offsets, self._targets, self._weights
+        if st:
+            raise DamfError(st, "create_from_factors failed")
+        self.d = d
+        self.alpha = alpha
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().damf_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, st, index=-1):
+        if st:
+            raise DamfError(st, lib().damf_gpu_last_error(self.h).decode(), index)
+
+    def apply(self, ev, mode=0):
+        b, keep = make_batch(ev)
+        s = ApplyStats()
+        st = lib().damf_gpu_apply(self.h, C.byref(b), mode, C.byref(s))
+        del keep
+        self._check(st, s.failed_index)
+        return s.as_dict()
+
+    def latencies_us(self):
+        n = lib().damf_gpu_event_latencies(self.h, None, 0)
+        out = np.zeros(n)
+        lib().damf_gpu_event_latencies(self.h, _p(out, f64p), n)
+        return out
+
+    def diag(self):
+        o = Diag()
+        self._check(lib().damf_gpu_diagnostics(self.h, C.byref(o)))
+        return {f: getattr(o, f) for f, _ in o._fields_}
+
+    @property
+    def k(self):
+        return self.diag()["k"]
+
+    @property
+    def n(self):
+        return self.diag()["n"]
+
+    def get(self, which):
+        dg = self.diag()
+        n, k = dg["n"], dg["k"]
+        if which in (XB, YB, ZB, RB, X, Y, Z):
+            out = np.zeros((n, k), np.float32)
+        elif which in (PX, PY, QX, QY):
+            out = np.zeros((k, k), np.float64)
+        else:
+            out = np.zeros(k, np.float64)
+        self._check(lib().damf_gpu_get_state(self.h, which, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def query(self, which, ids):
+        ids = np.ascontiguousarray(ids, np.int64)
+        out = np.zeros((len(ids), self.k), np.float32)
+        self._check(lib().damf_gpu_query_rows(self.h, which, _p(ids, i64p), len(ids), _p(out, f32p)))
+        return out
+
+    def context(self, u):
+        return self.query(X, [u])[0]
+
+    def content(self, u):
+        return self.query(Y, [u])[0]
+
+    def enhanced(self, u):
+        return self.query(Z, [u])[0]
+
+    def score(self, u, v, enhanced=True):
+        out = C.c_double()
+        self._check(lib().damf_gpu_score(self.h, u, v, int(enhanced), C.byref(out)))
+        return out.value
+
+    def materialize(self, which=X):
+        return self.get(which)
+
+    def graph_sets(self):
+        n = self.n
+        arcs = self.diag()["arcs"]
+        off = np.zeros(n + 1, np.int64)
+        ids = np.zeros(max(arcs, 1), np.int32)
+        deg = np.zeros(n)
+        self._check(lib().damf_gpu_get_graph(self.h, _p(off, i64p), _p(ids, i32p), _p(deg, f64p)))
+        return off, ids[:arcs], deg
+
+    def ppr_init(self):
+        s = ApplyStats()
+        self._check(lib().damf_gpu_ppr_init(self.h, C.byref(s)))
+        return s.as_dict()
+
+    def ppr_push(self):
+        s = ApplyStats()
+        self._check(lib().damf_gpu_ppr_push(self.h, C.byref(s)))
+        return s.as_dict()
+
+    def rebase(self):
+        self._check(lib().damf_gpu_rebase(self.h))
+
+    def sync(self):
+        self._check(lib().damf_gpu_sync(self.h))
+
+
+def materialize_dev(x_ptr, n, d, F, z_ptr, stream=None):
+    """Standalone Z = X F on device buffers (pointers as ints). Returns ms."""
+    F = np.ascontiguousarray(F, np.float64)
+    ms = C.c_float()
+    st = lib().damf_materialize_dev(C.c_void_p(x_ptr), n, d, _p(F, f64p), C.c_void_p(z_ptr),
+                                    C.c_void_p(stream) if stream else None, C.byref(ms))
+    if st:
+        raise DamfError(st, "damf_materialize_dev failed")
+    return ms.value

@@ -1,0 +1,92 @@
+"""GPU parity of the PPR enhancer (test_enhancer.cpp, acceptance criterion 4)
+and of Z = X F materialisation (factor_state.cpp:120-123)."""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import dense_defect, gpu_from_oracle, rel_frob
+from paper_2306_08967_b200 import engine as ge
+from paper_2306_08967_b200.workloads import EventList
+
+pytestmark = pytest.mark.gpu
+
+
+def test_enhanced_query_matches_dense_linear_solve():
+    # test_enhancer.cpp:117-145
+    g = oracle.gen_random_graph(30, 140, 77)
+    oe = oracle.OracleEngine(g, d=8, alpha=0.3, eps=1e-7, seed=77)
+    e = gpu_from_oracle(g, oe, d=8, alpha=0.3, eps=1e-7)
+    n = g.n
+    x = e.get(ge.X).astype(np.float64)
+    off, ids, deg = e.graph_sets()
+    op = np.eye(n)
+    for u in range(n):
+        if deg[u] > 0:
+            for v in ids[off[u]:off[u + 1]]:
+                op[u, v] -= 0.7 / deg[u]
+    z_exact = np.linalg.solve(op, 0.3 * x)
+    z = e.get(ge.Z).astype(np.float64)
+    maxdeg = max(1.0, deg.max())
+    assert np.abs(z - z_exact).max() <= 1e-7 * (1 + maxdeg) + 1e-6 * np.abs(z_exact).max()
+
+
+def test_two_cycle_fixed_point():
+    # test_enhancer.cpp:44-50
+    g = oracle.Graph(2, [0, 1], [1, 0])
+    off, tgt, _ = (np.array([0, 1, 2]), np.array([1, 0], np.int32), None)
+    e = ge.Engine(2, off, tgt, None, 1, 1, np.array([[1.0], [0.0]], np.float32),
+                  np.array([[1.0], [0.0]], np.float32), np.eye(1), np.eye(1), np.ones(1),
+                  alpha=0.5, eps=1e-9)
+    z = e.get(ge.Z)
+    assert abs(z[0, 0] - 2 / 3) < 1e-6 and abs(z[1, 0] - 1 / 3) < 1e-6
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_defect_bound_after_structural_churn(seed):
+    # acceptance_main.cpp:222-262 (node adds, adds, removals; alpha 0.3, eps 1e-5)
+    rng = np.random.default_rng(500 + seed)
+    n = 20 + int(rng.integers(181))
+    g = oracle.gen_random_graph(n, 4 * n, 500 + seed)
+    oe = oracle.OracleEngine(g, d=8, alpha=0.3, eps=1e-5, seed=500 + seed)
+    e = gpu_from_oracle(g, oe, d=8, alpha=0.3, eps=1e-5)
+    worst = 0.0
+    for t in range(30):
+        nn = e.n
+        off, ids, deg = e.graph_sets()
+        if rng.random() < 0.15:
+            a, b = int(rng.integers(nn)), int(rng.integers(nn))
+            ev = EventList(np.array([ge.ADD_NODE], np.int32), np.array([nn]), np.array([0]),
+                           np.ones(1), np.array([0, 1]), np.array([a]), np.ones(1),
+                           np.array([0, 1]), np.array([b]), np.ones(1))
+        else:
+            u, v = int(rng.integers(nn)), int(rng.integers(nn))
+            if u == v:
+                continue
+            has = v in ids[off[u]:off[u + 1]]
+            ev = EventList.edges(ge.REMOVE_EDGE if has else ge.ADD_EDGE, [u], [v])
+        e.apply(ev)
+        oe.apply(ev)
+        off, ids, deg = e.graph_sets()
+        dfc = dense_defect(e.n, off, ids, deg, e.get(ge.X), e.get(ge.Z), 0.3)
+        worst = max(worst, dfc)
+    print("worst scaled defect", worst)
+    # the reference's bound eps (1 + 1e-6) plus fp32 residual rounding
+    assert worst <= 1e-5 * (1 + 1e-6) + 2e-7
+
+
+def test_materialize_matches_fp64():
+    import torch
+    rng = np.random.default_rng(3)
+    for d in (32, 64, 128, 256):
+        n = 20000
+        x = (rng.standard_normal((n, d)) / np.sqrt(d)).astype(np.float32)
+        q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+        F = q * rng.uniform(0.5, 2.0, d)[None, :]
+        X = torch.from_numpy(x).cuda()
+        Z = torch.empty_like(X)
+        ge.materialize_dev(X.data_ptr(), n, d, F, Z.data_ptr())
+        torch.cuda.synchronize()
+        ref = x.astype(np.float64) @ F
+        err = rel_frob(Z.cpu().numpy().astype(np.float64), ref)
+        print(d, err)
+        assert err <= 1e-5
