@@ -136,6 +136,7 @@ typedef struct damf_diag {
   double proj_row_bound;  /* factor_state.cpp:251-259                      */
   int64_t total_pushes;   /* enhancer.hpp:41                               */
   int64_t device_bytes;   /* HBM held by the handle                        */
+  int64_t kernel_launches;/* kernels this handle has launched (all calls)  */
 } damf_diag;
 
 typedef struct damf_gpu damf_gpu; /* opaque handle: owns all device memory */
@@ -197,6 +198,14 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats);
 int damf_gpu_rebase(damf_gpu* h);
 
 int damf_gpu_diagnostics(damf_gpu* h, damf_diag* out);
+
+/* The handle's CUDA stream (cudaStream_t as void*), for callers that time
+ * or order work against it. */
+void* damf_gpu_stream(damf_gpu* h);
+
+/* Cumulative PPR push work since creation, for algorithmic-byte accounting:
+ * out4 = {sum |frontier|, sum |affected|, sum outdeg(affected), pulled arcs}. */
+int damf_gpu_push_counters(damf_gpu* h, int64_t* out4);
 
 /* Standalone materialisation kernel, Z = X * F (cfg 4): x_dev/z_dev are
  * n x d fp32 device buffers (may alias for in-place), f_host is d x d fp64.

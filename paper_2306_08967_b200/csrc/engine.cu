@@ -222,6 +222,7 @@ struct damf_gpu {
   int64_t total_pushes = 0;
   int round_base = 0;
   size_t bytes = 0;
+  int64_t launches = 0;
   std::string err;
   std::vector<void*> allocs;
 };
@@ -323,9 +324,11 @@ PprArgs ppr_args(damf_gpu* h) {
   return a;
 }
 
+bool ed_absorb_nonempty(damf_gpu* h, int64_t e) { return h->ev.h[e].touched_cnt > 0; }
+
 int sync_ctl(damf_gpu* h) {
   CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->st));
-  CK(cudaMemcpyAsync(h->h_pstats, h->pstats, 3 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(h->h_pstats, h->pstats, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   h->k = h->h_ctl->k;
   h->round_base = (int)h->h_pstats[2];
@@ -338,6 +341,7 @@ double* live_Q(damf_gpu* h, int side) { return h->Q[side][h->h_ctl->pp[side]]; }
 // PPR push with the current s_max (computed and consumed on the device: no
 // host round trip per event); grid sized to the expected work.
 int run_push(damf_gpu* h, int grid, unsigned long long* t_end) {
+  h->launches += 2;
   CK(launch_smax(h->PT[0][0], h->PT[0][1], h->ctl, h->ld, h->smax, h->st));
   PprArgs a = ppr_args(h);
   a.t_end = t_end;
@@ -411,7 +415,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev);
   CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
   CK(cudaMallocHost(&h->h_ctl, sizeof(DevCtl)));
-  CK(cudaMallocHost(&h->h_pstats, 4 * sizeof(long long)));
+  CK(cudaMallocHost(&h->h_pstats, 8 * sizeof(long long)));
   const int64_t n = g->n, ncap = h->n_cap, d = h->d, ld = h->ld;
   // ---- factor state
   CK(dalloc(h, &h->ctl, 1));
@@ -433,8 +437,8 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   CK(cudaMemcpyAsync(h->sigma, sigma, k * 8, cudaMemcpyHostToDevice, h->st));
   CK(dalloc(h, &h->ws, (size_t)8 * ld * ld));
   CK(dalloc(h, &h->smax, 1));
-  CK(dalloc(h, &h->pstats, 4));
-  CK(cudaMemsetAsync(h->pstats, 0, 4 * sizeof(long long), h->st));
+  CK(dalloc(h, &h->pstats, 8));
+  CK(cudaMemsetAsync(h->pstats, 0, 8 * sizeof(long long), h->st));
   {
     // P (row-major k x k on host) -> device, transpose into PT, invert into Q.
     double* tmp = nullptr;
@@ -862,11 +866,13 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
       ea.e_begin = i;
       ea.e_end = j;
       CK(launch_event_kernel(ea, h->st));
+      h->launches += 1;
     } else {
       for (int64_t e = i; e < j; ++e) {
         ea.e_begin = e;
         ea.e_end = e + 1;
         CK(launch_event_kernel(ea, h->st));
+        h->launches += 1 + (ed_absorb_nonempty(h, e) ? 1 : 0);
         // rows appended by AddNode are visible to the enhancer from here
         const EventDesc& ed = h->ev.h[e];
         if (ed.kind == DAMF_ADD_NODE) h->n = ed.u + 1;
@@ -1096,6 +1102,15 @@ int damf_gpu_diagnostics(damf_gpu* h, damf_diag* o) {
   o->proj_row_bound = sm;
   o->total_pushes = h->h_pstats[0];
   o->device_bytes = (int64_t)h->bytes;
+  o->kernel_launches = h->launches;
+  return 0;
+}
+
+void* damf_gpu_stream(damf_gpu* h) { return (void*)h->st; }
+
+int damf_gpu_push_counters(damf_gpu* h, int64_t* out4) {
+  if (int r = sync_ctl(h)) return r;
+  for (int i = 0; i < 4; ++i) out4[i] = h->h_pstats[3 + i];
   return 0;
 }
 

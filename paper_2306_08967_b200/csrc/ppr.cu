@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(PT_) ppr_push_kernel(PprArgs A) {
         },
         A.listL, A.blk);
     // P3: pull update of affected rows
+    if (blockIdx.x == 0 && threadIdx.x == 0) A.stats[4] += nL;
     for (int q = gw; q < nL; q += nwarps) {
       const int v = A.listL[q];
       float acc[kMaxD / 32];
@@ -168,9 +169,11 @@ __global__ void __launch_bounds__(PT_) ppr_push_kernel(PprArgs A) {
       for (int t = 0; t < kMaxD / 32; ++t) acc[t] = 0.0f;
       const int64_t base = A.out.off[v];
       const int c = A.out.cnt[v];
+      int matched = 0;
       for (int p = 0; p < c; ++p) {
         const int u = A.out.ids[base + p];
         if (A.stamp[u] != R) continue;
+        ++matched;
         const float w = A.out.wts ? (float)A.out.wts[base + p] : 1.0f;
         const float* du = A.delta + (int64_t)u * d;
 #pragma unroll
@@ -194,7 +197,11 @@ __global__ void __launch_bounds__(PT_) ppr_push_kernel(PprArgs A) {
         }
       }
       m = warp_max(m);
-      if (lane == 0) A.key[v] = (float)((double)m / fmax(degv, 1.0));
+      if (lane == 0) {
+        A.key[v] = (float)((double)m / fmax(degv, 1.0));
+        atomicAdd((unsigned long long*)&A.stats[5], (unsigned long long)c);        // stats only
+        atomicAdd((unsigned long long*)&A.stats[6], (unsigned long long)matched);
+      }
     }
     g.sync();
     // next frontier from the affected list
@@ -209,6 +216,7 @@ __global__ void __launch_bounds__(PT_) ppr_push_kernel(PprArgs A) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.stats[0] += pushes;
     A.stats[1] += rounds;
+    A.stats[3] += pushes;
     A.stats[2] = R;  // next round base
     if (A.t_end) *A.t_end = globaltimer();
   }

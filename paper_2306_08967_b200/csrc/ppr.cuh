@@ -26,7 +26,8 @@ struct PprArgs {
   const int* cand;    // candidate rows for the first frontier (ncand >= 0)
   int ncand;          // -1: scan all rows
   long long push_guard;
-  long long* stats;   // [pushes, rounds, next round base]
+  long long* stats;   // [pushes, rounds, next round base, sum|F|, sum|L|,
+                      //  sum outdeg(L), matched arcs] (bench accounting)
   unsigned long long* t_end;
   DevCtl* ctl;
 };

@@ -73,7 +73,8 @@ class Diag(C.Structure):
     _fields_ = [("n", C.c_int64), ("k", C.c_int64), ("d", C.c_int64), ("arcs", C.c_int64),
                 ("events_applied", C.c_int64), ("events_since_rebase", C.c_int64),
                 ("cond_estimate", C.c_double), ("proj_row_bound", C.c_double),
-                ("total_pushes", C.c_int64), ("device_bytes", C.c_int64)]
+                ("total_pushes", C.c_int64), ("device_bytes", C.c_int64),
+                ("kernel_launches", C.c_int64)]
 
 
 _lib = None
@@ -107,6 +108,9 @@ def lib():
         L.damf_gpu_ppr_push.argtypes = [vp, C.POINTER(ApplyStats)]
         L.damf_gpu_rebase.argtypes = [vp]
         L.damf_gpu_diagnostics.argtypes = [vp, C.POINTER(Diag)]
+        L.damf_gpu_stream.argtypes = [vp]
+        L.damf_gpu_stream.restype = C.c_void_p
+        L.damf_gpu_push_counters.argtypes = [vp, i64p]
         L.damf_materialize_dev.argtypes = [vp, C.c_int64, C.c_int64, f64p, vp, vp, f32p]
         _lib = L
     return _lib
@@ -259,6 +263,15 @@ class Engine:
 
     def rebase(self):
         self._check(lib().damf_gpu_rebase(self.h))
+
+    def push_counters(self):
+        out = np.zeros(4, np.int64)
+        self._check(lib().damf_gpu_push_counters(self.h, _p(out, i64p)))
+        return dict(frontier=int(out[0]), affected=int(out[1]), affected_arcs=int(out[2]),
+                    pulled_arcs=int(out[3]))
+
+    def stream_ptr(self):
+        return lib().damf_gpu_stream(self.h)
 
     def sync(self):
         self._check(lib().damf_gpu_sync(self.h))
