@@ -207,6 +207,10 @@ void* damf_gpu_stream(damf_gpu* h);
  * out4 = {sum |frontier|, sum |affected|, sum outdeg(affected), pulled arcs}. */
 int damf_gpu_push_counters(damf_gpu* h, int64_t* out4);
 
+/* Developer profiling: cumulative SM cycles per phase of the per-event
+ * kernel (cluster rank 0), 32 slots (see event_kernel.cu PROF_MARK). */
+int damf_gpu_profile_counters(damf_gpu* h, uint64_t* out16);
+
 /* Standalone materialisation kernel, Z = X * F (cfg 4): x_dev/z_dev are
  * n x d fp32 device buffers (may alias for in-place), f_host is d x d fp64.
  * stream is a cudaStream_t passed as void* (NULL = default stream). The

@@ -283,13 +283,7 @@ EventKernelArgs event_args(damf_gpu* h) {
   a.deg = h->deg;
   const size_t m = (size_t)h->ld * h->ld;
   a.ws_Q1T = h->ws;
-  a.ws_Q2T = h->ws + m;
-  a.ws_ET = h->ws + 2 * m;
-  a.ws_HT = h->ws + 3 * m;
-  a.ws_FT = h->ws + 4 * m;
-  a.ws_GT = h->ws + 5 * m;
-  a.ws_Fi = h->ws + 6 * m;
-  a.ws_Gi = h->ws + 7 * m;
+  a.ws_priv = h->ws + m;
   return a;
 }
 
@@ -435,7 +429,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   CK(dalloc(h, &h->sigma, (size_t)ld));
   CK(cudaMemsetAsync(h->sigma, 0, (size_t)ld * 8, h->st));
   CK(cudaMemcpyAsync(h->sigma, sigma, k * 8, cudaMemcpyHostToDevice, h->st));
-  CK(dalloc(h, &h->ws, (size_t)8 * ld * ld));
+  CK(dalloc(h, &h->ws, (size_t)ld * ld + (size_t)4 * 16 * 20 * ld));
   CK(dalloc(h, &h->smax, 1));
   CK(dalloc(h, &h->pstats, 8));
   CK(cudaMemsetAsync(h->pstats, 0, 8 * sizeof(long long), h->st));
@@ -1107,6 +1101,12 @@ int damf_gpu_diagnostics(damf_gpu* h, damf_diag* o) {
 }
 
 void* damf_gpu_stream(damf_gpu* h) { return (void*)h->st; }
+
+int damf_gpu_profile_counters(damf_gpu* h, uint64_t* out16) {
+  if (int r = sync_ctl(h)) return r;
+  for (int i = 0; i < 32; ++i) out16[i] = h->h_ctl->prof[i];
+  return 0;
+}
 
 int damf_gpu_push_counters(damf_gpu* h, int64_t* out4) {
   if (int r = sync_ctl(h)) return r;

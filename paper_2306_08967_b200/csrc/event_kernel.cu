@@ -9,20 +9,25 @@
 //      eigen-decomposition of M M^T: node steps are one symmetric rank-1
 //      modification of D^2; edge steps are a rank-1 update followed by a
 //      rank-1 downdate (the 2x2 core [[|b|^2,1],[1,0]] split by sign). Each
-//      is a secular equation solved root-parallel (one warp per root) with
-//      Gu-Eisenstat z-hat recomputation and LAPACK-style deflation.       K2
+//      is a secular equation solved root-parallel (one 16-lane group per
+//      root) with Gu-Eisenstat z-hat recomputation and LAPACK-style
+//      deflation.                                                          K2
 //   3. closed forms F = S1^1/2 H S2^-1/2, G = S1^1/2 E S2^-1/2 (edge), the
 //      inverses from the orthonormal-column identity
 //      A^-1 = A^T + d (A d)^T / (1 - |d|^2), P <- P F and P^-1 <- F^-1 P^-1
-//      as cluster-split fp64 GEMMs, and the row fixes X_b[u] += ex P^-1.    K3
+//      on the FP64 tensor cores (DMMA m8n8k4), and the row fixes
+//      X_b[u] += (ex F^-1) P_old^-1 computed before the new P^-1 exists.     K3
 //   4. conditioning bookkeeping for the rebase policy.                     K4
 // Rank growth, shrinkage or an ill-conditioned F fold eagerly (X_b <- X_b P F)
 // exactly like factor_state.cpp:168-192.
 //
-// Matrices exchanged between CTAs are stored "one owned vector per row":
-// P is kept TRANSPOSED (PT[j][i] = P[i][j]) and Q = P^-1 row-major, so every
-// GEMM is Out[t][:] = sum_m Coef[t][m] In[m][:] with Coef row t owned locally
-// and In streamed with coalesced loads.
+// Data placement (what drives the latency): a cluster barrier costs ~400
+// cycles but ~1800 when global stores are pending (the release drains them),
+// so only the matrices every CTA needs (Q1^T, the new P^T and P^-1, touched
+// rows) go through L2; each CTA's owned rows of Q2^T, E, H, F, G, F^-1, G^-1
+// stay in its shared memory, and small vectors move over DSMEM.
+// Ownership: CTA r owns output index t in [r*ceil(k/C), ...) of [0,k); the
+// discarded (k+1)-th direction belongs to the last CTA.
 #include <cooperative_groups.h>
 
 #include <cfloat>
@@ -41,30 +46,30 @@ constexpr int NW = NT / 32;
 constexpr int NMAX = kMaxD + 1;    // k + 1 <= 257
 constexpr int NPAD = kMaxD + 4;
 constexpr double EPS = DBL_EPSILON;
-constexpr int TCH = 9;  // GEMM output rows per chunk (registers)
+constexpr int PLD = 132;           // private-matrix row stride (d <= 128 in smem)
 
 template <int C>
 struct Smem {
-  static constexpr int PER = (NMAX + C - 1) / C;  // owned block size (max)
+  static constexpr int PROWS = (128 + C - 1) / C + 1;  // owned rows (+ the discarded one)
   // small vectors (fp64)
   double sig[NPAD], gA[NPAD], gB[NPAD], wA[NPAD], wB[NPAD];
   double av[NPAD], bv[NPAD], Dg[NPAD], dd[NPAD], zz[NPAD], um[NPAD];
   double sd[NPAD], sz[NPAD], kd[NPAD], kz[NPAD], kz2[NPAD];
   int kidx[NPAD], defl[NPAD], src[NPAD], org[NPAD];
   double tau[NPAD], zhat[NPAD], lamA[NPAD], lamB[NPAD];
-  double s2[NPAD], exv[NPAD], eyv[NPAD], dH[NPAD], dE[NPAD], AHdH[NPAD], AEdE[NPAD];
+  double s2[NPAD], exv[NPAD], eyv[NPAD], dH[NPAD], dE[NPAD];
+  double AHdH[NPAD], AEdE[NPAD], yA1[NPAD], yB1[NPAD];
   int rot_p[NPAD], rot_q[NPAD];
   double rot_c[NPAD], rot_s[NPAD];
-  double partH[C][kMaxD], partE[C][kMaxD];
+  double partL[4][kMaxD];         // this CTA's partial column sums
+  double partS[4];                // this CTA's partial scalars
   double pnorm[C][4];
-  double coef[TCH * NPAD];        // staged GEMM coefficient rows
-  double red[NT * TCH];           // GEMM split-K reduction
-  double vscr[NW][NPAD];          // per-warp eigenvector scratch
+  double priv[4][PROWS * PLD];    // owned rows of Q2T/F, E/G^-1, H/F^-1, G
+  double vscr[NW][NPAD];          // per-warp eigenvector scratch (rare deflation path)
   double bred[NW];
   long long found[C][2];          // graph row-scan results
   int K, nrot, need;
   int k, pp[2];
-  double rhoN, sumkz2;
   int err;
 };
 
@@ -86,15 +91,16 @@ DAMF_D int block_or(Smem<C>& S, int v) {
   return __syncthreads_or(v);
 }
 
-template <int C>
-DAMF_D void bcast(cg::cluster_group& cl, double* local, int idx, double val) {
-#pragma unroll 1
-  for (int r = 0; r < C; ++r) *cl.map_shared_rank(local + idx, r) = val;
+// 16-lane group reductions (xor butterfly: bitwise identical in all lanes)
+DAMF_D double gsum(double v, unsigned mask) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, 16);
+  return v;
 }
-template <int C>
-DAMF_D void bcast_i(cg::cluster_group& cl, int* local, int idx, int val) {
-#pragma unroll 1
-  for (int r = 0; r < C; ++r) *cl.map_shared_rank(local + idx, r) = val;
+DAMF_D double gprod(double v, unsigned mask) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v *= __shfl_xor_sync(mask, v, o, 16);
+  return v;
 }
 
 DAMF_D void block_range(int total, int C, int rank, int& lo, int& hi) {
@@ -103,61 +109,88 @@ DAMF_D void block_range(int total, int C, int rank, int& lo, int& hi) {
   hi = min(total, lo + per);
 }
 
+// Owned output indices: [r*ceil(k/C), ...) of [0,k); the last CTA also owns
+// [k, n) (the (k+1)-th singular direction).
+DAMF_D void own_range(int k, int n, int C, int rank, int& lo, int& hi) {
+  block_range(k, C, rank, lo, hi);
+  if (rank == C - 1) hi = n;
+}
+
 // ------------------------------------------------------------- row GEMM
-// Out[t][j] = sum_m Coef[t][m] In[m][j], t in [t0,t1), j < J, m < M.
-// Coef/In/Out global fp64 with leading dims. Coef rows are staged in smem;
-// In is streamed once per CTA with coalesced loads (split-K over thread
-// groups, reduced through smem in a fixed order). Optionally accumulates
-// the Frobenius norm^2 of the written block into *fro (thread 0 result).
+// FP64 tensor-core MMA (DMMA): D[8x8] += A[8x4] (row) * B[4x8] (col).
+// Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane>>2][lane&3],
+// b = B[lane&3][lane>>2], d{0,1} = D[lane>>2][2*(lane&3) + {0,1}].
+DAMF_D void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Out[o0 + r][j] = sum_m Coef[r][m] In[m][j] for r < nt (<= 16), j < J, m < M.
+// Coef rows (local smem or global, stride ldc) feed the A fragments; In is
+// streamed from L2 with TP*KU independent loads in flight per lane; each
+// warp owns TP 8-column tiles. Returns the Frobenius norm^2 of the block
+// (block-reduced) when fro != nullptr.
 template <int C>
-DAMF_D void rows_gemm(Smem<C>& S, double* Out, int ldo, const double* Coef, int ldc,
-                      const double* __restrict__ In, int ldi, int t0, int t1, int M, int J,
-                      double* fro) {
+DAMF_D void rows_gemm16(Smem<C>& S, double* Out, int ldo, int o0, const double* Coef, int ldc,
+                        int nt, const double* __restrict__ In, int ldi, int M, int J,
+                        double* fro) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int MP = (M + 3) & ~3;
   double frob = 0.0;
-  int jt = 32;
-  while (jt < J) jt <<= 1;
-  if (jt > NT) jt = NT;
-  const int G = NT / jt;
-  const int j = threadIdx.x % jt, g = threadIdx.x / jt;
-  for (int c0 = t0; c0 < t1; c0 += TCH) {
-    const int nt = min(TCH, t1 - c0);
-    __syncthreads();
-    for (int x = threadIdx.x; x < nt * M; x += NT) {
-      const int t = x / M, m = x % M;
-      S.coef[t * NPAD + m] = Coef[(int64_t)(c0 + t) * ldc + m];
+  const int ntiles = (J + 7) >> 3;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int mt = (nt + 7) >> 3;  // m8 tiles (1 or 2)
+  constexpr int TP = 2;
+  constexpr int KU = 8;
+  for (int tb = warp * TP; tb < ntiles; tb += NW * TP) {
+    double d0[TP][2], d1[TP][2];
+    int bc[TP];
+    bool bok[TP];
+#pragma unroll
+    for (int p = 0; p < TP; ++p) {
+      bc[p] = ((tb + p) << 3) + (lane >> 2);
+      bok[p] = (tb + p) < ntiles && bc[p] < J;
+      d0[p][0] = d1[p][0] = d0[p][1] = d1[p][1] = 0.0;
     }
-    __syncthreads();
-    for (int jb = 0; jb < J; jb += jt) {
-      const int jj = jb + j;
-      double acc[TCH];
+    for (int k0 = 0; k0 < MP; k0 += 4 * KU) {
+      double b[TP][KU];
 #pragma unroll
-      for (int t = 0; t < TCH; ++t) acc[t] = 0.0;
-      if (jj < J) {
-        for (int m = g; m < M; m += G) {
-          const double x = In[(int64_t)m * ldi + jj];
+      for (int q = 0; q < KU; ++q)
 #pragma unroll
-          for (int t = 0; t < TCH; ++t)
-            if (t < nt) acc[t] = fma(S.coef[t * NPAD + m], x, acc[t]);
+        for (int p = 0; p < TP; ++p) {
+          const int m = k0 + 4 * q + ac;
+          b[p][q] = (bok[p] && m < M) ? In[(int64_t)m * ldi + bc[p]] : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < KU; ++q) {
+        const int m = k0 + 4 * q + ac;
+        if (k0 + 4 * q >= MP) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= mt) break;
+          const int r = 8 * h + ar;
+          const double a = (r < nt && m < M) ? Coef[(int64_t)r * ldc + m] : 0.0;
+#pragma unroll
+          for (int p = 0; p < TP; ++p) dmma(d0[p][h], d1[p][h], a, b[p][q]);
         }
       }
-      if (G > 1) {
+    }
 #pragma unroll
-        for (int t = 0; t < TCH; ++t)
-          if (t < nt) S.red[(t * G + g) * jt + j] = acc[t];
-        __syncthreads();
-        if (g == 0 && jj < J) {
-          for (int t = 0; t < nt; ++t) {
-            double s = 0;
-            for (int q = 0; q < G; ++q) s += S.red[(t * G + q) * jt + j];
-            Out[(int64_t)(c0 + t) * ldo + jj] = s;
-            frob += s * s;
+    for (int p = 0; p < TP; ++p) {
+      const int col = ((tb + p) << 3) + 2 * ac;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * h + ar;
+        if (h < mt && r < nt && (tb + p) < ntiles) {
+          if (col < J) {
+            Out[(int64_t)(o0 + r) * ldo + col] = d0[p][h];
+            frob += d0[p][h] * d0[p][h];
           }
-        }
-        __syncthreads();
-      } else if (jj < J) {
-        for (int t = 0; t < nt; ++t) {
-          Out[(int64_t)(c0 + t) * ldo + jj] = acc[t];
-          frob += acc[t] * acc[t];
+          if (col + 1 < J) {
+            Out[(int64_t)(o0 + r) * ldo + col + 1] = d1[p][h];
+            frob += d1[p][h] * d1[p][h];
+          }
         }
       }
     }
@@ -166,20 +199,34 @@ DAMF_D void rows_gemm(Smem<C>& S, double* Out, int ldo, const double* Coef, int 
   __syncthreads();
 }
 
+template <int C>
+DAMF_D void rows_gemm(Smem<C>& S, double* Out, int ldo, int o0, const double* Coef, int ldc,
+                      int nt, const double* __restrict__ In, int ldi, int M, int J, double* fro) {
+  double total = 0.0;
+  for (int c = 0; c < nt; c += 16) {
+    double f = 0.0;
+    rows_gemm16<C>(S, Out, ldo, o0 + c, Coef + (int64_t)c * ldc, ldc, min(16, nt - c), In, ldi,
+                   M, J, fro ? &f : nullptr);
+    total += f;
+  }
+  if (fro) *fro = total;
+}
+
 // ------------------------------------------------------------ secular solver
 // Root j of 1 + rho * sum_i kz2[i] / (kd[i] - lambda) = 0 (kd ascending,
 // rho > 0, sum kz2 <= 1), one warp. Returns tau and the origin pole o with
 // lambda = kd[o] + tau, so lambda - kd[i] is formed as tau - (kd[i]-kd[o]).
-DAMF_D void secular_root(const double* kd, const double* kz2, int K, double rho, double sumz2,
-                         int j, double& tau_out, int& org_out) {
-  const int lane = threadIdx.x & 31;
+DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, double sumz2,
+                        int j, double& tau_out, int& org_out) {
+  const int gl = threadIdx.x & 15;
+  const unsigned gm = 0xFFFFu << (threadIdx.x & 16);
   int o;
   double lo, hi;
   if (j < K - 1) {
     const double mid = 0.5 * (kd[j + 1] - kd[j]);
     double s = 0;
-    for (int i = lane; i < K; i += 32) s += kz2[i] / ((kd[i] - kd[j]) - mid);
-    s = warp_sum(s);
+    for (int i = gl; i < K; i += 16) s += kz2[i] / ((kd[i] - kd[j]) - mid);
+    s = gsum(s, gm);
     if (1.0 + rho * s >= 0.0) {
       o = j;
       lo = 0.0;
@@ -196,12 +243,13 @@ DAMF_D void secular_root(const double* kd, const double* kz2, int K, double rho,
   }
   const double dorg = kd[o];
   double tau = 0.5 * (lo + hi);
-  for (int it = 0; it < 120; ++it) {
+  int it = 0;
+  for (; it < 120; ++it) {
     double psi = 0, phi = 0, dpsi = 0, dphi = 0, aerr = 0;
-    for (int i = lane; i < K; i += 32) {
-      const double del = (kd[i] - dorg) - tau;
-      const double t = kz2[i] / del;
-      const double dt = t / del;
+    for (int i = gl; i < K; i += 16) {
+      const double rdel = 1.0 / ((kd[i] - dorg) - tau);
+      const double t = kz2[i] * rdel;
+      const double dt = t * rdel;
       if (i <= j) {
         psi += t;
         dpsi += dt;
@@ -211,11 +259,11 @@ DAMF_D void secular_root(const double* kd, const double* kz2, int K, double rho,
       }
       aerr += fabs(t);
     }
-    psi = rho * warp_sum(psi);
-    phi = rho * warp_sum(phi);
-    dpsi = rho * warp_sum(dpsi);
-    dphi = rho * warp_sum(dphi);
-    aerr = rho * warp_sum(aerr);
+    psi = rho * gsum(psi, gm);
+    phi = rho * gsum(phi, gm);
+    dpsi = rho * gsum(dpsi, gm);
+    dphi = rho * gsum(dphi, gm);
+    aerr = rho * gsum(aerr, gm);
     const double f = 1.0 + psi + phi;
     if (f < 0.0)
       lo = fmax(lo, tau);
@@ -257,6 +305,7 @@ DAMF_D void secular_root(const double* kd, const double* kz2, int K, double rho,
   }
   tau_out = tau;
   org_out = o;
+  return it;
 }
 
 // Eigen-decomposition of diag(dd) + rho z z^T over n entries, cluster-wide.
@@ -267,10 +316,20 @@ DAMF_D void secular_root(const double* kd, const double* kz2, int K, double rho,
 // in this CTA's block. Ends WITHOUT a cluster barrier.
 template <int C>
 DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const double* z,
-                      double rho, int n, double* QT, int ldq, double* lamOut) {
+                      double rho, int n, int elo, int ehi, double* QT, int ldq, int row_off,
+                      double* lamOut, unsigned long long* A_prof) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cl.block_rank();
   const bool neg = rho < 0.0;
+  long long _pt = clock64();
+#define EPROF(slot)                                                        \
+  do {                                                                     \
+    if (rank == 0 && threadIdx.x == 0) {                                   \
+      const long long _t = clock64();                                      \
+      A_prof[slot] += (unsigned long long)(_t - _pt);                      \
+      _pt = _t;                                                            \
+    }                                                                      \
+  } while (0)
   for (int c = tid; c < n; c += NT) {
     const int i = n - 1 - c;
     S.sd[c] = neg ? -dd[i] : dd[i];
@@ -352,6 +411,7 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
     S.nrot = nrot;
   }
   __syncthreads();
+  EPROF(16);
   const int K = S.K;
   double sz2 = 0;
   for (int j = tid; j < K; j += NT) sz2 += S.kz2[j];
@@ -359,29 +419,39 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   // --- roots (this CTA's block of K)
   int lo, hi;
   block_range(K, C, rank, lo, hi);
-  for (int j = lo + warp; j < hi; j += NW) {
+  const int grp = tid >> 4, gl = tid & 15;
+  const unsigned gm = 0xFFFFu << (tid & 16);
+  constexpr int NG = NT / 16;
+  for (int j = lo + grp; j < hi; j += NG) {
     double t;
     int o;
-    secular_root(S.kd, S.kz2, K, rhoN, sz2, j, t, o);
-    if (lane < C) {
-      *cl.map_shared_rank(S.tau + j, lane) = t;
-      *cl.map_shared_rank(S.org + j, lane) = o;
+    const int its = secular_root(S.kd, S.kz2, K, rhoN, sz2, j, t, o);
+    if (gl == 0 && rank == 0) atomicAdd(&A_prof[13], (unsigned long long)its);
+    if (gl == 0 && rank == 0) atomicAdd(&A_prof[14], 1ull);
+    if (gl == 0) atomicMax(&A_prof[15], (unsigned long long)its);
+    if (gl < C) {
+      *cl.map_shared_rank(S.tau + j, gl) = t;
+      *cl.map_shared_rank(S.org + j, gl) = o;
     }
   }
+  EPROF(17);
   cl.sync();
+  EPROF(18);
   // --- Gu-Eisenstat z-hat: zhat_i^2 = prod_j (lam_j - d_i) / prod_{j!=i} (d_j - d_i) / rho
-  for (int i = lo + warp; i < hi; i += NW) {
+  for (int i = lo + grp; i < hi; i += NG) {
     const double di = S.kd[i];
     double p = 1.0;
-    for (int j = lane; j < K; j += 32) {
+    for (int j = gl; j < K; j += 16) {
       const double lmd = S.tau[j] - (di - S.kd[S.org[j]]);  // lambda_j - d_i
       p *= (j == i) ? lmd / rhoN : lmd / (S.kd[j] - di);
     }
-    p = warp_prod(p);
+    p = gprod(p, gm);
     const double zh = copysign(sqrt(fmax(p, 0.0)), S.kz[i]);
-    if (lane < C) *cl.map_shared_rank(S.zhat + i, lane) = zh;
+    if (gl < C) *cl.map_shared_rank(S.zhat + i, gl) = zh;
   }
+  EPROF(19);
   cl.sync();
+  EPROF(20);
   // --- output order (ascending canonical eigenvalues)
   if (!need) {
     for (int e = tid; e < n; e += NT) {
@@ -421,9 +491,34 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
     }
   }
   __syncthreads();
+  EPROF(21);
   // --- eigenvectors for this CTA's block of output columns
-  int elo, ehi;
-  block_range(n, C, rank, elo, ehi);
+  if (S.nrot == 0) {
+    for (int e = elo + grp; e < ehi; e += NG) {
+      const int item = S.src[e];
+      double* row = QT + (int64_t)(e - row_off) * ldq;
+      if (K < n)
+        for (int i = gl; i < n; i += 16) row[i] = 0.0;
+      __syncwarp(gm);
+      if (item < K) {
+        const double dj = S.kd[S.org[item]], tj = S.tau[item];
+        double nn = 0;
+        for (int t = gl; t < K; t += 16) {
+          const double y = S.zhat[t] / ((S.kd[t] - dj) - tj);
+          nn += y * y;
+        }
+        const double inv = 1.0 / sqrt(gsum(nn, gm));
+        for (int t = gl; t < K; t += 16)
+          row[n - 1 - S.kidx[t]] = S.zhat[t] / ((S.kd[t] - dj) - tj) * inv;
+      } else if (gl == 0) {
+        row[n - 1 - (item - K)] = 1.0;
+      }
+      __syncwarp(gm);
+    }
+    __syncthreads();
+    EPROF(22);
+    return;
+  }
   double* v = S.vscr[warp];
   for (int e = elo + warp; e < ehi; e += NW) {
     const int item = S.src[e];
@@ -454,10 +549,11 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
         v[q] = ss * yp + cc * yq;
       }
     __syncwarp();
-    for (int i = lane; i < n; i += 32) QT[(int64_t)e * ldq + i] = v[n - 1 - i];
+    for (int i = lane; i < n; i += 32) QT[(int64_t)(e - row_off) * ldq + i] = v[n - 1 - i];
     __syncwarp();
   }
   __syncthreads();
+  EPROF(22);
 }
 
 // --------------------------------------------------------- graph mutation K9
@@ -535,6 +631,25 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
 }
 
 // ------------------------------------------------------------ rank-1 step
+#define PROF_MARK(slot)                                                   \
+  do {                                                                    \
+    if (rank == 0 && threadIdx.x == 0) {                                  \
+      const long long _t = clock64();                                     \
+      A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
+      _pt = _t;                                                           \
+    }                                                                     \
+  } while (0)
+
+// ------------------------------------------------------------ rank-1 step
+#define PROF_MARK(slot)                                                   \
+  do {                                                                    \
+    if (rank == 0 && threadIdx.x == 0) {                                  \
+      const long long _t = clock64();                                     \
+      A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
+      _pt = _t;                                                           \
+    }                                                                     \
+  } while (0)
+
 template <int C>
 DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& cl,
                        const StepDesc& st) {
@@ -553,8 +668,24 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   const double* QA = A.Q[sA][S.pp[sA]];
   const double* QB = A.Q[sB][S.pp[sB]];
   const int ld = A.ld;
+  long long _pt = clock64();
+  // owned output rows and the private (per-CTA) matrices
+  int olo, ohi;
+  own_range(k, n, C, rank, olo, ohi);
+  const int kohi = min(ohi, k);  // owned rows among the kept k
+  double* PB[4];
+  int pld;
+  if (d <= 128) {
+    for (int i = 0; i < 4; ++i) PB[i] = S.priv[i];
+    pld = PLD;
+  } else {
+    const int prg = (NMAX + C - 1) / C + 1;
+    for (int i = 0; i < 4; ++i) PB[i] = A.ws_priv + ((int64_t)i * C + rank) * prg * ld;
+    pld = ld;
+  }
+  auto prow = [&](int buf, int t) -> double* { return PB[buf] + (int64_t)(t - olo) * pld; };
 
-  // ---- 1. gather (fp64) -------------------------------------------------
+  // ---- 1. gather (fp64) and w = S^-1/2 (g P), this CTA's columns ---------
   for (int j = tid; j < k; j += NT) {
     double s = 0;
     for (int t = 0; t < st.nb; ++t)
@@ -564,7 +695,6 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     S.sig[j] = A.sigma[j];
   }
   __syncthreads();
-  // ---- w = S^-1/2 (g P), this CTA's block of columns --------------------
   {
     int lo, hi;
     block_range(k, C, rank, lo, hi);
@@ -582,7 +712,8 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       }
     }
   }
-  cl.sync();
+  cl.sync();  // B1
+  PROF_MARK(0);
   // ---- 2. bordered system (redundant per CTA) -----------------------------
   double wa2 = 0, wb2 = 0;
   for (int j = tid; j < k; j += NT) {
@@ -605,9 +736,7 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     allow_grow = k < d && (long long)k < min(st.n_a, st.n_b + 1) && RA >= 1e-6 * fmax(1.0, bnorm);
   double lp = 1.0, lm = 0.0;
   if (edge) {
-    double beta = 0;
-    for (int j = tid; j < k; j += NT) beta += S.wB[j] * S.wB[j];
-    beta = block_sum(S, beta) + rB * rB;
+    const double beta = wb2 + rB * rB;
     const double sq = sqrt(beta * beta + 4.0);
     lp = 0.5 * (beta + sq);
     lm = -2.0 / (beta + sq);
@@ -629,95 +758,140 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     }
   }
   __syncthreads();
-  // ---- 3. eigen step A: D^2 + rho z z^T -----------------------------------
-  eig_rank1<C>(S, cl, S.dd, S.zz, edge ? lp : 1.0, n, A.ws_Q1T, ld, S.lamA);
-  if (!edge) cl.sync();  // node steps read other CTAs' Q1T rows (t -> n-1-t)
-  int tlo, thi;
-  block_range(n, C, rank, tlo, thi);
+  PROF_MARK(1);
+  // ---- 3. eigen step A: D^2 + rho z z^T -> Q1^T rows (L2, shared) ---------
+  eig_rank1<C>(S, cl, S.dd, S.zz, edge ? lp : 1.0, n, olo, ohi, A.ws_Q1T, ld, 0, S.lamA,
+               A.ctl->prof);
+  PROF_MARK(2);
   if (edge) {
     // z2 = Q1^T u_minus for this CTA's columns, broadcast
-    for (int e = tlo + warp; e < thi; e += NW) {
+    for (int e = olo + warp; e < ohi; e += NW) {
       double s = 0;
       for (int i = lane; i < n; i += 32) s += A.ws_Q1T[(int64_t)e * ld + i] * S.um[i];
       s = warp_sum(s);
       if (lane < C) *cl.map_shared_rank(S.zz + e, lane) = s;
     }
-    cl.sync();
-    // ---- eigen step B: Lambda1 + lm z2 z2^T (downdate) ----------------------
-    eig_rank1<C>(S, cl, S.lamA, S.zz, lm, n, A.ws_Q2T, ld, S.lamB);
-    // E columns (rows of ET) t in block: ET[t] = sum_e Q2T[t][e] Q1T[e]
-    rows_gemm<C>(S, A.ws_ET, ld, A.ws_Q2T, ld, A.ws_Q1T, ld, tlo, thi, n, n, nullptr);
   }
+  cl.sync();  // B4: Q1^T rows visible (and z2 for edges)
+  PROF_MARK(3);
+  if (edge) {
+    // ---- eigen step B: Lambda1 + lm z2 z2^T -> Q2^T rows (private) ---------
+    eig_rank1<C>(S, cl, S.lamA, S.zz, lm, n, olo, ohi, PB[0], pld, olo, S.lamB, A.ctl->prof);
+    PROF_MARK(4);
+    // E columns t (rows of E^T, private): E^T[t] = sum_e Q2^T[t][e] Q1^T[e]
+    rows_gemm<C>(S, PB[1], pld, 0, PB[0], pld, ohi - olo, A.ws_Q1T, ld, n, n, nullptr);
+  } else {
+    for (int x = tid; x < (ohi - olo) * n; x += NT) {
+      const int t = olo + x / n, i = x % n;
+      prow(1, t)[i] = A.ws_Q1T[(int64_t)(n - 1 - t) * ld + i];
+    }
+    __syncthreads();
+  }
+  PROF_MARK(5);
   const double* lamF = edge ? S.lamB : S.lamA;
-  // final order t (descending): edge t = e; node t = n-1-e
-  auto lam_t = [&](int t) { return edge ? lamF[t] : lamF[n - 1 - t]; };
-  auto Erow = [&](int t) -> const double* {
-    return edge ? A.ws_ET + (int64_t)t * ld : A.ws_Q1T + (int64_t)(n - 1 - t) * ld;
-  };
   // ---- truncation (update_engine.cpp:39-52, svd.cpp:37-38) ----------------
-  for (int t = tid; t < n; t += NT) S.s2[t] = sqrt(fmax(lam_t(t), 0.0));
+  for (int t = tid; t < n; t += NT) S.s2[t] = sqrt(fmax(edge ? lamF[t] : lamF[n - 1 - t], 0.0));
   __syncthreads();
   int k2 = allow_grow ? n : k;
   while (k2 > 0 && S.s2[k2 - 1] <= 0.0) --k2;
   const double floor_ = k2 > 0 ? 1e-12 * S.s2[0] : 0.0;
   while (k2 > 0 && S.s2[k2 - 1] < floor_) --k2;
-  // ---- 4. per-column H, F, G, ex, ey, partial sums --------------------------
-  {
-    double* pH = S.vscr[0];  // reuse as accumulators (NW*NPAD doubles, need 2*k)
-    for (int i = tid; i < 2 * NPAD; i += NT) pH[i] = 0.0;
-    __syncthreads();
-    // warp per column t of this CTA (t < k2)
-    for (int t = tlo; t < min(thi, k2); ++t) {
-      const double* Et = Erow(t);
-      const double st_ = S.s2[t], rst = sqrt(st_);
-      // aE = a . E_t, bH = b . H_t computed by warp 0..1 then shared
-      double aE = 0;
-      for (int i = tid; i < n; i += NT) aE += S.av[i] * Et[i];
-      aE = block_sum(S, aE);
-      double bH = 0;
-      for (int i = tid; i < n; i += NT) {
-        const double Hi = (S.Dg[i] * Et[i] + S.bv[i] * aE) / st_;
-        A.ws_HT[(int64_t)t * ld + i] = Hi;
-        bH += S.bv[i] * Hi;
-        if (i < k) {
-          // F column t (A side): sqrt(sig_i) H_it / sqrt(s_t)
-          A.ws_FT[(int64_t)t * ld + i] = sqrt(S.sig[i]) * Hi / rst;
-          // G column t (B side)
-          A.ws_GT[(int64_t)t * ld + i] =
-              edge ? sqrt(S.sig[i]) * Et[i] / rst : Hi * rst / sqrt(S.sig[i]);
-        }
+  const int tend = min(ohi, k2);
+  // ---- 4. per-column H, F, G, ex, ey (one warp per owned column t) --------
+  for (int t = olo + warp; t < tend; t += NW) {
+    const double* Et = prow(1, t);
+    double* Ht = prow(2, t);
+    double* Ft = prow(0, t);
+    double* Gt = prow(3, t);
+    const double st_ = S.s2[t], rst = sqrt(st_), ist = 1.0 / st_, irst = 1.0 / rst;
+    double aE = 0;
+    for (int i = lane; i < n; i += 32) aE += S.av[i] * Et[i];
+    aE = warp_sum(aE);
+    double bH = 0;
+    for (int i = lane; i < n; i += 32) {
+      const double e_i = Et[i];
+      const double Hi = (S.Dg[i] * e_i + S.bv[i] * aE) * ist;
+      Ht[i] = Hi;
+      bH += S.bv[i] * Hi;
+      if (i < k) {
+        const double rs = sqrt(S.sig[i]);
+        Ft[i] = rs * Hi * irst;                             // F column t (A side)
+        Gt[i] = edge ? rs * e_i * irst : Hi * rst / rs;     // G column t (B side)
       }
-      bH = block_sum(S, bH);
-      const double dHt = (S.Dg[k] * Et[k] + S.bv[k] * aE) / st_;  // H[k][t]
-      const double dEt = Et[k];
-      double exv, eyv;
-      if (edge) {
-        exv = bH / rst;  // (b^T H_t)/sqrt(s_t)
-        eyv = aE / rst;  // (a^T E_t)/sqrt(s_t)
-      } else {
-        exv = dHt / rst;  // H[k][t]/sqrt(s_t)
-        eyv = dHt * rst;  // appended row value
-      }
-      if (tid < C) {
-        *cl.map_shared_rank(S.exv + t, tid) = exv;
-        *cl.map_shared_rank(S.eyv + t, tid) = eyv;
-        *cl.map_shared_rank(S.dH + t, tid) = dHt;
-        *cl.map_shared_rank(S.dE + t, tid) = dEt;
-      }
-      for (int i = tid; i < k; i += NT) {
-        pH[i] += A.ws_HT[(int64_t)t * ld + i] * dHt;
-        pH[NPAD + i] += Et[i] * dEt;
-      }
-      __syncthreads();
     }
-    // partial sums to every CTA
-    for (int x = tid; x < C * k; x += NT) {
-      const int r = x / k, i = x % k;
-      *cl.map_shared_rank(&S.partH[rank][i], r) = pH[i];
-      *cl.map_shared_rank(&S.partE[rank][i], r) = pH[NPAD + i];
+    bH = warp_sum(bH);
+    const double dHt = (S.Dg[k] * Et[k] + S.bv[k] * aE) * ist;  // H[k][t]
+    const double dEt = Et[k];
+    const double exv = edge ? bH * irst : dHt * irst;   // ex_t
+    const double eyv = edge ? aE * irst : dHt * rst;    // ey_t (edge) / appended row (node)
+    if (lane < C) {
+      *cl.map_shared_rank(S.exv + t, lane) = exv;
+      *cl.map_shared_rank(S.eyv + t, lane) = eyv;
+      *cl.map_shared_rank(S.dH + t, lane) = dHt;
+      *cl.map_shared_rank(S.dE + t, lane) = dEt;
     }
   }
-  cl.sync();
+  __syncthreads();
+  // partial column sums over this CTA's kept columns (local smem):
+  //  0: sum_t H[i][t] dH_t          (A_H d_H)
+  //  1: sum_t E[i][t] dE_t          (A_E d_E)
+  //  2: sum_t c_t w_t H[i][t]       (row fix, side A: c = ex, w = sqrt(s))
+  //  3: sum_t c_t w_t B[i][t]       (row fix, side B: edge c = ey, w = sqrt(s), B = E;
+  //                                  node c = vrow, w = 1/sqrt(s), B = H)
+  {
+    const int tk = min(ohi, k);
+    for (int i = tid; i < k; i += NT) {
+      double p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+      for (int t = olo; t < tk; ++t) {
+        const double Hi = prow(2, t)[i], Ei = prow(1, t)[i];
+        const double rs = sqrt(S.s2[t]);
+        p0 += Hi * S.dH[t];
+        p1 += Ei * S.dE[t];
+        p2 += S.exv[t] * rs * Hi;
+        p3 += edge ? S.eyv[t] * rs * Ei : S.eyv[t] / rs * Hi;
+      }
+      S.partL[0][i] = p0;
+      S.partL[1][i] = p1;
+      S.partL[2][i] = p2;
+      S.partL[3][i] = p3;
+    }
+    if (warp == 0) {
+      double q0 = 0, q1 = 0;
+      for (int t = olo + lane; t < tk; t += 32) {
+        const double rs = sqrt(S.s2[t]);
+        q0 += S.exv[t] * rs * S.dH[t];
+        q1 += edge ? S.eyv[t] * rs * S.dE[t] : S.eyv[t] / rs * S.dH[t];
+      }
+      q0 = warp_sum(q0);
+      q1 = warp_sum(q1);
+      if (lane == 0) {
+        S.partS[0] = q0;
+        S.partS[1] = q1;
+      }
+    }
+  }
+  cl.sync();  // B7a: partials complete in every CTA
+  PROF_MARK(6);
+  // reduce-scatter + all-gather over DSMEM: this CTA reduces its block of i
+  {
+    int lo, hi;
+    block_range(k, C, rank, lo, hi);
+    const int w = hi - lo;
+    for (int x = tid; x < 4 * w; x += NT) {
+      const int q = x / w, i = lo + x % w;
+      double s = 0;
+      for (int r = 0; r < C; ++r) s += *cl.map_shared_rank(&S.partL[q][i], r);
+      double* dst = q == 0 ? S.AHdH : q == 1 ? S.AEdE : q == 2 ? S.yA1 : S.yB1;
+      for (int r = 0; r < C; ++r) *cl.map_shared_rank(dst + i, r) = s;
+    }
+  }
+  double sA_ = 0, sB_ = 0;
+  for (int r = 0; r < C; ++r) {
+    sA_ += *cl.map_shared_rank(&S.partS[0], r);
+    sB_ += *cl.map_shared_rank(&S.partS[1], r);
+  }
+  cl.sync();  // B7b
+  PROF_MARK(7);
   double nH = 0, nE = 0;
   for (int t = tid; t < min(k2, k); t += NT) {
     nH += S.dH[t] * S.dH[t];
@@ -725,16 +899,6 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   }
   nH = block_sum(S, nH);
   nE = block_sum(S, nE);
-  for (int i = tid; i < k; i += NT) {
-    double a = 0, b = 0;
-    for (int r = 0; r < C; ++r) {
-      a += S.partH[r][i];
-      b += S.partE[r][i];
-    }
-    S.AHdH[i] = a;
-    S.AEdE[i] = b;
-  }
-  __syncthreads();
   const double gH = 1.0 - nH, gE = 1.0 - nE;
   const bool lazy = k2 == k && gH > 1e-10 && (!edge || gE > 1e-10);
   const int npp = 1 - S.pp[sA], nppB = 1 - S.pp[sB];
@@ -743,51 +907,80 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   double* QA_n = A.Q[sA][npp];
   double* QB_n = A.Q[sB][nppB];
   if (lazy) {
-    // ---- 5. inverse rows and the four GEMMs (this CTA's rows t) -----------
-    for (int t = tlo; t < min(thi, k); ++t) {
-      const double rst = sqrt(S.s2[t]);
-      for (int j = tid; j < k; j += NT) {
-        const double ahinv = A.ws_HT[(int64_t)t * ld + j] + S.dH[t] * S.AHdH[j] / gH;
-        A.ws_Fi[(int64_t)t * ld + j] = rst * ahinv / sqrt(S.sig[j]);
-        if (edge) {
-          const double aeinv = Erow(t)[j] + S.dE[t] * S.AEdE[j] / gE;
-          A.ws_Gi[(int64_t)t * ld + j] = rst * aeinv / sqrt(S.sig[j]);
-        } else {
-          A.ws_Gi[(int64_t)t * ld + j] = ahinv * sqrt(S.sig[j]) / rst;
+    const double igH = 1.0 / gH, igE = 1.0 / gE;
+    // ---- 5. row fixes from the OLD inverse: y = (ex F^-1) P_old^-1 ----------
+    //   ex F^-1 [m] = (1/sqrt(sig_m)) (sum_t ex_t sqrt(s_t) H[m][t]
+    //                                  + (A_H d_H)[m] / gH * sum_t ex_t sqrt(s_t) dH_t)
+    for (int m = tid; m < k; m += NT) {
+      const double rsm = sqrt(S.sig[m]);
+      S.yA1[m] = (S.yA1[m] + S.AHdH[m] * igH * sA_) / rsm;
+      S.yB1[m] = edge ? (S.yB1[m] + S.AEdE[m] * igE * sB_) / rsm
+                      : (S.yB1[m] + S.AHdH[m] * igH * sB_) * rsm;
+    }
+    __syncthreads();
+    {
+      int jlo, jhi;
+      block_range(k, C, rank, jlo, jhi);
+      for (int j = jlo + warp; j < jhi; j += NW) {
+        double ya = 0, yb = 0;
+        for (int m = lane; m < k; m += 32) {
+          ya += S.yA1[m] * QA[(int64_t)m * ld + j];
+          yb += S.yB1[m] * QB[(int64_t)m * ld + j];
+        }
+        ya = warp_sum(ya);
+        yb = warp_sum(yb);
+        if (lane == 0) {
+          for (int q = 0; q < st.nb; ++q) {
+            float* r = baseA + A.sp_rows[st.b_off + q] * (int64_t)d + j;
+            *r = (float)((double)*r + A.sp_vals[st.b_off + q] * ya);
+          }
+          if (edge) {
+            float* r = baseB + st.c_row * (int64_t)d + j;
+            *r = (float)((double)*r + st.c_val * yb);
+          } else {
+            baseB[st.c_row * (int64_t)d + j] = (float)yb;  // appended row
+          }
         }
       }
     }
-    __syncthreads();
-    const int t1 = min(thi, k);
-    double fro[4];
-    rows_gemm<C>(S, PTA_n, ld, A.ws_FT, ld, PTA, ld, tlo, t1, k, k, &fro[0]);
-    rows_gemm<C>(S, QA_n, ld, A.ws_Fi, ld, QA, ld, tlo, t1, k, k, &fro[1]);
-    rows_gemm<C>(S, PTB_n, ld, A.ws_GT, ld, PTB, ld, tlo, t1, k, k, &fro[2]);
-    rows_gemm<C>(S, QB_n, ld, A.ws_Gi, ld, QB, ld, tlo, t1, k, k, &fro[3]);
-    if (tid < C)
-      for (int q = 0; q < 4; ++q) *cl.map_shared_rank(&S.pnorm[rank][q], tid) = fro[q];
-    cl.sync();
-    // ---- 6. row fixes: base[row] += val * (ex Q_new), this CTA's columns ----
-    int jlo, jhi;
-    block_range(k, C, rank, jlo, jhi);
-    for (int j = jlo + tid; j < jhi; j += NT) {
-      double ya = 0, yb = 0;
-      for (int t = 0; t < k; ++t) {
-        ya += S.exv[t] * QA_n[(int64_t)t * ld + j];
-        yb += S.eyv[t] * QB_n[(int64_t)t * ld + j];
-      }
-      for (int q = 0; q < st.nb; ++q) {
-        float* r = baseA + A.sp_rows[st.b_off + q] * (int64_t)d + j;
-        *r = (float)((double)*r + A.sp_vals[st.b_off + q] * ya);
-      }
-      if (edge) {
-        float* r = baseB + st.c_row * (int64_t)d + j;
-        *r = (float)((double)*r + st.c_val * yb);
-      } else {
-        baseB[st.c_row * (int64_t)d + j] = (float)yb;  // appended row
-      }
+    // ---- inverse rows (private, in place) ----------------------------------
+    //   F^-1[t][m] = sqrt(s_t) (H[m][t] + dH_t (A_H d_H)[m]/gH) / sqrt(sig_m)
+    //   edge: G^-1[t][m] = sqrt(s_t) (E[m][t] + dE_t (A_E d_E)[m]/gE) / sqrt(sig_m)
+    //   node: G^-1[t][m] = (H[m][t] + dH_t (A_H d_H)[m]/gH) sqrt(sig_m) / sqrt(s_t)
+    const int fbuf = edge ? 2 : 1, gbuf = edge ? 1 : 2;
+    for (int x = tid; x < (kohi - olo) * k; x += NT) {
+      const int t = olo + x / k, m = x % k;
+      const double rst = sqrt(S.s2[t]), rsm = sqrt(S.sig[m]);
+      const double ahinv = prow(2, t)[m] + S.dH[t] * S.AHdH[m] * igH;
+      double gi;
+      if (edge)
+        gi = rst * (prow(1, t)[m] + S.dE[t] * S.AEdE[m] * igE) / rsm;
+      else
+        gi = ahinv * rsm / rst;
+      prow(fbuf, t)[m] = rst * ahinv / rsm;  // edge: over H (read above); node: over E
+      prow(gbuf, t)[m] = gi;                 // edge: over E (read above); node: over H
     }
+    __syncthreads();
+    PROF_MARK(8);
+    // ---- the four GEMMs on the FP64 tensor cores (owned rows t) -------------
+    const int nt = kohi - olo;
+    double fro[4];
+    rows_gemm<C>(S, PTA_n, ld, olo, prow(0, olo), pld, nt, PTA, ld, k, k, &fro[0]);
+    rows_gemm<C>(S, QA_n, ld, olo, prow(fbuf, olo), pld, nt, QA, ld, k, k, &fro[1]);
+    rows_gemm<C>(S, PTB_n, ld, olo, prow(3, olo), pld, nt, PTB, ld, k, k, &fro[2]);
+    rows_gemm<C>(S, QB_n, ld, olo, prow(gbuf, olo), pld, nt, QB, ld, k, k, &fro[3]);
+    if (tid < 4) *cl.map_shared_rank(&S.pnorm[rank][tid], 0) = fro[tid];
+    if (rank == 0)
+      for (int t = tid; t < k; t += NT) A.sigma[t] = S.s2[t];
+    S.pp[sA] = npp;
+    S.pp[sB] = nppB;
+    PROF_MARK(9);
+    cl.sync();  // B8: new P^T, P^-1, rows and sigma visible
+    PROF_MARK(10);
     if (rank == 0 && tid == 0) {
+      A.ctl->pp[sA] = npp;
+      A.ctl->pp[sB] = nppB;
+      A.ctl->rank1 += 1;
       // cond(P_X) <= |P_X|_F |P_X^-1|_F (query-transparent rebase policy)
       const int xA = sA == 0;
       double p2 = 0, q2 = 0;
@@ -798,24 +991,12 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       A.ctl->cond_est = sqrt(p2) * sqrt(q2);
       if (A.ctl->cond_est > A.rebase_cond) A.ctl->need_rebase = 1;
     }
-    if (rank == 0)
-      for (int t = tid; t < k; t += NT) A.sigma[t] = S.s2[t];
-    S.pp[sA] = npp;
-    S.pp[sB] = nppB;
-    if (rank == 0 && tid == 0) {
-      A.ctl->pp[sA] = npp;
-      A.ctl->pp[sB] = nppB;
-      A.ctl->rank1 += 1;
-    }
   } else {
     // ---- eager fold (rank change or ill-conditioned step) ------------------
-    // T_A = P_A F_top (k x k2), T_B = P_B G_top; stored transposed in the new
-    // PT buffers: TT[t][i] = sum_m F[m][t] PT[i][m]... computed as rows of
-    // (F^T P^T): TT[t][:] = sum_m FT[t][m] PT[m][:].
-    rows_gemm<C>(S, PTA_n, ld, A.ws_FT, ld, PTA, ld, tlo, min(thi, k2), k, k, nullptr);
-    rows_gemm<C>(S, PTB_n, ld, A.ws_GT, ld, PTB, ld, tlo, min(thi, k2), k, k, nullptr);
+    // T_A = P_A F_top (k x k2), stored transposed: TT[t][:] = sum_m FT[t][m] PT[m][:]
+    rows_gemm<C>(S, PTA_n, ld, olo, prow(0, olo), pld, tend - olo, PTA, ld, k, k, nullptr);
+    rows_gemm<C>(S, PTB_n, ld, olo, prow(3, olo), pld, tend - olo, PTB, ld, k, k, nullptr);
     cl.sync();
-    // fold every row of both sides (and Z_b, r_b with the X-side transform)
     const int nmat = A.alpha_is_one ? 2 : 4;
     for (int mat = 0; mat < nmat; ++mat) {
       float* base;
@@ -887,6 +1068,7 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     S.pp[sA] = npp;
     S.pp[sB] = nppB;
     S.k = k2;
+    cl.sync();
     if (rank == 0 && tid == 0) {
       A.ctl->pp[sA] = npp;
       A.ctl->pp[sB] = nppB;
@@ -903,7 +1085,7 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     else
       A.ctl->rows_y += 1;
   }
-  cl.sync();
+  PROF_MARK(11);
 }
 
 }  // namespace
@@ -926,6 +1108,7 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     const EventDesc ev = A.ev[e];
     if (A.t_begin && rank == 0 && threadIdx.x == 0) A.t_begin[e] = globaltimer();
     int err = 0;
+    long long _pt = clock64();
     // ---- graph mutation (graph.cpp:83-185) -----------------------------
     if (ev.kind == 1) {  // AddEdge
       const bool two = A.undirected && ev.u != ev.v;
@@ -1021,6 +1204,7 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     for (int r = 0; r < C; ++r) any |= *cl.map_shared_rank(&S.err, r);
     cl.sync();
     if (any) break;
+    PROF_MARK(12);
     // ---- factor update (update_engine.cpp:206-226) ----------------------
     if (!(A.mode & 1)) {
       for (int s = 0; s < ev.nsteps; ++s) {

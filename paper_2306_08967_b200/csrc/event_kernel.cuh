@@ -36,15 +36,10 @@ struct EventKernelArgs {
   DevCSR out, in;
   int directed, undirected;
   double* deg;
-  // workspace (fp64, ld x ld each)
+  // workspace (fp64): Q1^T (ld x ld, shared by the cluster) and, for d > 128,
+  // the per-CTA private matrices (4 x C x (ceil(257/C)+1) x ld)
   double* ws_Q1T;
-  double* ws_Q2T;
-  double* ws_ET;
-  double* ws_HT;
-  double* ws_FT;
-  double* ws_GT;
-  double* ws_Fi;
-  double* ws_Gi;
+  double* ws_priv;
 };
 
 cudaError_t launch_event_kernel(const EventKernelArgs& a, cudaStream_t s);

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(PT_) ppr_push_kernel(PprArgs A) {
   const int k = A.ctl->k, d = A.d;
   const float thr = (float)(A.alpha_eps / *A.smax);
   const double om = 1.0 - A.alpha;
-  int R = A.round_base;
+  int R = (int)A.stats[2];  // device-resident round stamp base (monotonic)
   // initial frontier
   int nF;
   if (A.ncand >= 0) {

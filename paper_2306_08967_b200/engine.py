@@ -111,6 +111,7 @@ def lib():
         L.damf_gpu_stream.argtypes = [vp]
         L.damf_gpu_stream.restype = C.c_void_p
         L.damf_gpu_push_counters.argtypes = [vp, i64p]
+        L.damf_gpu_profile_counters.argtypes = [vp, C.POINTER(C.c_uint64)]
         L.damf_materialize_dev.argtypes = [vp, C.c_int64, C.c_int64, f64p, vp, vp, f32p]
         _lib = L
     return _lib
@@ -269,6 +270,11 @@ class Engine:
         self._check(lib().damf_gpu_push_counters(self.h, _p(out, i64p)))
         return dict(frontier=int(out[0]), affected=int(out[1]), affected_arcs=int(out[2]),
                     pulled_arcs=int(out[3]))
+
+    def profile_counters(self):
+        out = np.zeros(32, np.uint64)
+        self._check(lib().damf_gpu_profile_counters(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
 
     def stream_ptr(self):
         return lib().damf_gpu_stream(self.h)

@@ -74,6 +74,24 @@ def test_defect_bound_after_structural_churn(seed):
     assert worst <= 1e-5 * (1 + 1e-6) + 2e-7
 
 
+def test_defect_bound_holds_for_batched_streams():
+    # many events per apply() call (round stamps, keys and s_max stay on the
+    # device across events); the bound is checked after the whole batch and
+    # the push counts are compared with the reference FIFO order
+    g, ev = oracle.gen_mixed_stream(300, 250, 1200, 200, 99)
+    oe = oracle.OracleEngine(g, d=12, alpha=0.2, eps=1e-6, seed=99)
+    e = gpu_from_oracle(g, oe, d=12, alpha=0.2, eps=1e-6)
+    p0 = oe.stat(5)
+    st = e.apply(ev)
+    oe.apply(ev)
+    off, ids, deg = e.graph_sets()
+    dfc = dense_defect(e.n, off, ids, deg, e.get(ge.X), e.get(ge.Z), 0.2)
+    print("defect", dfc, "gpu pushes", st["pushes"], "oracle pushes", oe.stat(5) - p0)
+    assert dfc <= 1e-6 * (1 + 1e-6) + 2e-7
+    # frontier-synchronous rounds push more than FIFO (~1.8x)
+    assert st["pushes"] <= 6 * (oe.stat(5) - p0) + 1000
+
+
 def test_materialize_matches_fp64():
     import torch
     rng = np.random.default_rng(3)

@@ -1,0 +1,38 @@
+"""Dev profiling helper: per-event latency of the cfg2 stream with and
+without the PPR enhancer (alpha = 1 bypasses it), for kernel breakdowns."""
+import sys, os, time, json
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench
+from paper_2306_08967_b200 import engine as ge
+
+nev = int(sys.argv[1]) if len(sys.argv) > 1 else 300
+alphas = [float(a) for a in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1.0, 0.15]
+d = bench.build_cfg2()
+w = d["w"]
+for alpha in alphas:
+    k = len(d["sig"])
+    e = ge.Engine(d["n"], d["off"], d["tgt"], None, w["d"], k, d["xb"], d["yb"], np.eye(k), np.eye(k),
+                  d["sig"], alpha=alpha, eps=w["eps"], undirected=True, node_capacity=4096)
+    s = w["stream"]
+    e.apply(s.slice(0, 50))
+    t0 = time.perf_counter()
+    st = e.apply(s.slice(50, 50 + nev), mode=ge.APPLY_TIME_EVENTS)
+    t1 = time.perf_counter()
+    lat = e.latencies_us()
+    kinds = s.kind[50:50 + nev]
+    out = {"alpha": alpha, "events": nev, "wall_ms": (t1 - t0) * 1e3, "p50_us": float(np.median(lat)),
+           "mean_us": float(lat.mean()), "stats": st}
+    for kk, nm in ((0, "node"), (1, "add"), (2, "remove")):
+        if np.any(kinds == kk):
+            out[nm + "_p50_us"] = float(np.median(lat[kinds == kk]))
+    pc = e.profile_counters().astype(np.float64)
+    names = ["gather+w", "prep", "eigA", "z2", "eigB", "E-gemm", "cols", "inv-rows", "gemms",
+             "sync9", "rowfix", "tail", "graph"]
+    out["phase_us_per_event"] = {nm: round(pc[i] / 1.965e3 / (nev + 50), 2) for i, nm in enumerate(names)}
+    en = ["eig.prep", "eig.roots", "eig.sync1", "eig.zhat", "eig.sync2", "eig.order", "eig.vecs"]
+    out["eig_us_per_event"] = {nm: round(pc[16 + i] / 1.965e3 / (nev + 50), 2) for i, nm in enumerate(en)}
+    out["root_iters_mean"] = float(pc[13] / max(pc[14], 1))
+    out["root_iters_max"] = int(pc[15])
+    print(json.dumps(out))
+    e.close()
