@@ -201,6 +201,9 @@ struct damf_gpu {
   float *Xb = nullptr, *Yb = nullptr, *Zb = nullptr, *rb = nullptr, *delta = nullptr,
         *key = nullptr;
   int *stamp = nullptr, *mark = nullptr, *listF = nullptr, *listL = nullptr, *blk = nullptr;
+  long long* blk64 = nullptr;
+  int *heavy = nullptr, *hidx = nullptr, *hoff = nullptr, *hact = nullptr;
+  float* hpart = nullptr;
   double* PT[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   double* Q[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   double* sigma = nullptr;
@@ -302,6 +305,12 @@ PprArgs ppr_args(damf_gpu* h) {
   a.listF = h->listF;
   a.listL = h->listL;
   a.blk = h->blk;
+  a.blk64 = h->blk64;
+  a.heavy = h->heavy;
+  a.hidx = h->hidx;
+  a.hoff = h->hoff;
+  a.hact = h->hact;
+  a.hpart = h->hpart;
   a.out = h->out;
   a.in = h->in;
   a.directed = h->directed;
@@ -339,7 +348,7 @@ int run_push(damf_gpu* h, int grid, unsigned long long* t_end) {
   CK(launch_smax(h->PT[0][0], h->PT[0][1], h->ctl, h->ld, h->smax, h->st));
   PprArgs a = ppr_args(h);
   a.t_end = t_end;
-  const int gmax = ppr_push_max_grid(h->nsm);
+  const int gmax = ppr_push_max_grid(h->nsm, h->d);
   CK(launch_ppr_push(a, std::min(grid, gmax), h->st));
   return 0;
 }
@@ -571,6 +580,20 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
     CK(dalloc(h, &h->listF, (size_t)ncap));
     CK(dalloc(h, &h->listL, (size_t)ncap));
     CK(dalloc(h, &h->blk, (size_t)4096));
+    CK(dalloc(h, &h->blk64, (size_t)4096));
+    CK(dalloc(h, &h->heavy, (size_t)ncap));
+    CK(dalloc(h, &h->hidx, (size_t)ncap));
+    CK(dalloc(h, &h->hoff, (size_t)ncap + 1));
+    CK(dalloc(h, &h->hact, (size_t)ncap));
+    CK(cudaMemsetAsync(h->hidx, 0xff, (size_t)ncap * 4, h->st));
+    CK(cudaMemsetAsync(h->hact, 0, (size_t)ncap * 4, h->st));
+    {
+      // chunk partials: every heavy row contributes ceil(cnt/1024) <= cnt/1024 + 1
+      // chunks; bounded by (pool slots / 1024 + heavy rows) with heavy rows
+      // having > 2048 arcs, i.e. <= pool/1024 + pool/2048.
+      const size_t chunks = (size_t)(h->out.pool_size / 1024 + h->out.pool_size / 2048 + 16);
+      CK(dalloc(h, &h->hpart, chunks * (size_t)d));
+    }
     CK(cudaMemsetAsync(h->Zb, 0, (size_t)ncap * d * 4, h->st));
     CK(cudaMemsetAsync(h->rb, 0, (size_t)ncap * d * 4, h->st));
     CK(cudaMemsetAsync(h->key, 0, (size_t)ncap * 4, h->st));

@@ -16,6 +16,12 @@ struct PprArgs {
   int* listF;
   int* listL;
   int* blk;
+  long long* blk64;   // per-block push counts (gridDim)
+  int* heavy;         // heavy-row list (n)
+  int* hidx;          // row -> heavy index or -1 (n, kept at -1 between calls)
+  int* hoff;          // heavy chunk prefix (n+1)
+  int* hact;          // heavy row active stamp (n)
+  float* hpart;       // chunk partial sums (arcs/CH + n) x d
   DevCSR out, in;
   int directed;
   double* deg;
@@ -33,7 +39,7 @@ struct PprArgs {
 };
 
 cudaError_t launch_ppr_push(const PprArgs& a, int grid, cudaStream_t s);
-int ppr_push_max_grid(int nsm);
+int ppr_push_max_grid(int nsm, int d);
 cudaError_t launch_ppr_absorb(const PprArgs& a, const int64_t* rows, int nrows, cudaStream_t s);
 cudaError_t launch_ppr_keys(const PprArgs& a, int nsm, cudaStream_t s);
 cudaError_t launch_ppr_init(const PprArgs& a, int nsm, cudaStream_t s);
