@@ -272,6 +272,16 @@ EventKernelArgs event_args(damf_gpu* h) {
   a.rb = h->rb;
   a.alpha_is_one = h->alpha1;
   a.key = h->key;
+  a.fused_ppr = 0;
+  a.alpha = h->cfg.alpha;
+  a.eps = h->cfg.eps;
+  a.delta = h->delta;
+  a.stamp = h->stamp;
+  a.mark = h->mark;
+  a.listF = h->listF;
+  a.listL = h->listL;
+  a.touched = h->touched.d;
+  a.pstats = h->pstats;
   for (int s = 0; s < 2; ++s)
     for (int p = 0; p < 2; ++p) {
       a.PT[s][p] = h->PT[s][p];
@@ -577,8 +587,9 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
     CK(dalloc(h, &h->key, (size_t)ncap));
     CK(dalloc(h, &h->stamp, (size_t)ncap));
     CK(dalloc(h, &h->mark, (size_t)ncap));
-    CK(dalloc(h, &h->listF, (size_t)ncap));
-    CK(dalloc(h, &h->listL, (size_t)ncap));
+    // fused in-cluster lists: C regions of (ceil(ceil(n/32)/C)*32/NW + 1)*NW
+    CK(dalloc(h, &h->listF, (size_t)ncap + 16 * 32 * 2 + 4096));
+    CK(dalloc(h, &h->listL, (size_t)ncap + 16 * 32 * 2 + 4096));
     CK(dalloc(h, &h->blk, (size_t)4096));
     CK(dalloc(h, &h->blk64, (size_t)4096));
     CK(dalloc(h, &h->heavy, (size_t)ncap));
@@ -879,9 +890,14 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     // events up to the next rebase_every boundary (engine.cpp:37-40)
     int64_t j = ok_count;
     if (h->cfg.rebase_every > 0) j = std::min<int64_t>(j, i + (h->cfg.rebase_every - h->since_rebase));
-    if (!ppr) {
+    // In-cluster enhancer when its per-round row scans are cheap (n <= 1M) or
+    // when only absorption is requested; otherwise one cooperative push
+    // kernel per event over the whole GPU.
+    const bool fused = ppr && (h->n_cap <= (1 << 20) || (mode & DAMF_APPLY_DEFER_PUSH));
+    if (!ppr || fused) {
       ea.e_begin = i;
       ea.e_end = j;
+      ea.fused_ppr = fused ? 1 : 0;
       CK(launch_event_kernel(ea, h->st));
       h->launches += 1;
     } else {

@@ -1090,6 +1090,295 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
 
 }  // namespace
 
+// ------------------------------------------------------- fused PPR (cluster)
+// For streaming events the enhancer work of one event is small (a few
+// touched rows, frontiers of tens to hundreds of rows), so it runs inside
+// the same cluster right after the factor update: absorb_structure_delta
+// (enhancer.cpp:77-96), s_max = proj_row_bound(P_X) (factor_state.cpp:
+// 251-259) and the frontier-synchronous pull push (enhancer.cpp:98-157
+// semantics, see ppr.cu). CTA c owns the row chunk [c*n/C, (c+1)*n/C): its
+// frontier / affected lists never leave the CTA, so each round needs only
+// two cluster barriers (after the pushes, after the pulls + count).
+template <int C>
+DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& cl,
+                      const EventDesc& ev) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = (int)cl.block_rank();
+  const int k = S.k, d = A.d;
+  const double alpha = A.alpha, om = 1.0 - alpha;
+  long long _pt = clock64();
+  // ---- absorb_structure_delta for the touched rows (warp per row)
+  for (int q = rank * NW + warp; q < ev.touched_cnt; q += C * NW) {
+    const int64_t u = A.touched[ev.touched_off + q];
+    float acc[kMaxD / 32];
+#pragma unroll
+    for (int t = 0; t < kMaxD / 32; ++t) acc[t] = 0.0f;
+    const int64_t base = A.out.off[u];
+    const int c = A.out.cnt[u];
+    for (int p = 0; p < c; ++p) {
+      const int v = A.out.ids[base + p];
+      const float w = A.out.wts ? (float)A.out.wts[base + p] : 1.0f;
+#pragma unroll
+      for (int t = 0; t < kMaxD / 32; ++t) {
+        const int j = lane + 32 * t;
+        if (j < k) acc[t] = fmaf(w, A.Zb[(int64_t)v * d + j], acc[t]);
+      }
+    }
+    const double deg = A.deg[u];
+    float m = 0.0f;
+#pragma unroll
+    for (int t = 0; t < kMaxD / 32; ++t) {
+      const int j = lane + 32 * t;
+      if (j < k) {
+        float r = (float)alpha * A.Xb[u * d + j] - A.Zb[u * d + j];
+        if (deg > 0.0) r += (float)(om / deg) * acc[t];
+        A.rb[u * d + j] = r;
+        m = fmaxf(m, fabsf(r));
+      }
+    }
+    m = warp_max(m);
+    if (lane == 0) A.key[u] = (float)((double)m / fmax(deg, 1.0));
+  }
+  PROF_MARK(23);
+  if (A.mode & 2) return;  // DAMF_APPLY_DEFER_PUSH: absorb only
+  // ---- s_max from P_X: col1 = max_j sum_i |P_ij| (rows of PT), rowinf = max_i sum_j |P_ij|
+  {
+    const double* PT = A.PT[0][S.pp[0]];
+    int lo, hi;
+    block_range(k, C, rank, lo, hi);
+    double c1 = 0;
+    for (int j = lo + warp; j < hi; j += NW) {
+      double s = 0;
+      for (int i = lane; i < k; i += 32) s += fabs(PT[(int64_t)j * A.ld + i]);
+      c1 = fmax(c1, warp_sum(s));
+    }
+    for (int i = tid; i < k; i += NT) {
+      double s = 0;
+      for (int j = lo; j < hi; ++j) s += fabs(PT[(int64_t)j * A.ld + i]);
+      S.partL[0][i] = s;
+    }
+    if (lane == 0) S.bred[warp] = c1;
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0;
+      for (int w = 0; w < NW; ++w) m = fmax(m, S.bred[w]);
+      S.partS[2] = m;
+    }
+  }
+  cl.sync();
+  double col1 = 0, rowinf = 0;
+  for (int r = 0; r < C; ++r) col1 = fmax(col1, *cl.map_shared_rank(&S.partS[2], r));
+  for (int i = tid; i < k; i += NT) {
+    double s = 0;
+    for (int r = 0; r < C; ++r) s += *cl.map_shared_rank(&S.partL[0][i], r);
+    rowinf = fmax(rowinf, s);
+  }
+  rowinf = warp_sum(0.0) + rowinf;  // keep lanes converged
+  {
+    double m = rowinf;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) S.bred[warp] = m;
+    __syncthreads();
+    m = 0;
+    for (int w = 0; w < NW; ++w) m = fmax(m, S.bred[w]);
+    rowinf = m;
+  }
+  const double smax = k == 0 ? 1.0 : fmax(col1, sqrt(col1 * rowinf));
+  const float thr = (float)(alpha * A.eps / smax);
+  PROF_MARK(24);
+  // ---- rounds (scatter form: small frontiers, no dependent pull chains)
+  //   P1  candidate rows (own chunk): key from r (first round: stored key);
+  //       over threshold -> delta = r, r = 0, Z += delta, key = 0
+  //   --- barrier (frontier counts) ---
+  //   P2  every pushed u: r[v] += (1-alpha) w / max(deg v, 1) * delta_u for
+  //       v in in(u) (red.global.add), mark[v] = R
+  //   --- barrier ---
+  //   next candidates: own-chunk rows marked this round
+  // Float reductions make the fp32 summation order nondeterministic; the
+  // defect bound (the reference's contract) is unaffected.
+  const int n = (int)A.ctl->rows_x;
+  // block-cyclic ownership: CTA `rank` owns the 32-row blocks b = rank + C*i
+  // (balances hot regions; each block is one coalesced 128-byte scan)
+  const int nblk = (n + 31) >> 5;
+  const int myblk = nblk > rank ? (nblk - rank + C - 1) / C : 0;
+  const int maxmine = ((nblk + C - 1) / C) * 32;
+  const int seg = (maxmine + NW - 1) / NW + 1;  // per-warp segment
+  const int stride = seg * NW;                   // uniform per-CTA list region
+  int* Fl = A.listF + (int64_t)rank * stride;
+  int* Ll = A.listL + (int64_t)rank * stride;
+  int R = (int)A.pstats[2];
+  long long pushes = 0;
+  int rounds = 0;
+  __shared__ int s_cnt[NW + 1];
+  // warp-per-block ballot compaction of own rows into per-warp segments of
+  // `out`, then an in-place gather into a contiguous, order-preserving list
+  auto compact = [&](auto pred, int* out) -> int {
+    int mycnt = 0;
+    constexpr int U = 4;
+    for (int b0 = warp; b0 < myblk; b0 += NW * U) {
+      bool hit[U];
+      int v[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int bi = b0 + q * NW;
+        v[q] = bi < myblk ? ((rank + C * bi) << 5) + lane : n;
+        hit[q] = v[q] < n && pred(v[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const unsigned ball = __ballot_sync(0xffffffffu, hit[q]);
+        if (hit[q]) out[warp * seg + mycnt + __popc(ball & ((1u << lane) - 1u))] = v[q];
+        mycnt += __popc(ball);
+      }
+    }
+    if (lane == 0) s_cnt[warp] = mycnt;
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < NW; ++w) {
+      if (w < warp) off += s_cnt[w];
+      tot += s_cnt[w];
+    }
+    // gather segments to the front (segments are disjoint and ordered by warp;
+    // warp w's destination [off, off+cnt) never overlaps a later segment's
+    // unread source because off <= w*seg)
+    for (int w = 1; w < NW; ++w) {
+      __syncthreads();
+      if (warp == w)
+        for (int i = lane; i < mycnt; i += 32) out[off + i] = out[w * seg + i];
+    }
+    __syncthreads();
+    return tot;
+  };
+  cl.sync();  // touched-row residuals and keys visible
+  // first candidates: own rows whose stored key is over threshold
+  int ncand = compact([&](int v) { return A.key[v] > thr; }, Ll);
+  bool first = true;
+  PROF_MARK(25);
+  for (;;) {
+    // P1: evaluate candidates (warp per row, 2 rows in flight), push the ones
+    // over threshold into this warp's segment of Fl
+    int myF = 0;
+    for (int q = warp; q < ncand; q += 2 * NW) {
+      int vv[2];
+      float rj[2][kMaxD / 32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int qq = q + h * NW;
+        vv[h] = qq < ncand ? Ll[qq] : -1;
+        const float* rv = A.rb + (int64_t)(vv[h] < 0 ? 0 : vv[h]) * d;
+#pragma unroll
+        for (int t = 0; t < kMaxD / 32; ++t) {
+          const int j = lane + 32 * t;
+          rj[h][t] = (vv[h] >= 0 && j < k) ? rv[j] : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int v = vv[h];
+        if (v < 0) continue;
+        float m = 0.0f;
+#pragma unroll
+        for (int t = 0; t < kMaxD / 32; ++t) m = fmaxf(m, fabsf(rj[h][t]));
+        m = warp_max(m);
+        const double degv = A.deg[v];
+        const float key = (float)((double)m / fmax(degv, 1.0));
+        const bool push = first ? A.key[v] > thr : key > thr;
+        if (!push) {
+          if (lane == 0) A.key[v] = key;
+          continue;
+        }
+        float* du = A.delta + (int64_t)v * d;
+        float* zu = A.Zb + (int64_t)v * d;
+        float* rv = A.rb + (int64_t)v * d;
+#pragma unroll
+        for (int t = 0; t < kMaxD / 32; ++t) {
+          const int j = lane + 32 * t;
+          if (j < k) {
+            du[j] = rj[h][t];
+            zu[j] += rj[h][t];
+            rv[j] = 0.0f;
+          }
+        }
+        if (lane == 0) {
+          A.key[v] = 0.0f;
+          Fl[warp * seg + myF] = v;
+        }
+        ++myF;
+      }
+    }
+    first = false;
+    if (lane == 0) s_cnt[warp] = myF;
+    __syncthreads();
+    int nF = 0;
+    for (int w = 0; w < NW; ++w) nF += s_cnt[w];
+    PROF_MARK(26);
+    if (tid == 0)
+      for (int r = 0; r < C; ++r) *cl.map_shared_rank(&S.found[rank][0], r) = nF;
+    cl.sync();  // all residuals of this round's frontier are read and zeroed
+    PROF_MARK(27);
+    long long tot = 0;
+    for (int r = 0; r < C; ++r) tot += S.found[r][0];
+    if (tot == 0) break;
+    ++R;
+    ++rounds;
+    pushes += tot;
+    if (pushes > 1000000000LL) {
+      if (rank == 0 && tid == 0) A.ctl->err = 9;  // NonConvergence
+      break;
+    }
+    // P2: scatter (1-alpha) w / max(deg v,1) delta_u into r[v], v in in(u)
+    const DevCSR& in = A.directed ? A.in : A.out;
+    for (int q = warp; q < nF; q += NW) {
+      int sw = 0, qq = q;
+      while (qq >= s_cnt[sw]) qq -= s_cnt[sw++];
+      const int u = Fl[sw * seg + qq];
+      float du[kMaxD / 32];
+#pragma unroll
+      for (int t = 0; t < kMaxD / 32; ++t) {
+        const int j = lane + 32 * t;
+        du[t] = j < k ? A.delta[(int64_t)u * d + j] : 0.0f;
+      }
+      const int64_t ib = in.off[u];
+      const int c = in.cnt[u];
+      for (int p0 = 0; p0 < c; p0 += 32) {
+        const int p = p0 + lane;
+        int v = -1;
+        float cf = 0.0f;
+        if (p < c) {
+          v = in.ids[ib + p];
+          const float w = in.wts ? (float)in.wts[ib + p] : 1.0f;
+          cf = (float)(om * w / fmax(A.deg[v], 1.0));
+          A.mark[v] = R;
+        }
+        const int cnt = min(32, c - p0);
+        for (int s2 = 0; s2 < cnt; ++s2) {
+          const int vv = __shfl_sync(0xffffffffu, v, s2);
+          const float cc = __shfl_sync(0xffffffffu, cf, s2);
+          float* rv = A.rb + (int64_t)vv * d;
+#pragma unroll
+          for (int t = 0; t < kMaxD / 32; ++t) {
+            const int j = lane + 32 * t;
+            if (j < k) atomicAdd(rv + j, cc * du[t]);  // RED.ADD.F32
+          }
+        }
+      }
+    }
+    PROF_MARK(28);
+    cl.sync();  // contributions landed
+    PROF_MARK(29);
+    // next candidates: own rows marked this round
+    ncand = compact([&](int v) { return A.mark[v] == R; }, Ll);
+    PROF_MARK(30);
+  }
+  if (rank == 0 && tid == 0) {
+    A.pstats[0] += pushes;
+    A.pstats[1] += rounds;
+    A.pstats[2] = R;
+    A.pstats[3] += pushes;
+  }
+  cl.sync();
+}
+
 // ------------------------------------------------------------------ kernel
 template <int C>
 __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
@@ -1211,6 +1500,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
         const StepDesc st = A.steps[ev.step0 + s];
         rank1_step<C>(A, S, cl, st);
       }
+    }
+    if (A.fused_ppr) {
+      cl.sync();  // factor / graph writes visible to the enhancer
+      ppr_event<C>(A, S, cl, ev);
     }
     if (A.t_end && rank == 0 && threadIdx.x == 0) A.t_end[e] = globaltimer();
   }

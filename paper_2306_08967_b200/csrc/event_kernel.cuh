@@ -28,6 +28,16 @@ struct EventKernelArgs {
   float* rb;
   float* key;  // enhancer residual keys (refreshed on folds)
   int alpha_is_one;
+  // fused per-event enhancer (alpha < 1, n small enough for in-cluster scans)
+  int fused_ppr;
+  double alpha, eps;
+  float* delta;
+  int* stamp;
+  int* mark;
+  int* listF;
+  int* listL;
+  const int64_t* touched;
+  long long* pstats;
   double* PT[2][2];  // [side X/Y][ping-pong]  P transposed
   double* Q[2][2];   // [side][ping-pong]      P^-1
   double* sigma;
