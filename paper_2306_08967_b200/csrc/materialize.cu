@@ -96,12 +96,35 @@ __global__ void __launch_bounds__(MT, 1)
 
 size_t materialize_smem(int k) { return ((size_t)k * CB + (size_t)RT * ((k + 3) & ~3)) * 4; }
 
+namespace {
+// F = P (fp64, given transposed) -> exact-TF32 hi part and fp32 lo part, both
+// in the FT layout the tensor-core kernel stages (row j = output column j).
+__global__ void split_f_kernel(const double* FT, int ldf, int k, float* hi, float* lo) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < k * k; x += gridDim.x * blockDim.x) {
+    const int j = x / k, m = x % k;
+    const double f = FT[(int64_t)j * ldf + m];
+    const float h = __uint_as_float(__float_as_uint((float)f) & 0xFFFFE000u);
+    hi[x] = h;
+    lo[x] = (float)(f - (double)h);
+  }
+}
+float* g_fsplit = nullptr;
+}  // namespace
+
 // Z[:, :k2] = X[:, :k] * F, F given transposed (FT[c][m] = F[m][c], fp64 on
 // device). In-place (Z == X) requires k2 <= CB so one pass covers all
 // output columns.
 cudaError_t launch_materialize(const float* X, int64_t n, int k, int ldx, const double* FT,
                                int ldf, int k2, float* Z, int ldz, cudaStream_t s, int nsm) {
   if (n <= 0 || k2 <= 0) return cudaSuccess;
+  if (k2 == k && materialize_tc_supported(k, ldx, ldz, X, Z)) {
+    if (!g_fsplit) {
+      cudaError_t e = cudaMalloc(&g_fsplit, 2 * 128 * 128 * sizeof(float));
+      if (e != cudaSuccess) return e;
+    }
+    split_f_kernel<<<64, 256, 0, s>>>(FT, ldf, k, g_fsplit, g_fsplit + k * k);
+    return launch_materialize_tc(X, n, k, ldx, g_fsplit, g_fsplit + k * k, Z, ldz, s, nsm);
+  }
   if (X == Z && k2 > CB) return cudaErrorInvalidValue;
   const size_t smem = materialize_smem(k);
   static size_t configured = 0;

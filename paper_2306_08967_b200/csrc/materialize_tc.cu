@@ -1,0 +1,578 @@
+// K5 on the 5th-generation tensor cores: Z = X * F for d in {32, 64, 128}
+// (factor_state.cpp:120-123 query_all, :215-222 rebase, enhancer.cpp:196-206).
+//
+// Precision: single-pass TF32 misses the 1e-4 contract (SURVEY hard part 3),
+// so each K-step issues three kind::tf32 MMAs into one FP32 TMEM accumulator:
+//     Z = Xhi*Fhi + Xhi*Flo + Xlo*Fhi      (relative error ~2^-20)
+// with Xhi = X rounded to an exact TF32 value in shared memory (low 13
+// mantissa bits cleared), Xlo = X - Xhi (exact), Fhi/Flo likewise from the
+// fp64 F on the host.
+//
+// Warp roles (320 threads, one persistent CTA per SM, 128-row tiles):
+//   warp 0      TMA producer: X chunks (128 rows x 32 fp32 = one 128-byte
+//               swizzle atom) into a ring of S stages
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5   split: Xhi in place and Xlo into the stage's second buffer,
+//               fence.proxy.async, arrive
+//   warps 6-9   epilogue: tcgen05.ld 32 lanes x 32 columns, row stores
+// F (hi and lo, K-major, SW128 layout) stays resident in shared memory; the
+// accumulator is double-buffered in TMEM so the epilogue of tile t overlaps
+// the MMAs of tile t+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "materialize.cuh"
+
+namespace dgpu {
+
+namespace {
+
+constexpr int TM = 128;         // rows per tile (UMMA M)
+constexpr int KC = 32;          // fp32 per 128-byte swizzle atom (one TMA box / stage)
+template <int D> constexpr int stages_for() { return D == 32 ? 5 : D == 64 ? 4 : 2; }
+constexpr int OSTAGE = 4096;  // epilogue staging: 32 rows x 128 B per buffer
+constexpr int THREADS = 320;
+constexpr int CHUNK_BYTES = TM * KC * 4;  // 16 KB
+
+DAMF_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+DAMF_D void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+DAMF_D void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+DAMF_D void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+DAMF_D void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+DAMF_D void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+DAMF_D void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+DAMF_D void tma_store_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+DAMF_D void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+DAMF_D void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+DAMF_D void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+DAMF_D void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128-byte-swizzled UMMA shared-memory descriptor (SBO = 1024 B
+// between 8-row core-matrix groups, LBO = 16 B, version 1 for sm_100).
+DAMF_D uint64_t umma_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;           // LBO (16 B units)
+  d |= (uint64_t)(1024 >> 4) << 32; // SBO
+  d |= (uint64_t)1 << 46;           // version
+  d |= (uint64_t)2 << 61;           // SWIZZLE_128B
+  return d;
+}
+
+DAMF_D void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+DAMF_D void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+DAMF_D void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Byte offset of element (row r, col c in [0,32)) inside a 128-row x 128-byte
+// SW128 atom: 16-byte chunk index XORed with (row mod 8).
+DAMF_HD uint32_t sw128(int r, int c) {
+  const int chunk = (c >> 2) ^ (r & 7);
+  return (uint32_t)(r * 128 + chunk * 16 + (c & 3) * 4);
+}
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1)
+    materialize_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap zmap,
+                          const float* __restrict__ Fhi_g, const float* __restrict__ Flo_g,
+                          int64_t n) {
+  constexpr int STAGES = stages_for<D>();
+  constexpr int KB = D / KC;                 // 128-byte K atoms per row
+  constexpr int FB = D * KC * 4;             // bytes of one K atom of F (D rows x 128 B)
+  constexpr uint32_t TMEM_COLS = D * 2 < 32 ? 32 : D * 2;  // double-buffered accumulator
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sF = sm;                          // [2][KB][D x 128 B]  hi, lo
+  unsigned char* sX = sm + 2 * KB * FB;            // [STAGES][2][16 KB]  X (hi in place), Xlo
+  unsigned char* sO = sX + STAGES * 2 * CHUNK_BYTES;   // [4 warps][2][4 KB] store staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 4 * 2 * OSTAGE);
+  uint64_t* full = bars;                 // TMA -> split
+  uint64_t* ready = bars + STAGES;       // split -> MMA
+  uint64_t* empty = bars + 2 * STAGES;   // MMA -> TMA
+  uint64_t* tfull = bars + 3 * STAGES;   // MMA -> epilogue (2)
+  uint64_t* tempty = bars + 3 * STAGES + 2;  // epilogue -> MMA (2)
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + TM - 1) / TM;
+
+  // ---- F (hi, lo) into the swizzled K-major layout: row = output column j
+  for (int x = threadIdx.x; x < D * D; x += THREADS) {
+    const int j = x / D, kk = x % D;  // B[j][kk] = F[kk][j] (FT rows given)
+    const int kb = kk / KC, c = kk % KC;
+    const uint32_t off = (uint32_t)kb * FB + sw128(j, c);
+    *reinterpret_cast<float*>(sF + off) = Fhi_g[(int64_t)j * D + kk];
+    *reinterpret_cast<float*>(sF + KB * FB + off) = Flo_g[(int64_t)j * D + kk];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();  // F written by the generic proxy, read by the tensor core
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_s)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+
+  if (warp == 0) {
+    // ===== TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          mbar_expect_tx(&full[s], CHUNK_BYTES);
+          tma_load_2d(sX + (size_t)s * 2 * CHUNK_BYTES, &xmap, kb * KC, (int)(t * TM), &full[s]);
+        }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(D >> 3) << 17) |
+                                 ((uint32_t)(TM >> 4) << 24);
+      uint32_t it = 0, tl = 0;
+      const uint32_t fbase = smem_u32(sF), xbase = smem_u32(sX);
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        const int a = tl & 1;
+        if (tl >= 2) mbar_wait(&tempty[a], ((tl >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + (uint32_t)(a * D);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&ready[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t xh = xbase + (uint32_t)s * 2 * CHUNK_BYTES, xl = xh + CHUNK_BYTES;
+          const uint32_t fh = fbase + (uint32_t)kb * FB, fl = fh + (uint32_t)KB * FB;
+#pragma unroll
+          for (int ks = 0; ks < KC / 8; ++ks) {  // 8 tf32 (32 B) per MMA
+            const uint32_t ko = ks * 32;
+            const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+            mma_tf32(dtm, umma_desc(xh + ko), umma_desc(fh + ko), idesc, acc0);
+            mma_tf32(dtm, umma_desc(xh + ko), umma_desc(fl + ko), idesc, 1u);
+            mma_tf32(dtm, umma_desc(xl + ko), umma_desc(fh + ko), idesc, 1u);
+          }
+          mma_commit(&empty[s]);  // stage free once these MMAs have read it
+        }
+        mma_commit(&tfull[a]);  // accumulator a complete
+      }
+    }
+  } else if (warp < 6) {
+    // ===== split: Xhi = tf32(X) in place, Xlo = X - Xhi
+    const int st = threadIdx.x - 64;  // 0..127
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        float4* xh = reinterpret_cast<float4*>(sX + (size_t)s * 2 * CHUNK_BYTES);
+        float4* xl = reinterpret_cast<float4*>(sX + (size_t)s * 2 * CHUNK_BYTES + CHUNK_BYTES);
+#pragma unroll
+        for (int q = 0; q < CHUNK_BYTES / 16 / 128; ++q) {
+          const int i = st + q * 128;
+          float4 v = xh[i];
+          float4 h, l;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          xh[i] = h;
+          xl[i] = l;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[s]);
+      }
+  } else {
+    // ===== epilogue: TMEM -> registers -> swizzled smem -> TMA store
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    unsigned char* stg = sO + (size_t)(warp - 6) * 2 * OSTAGE;
+    uint32_t tl = 0, sb = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+      const int a = tl & 1;
+      mbar_wait(&tfull[a], (tl >> 1) & 1);
+      tc_fence_after();
+      const int64_t row0 = t * TM + q * 32;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32, sb ^= 1) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * D + c0), r);
+        unsigned char* buf = stg + sb * OSTAGE;
+        if (lane == 0) tma_store_wait_read1();  // buffer sb free again
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4*>(buf + sw128(lane, 4 * v)) =
+              make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                          __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && row0 < n) tma_store_2d(&zmap, c0, (int)row0, buf);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// d = 128 variant with F in TMEM: Z^T = F^T X^T. A = F^T (hi and lo) lives in
+// TMEM (lane j = output column, column kk = K) for the whole kernel, B = the
+// X tile (K-major, rows = N), D^T accumulates in TMEM with lane = output
+// column and column = tile row. TMEM: Fhi 128 + Flo 128 + 2 x 128 (double-
+// buffered accumulator) = 512 columns; shared memory holds only the X stages
+// (6) and the store staging, so more loads stay in flight.
+constexpr int TS_STAGES = 6;
+DAMF_D void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+DAMF_D void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    materialize_tc128_ts(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap zmap,
+                         const float* __restrict__ Fhi_g, const float* __restrict__ Flo_g, int64_t n) {
+  constexpr int D = 128, KB = D / KC, STAGES = TS_STAGES;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sX = sm;                              // [STAGES][2][16 KB]
+  unsigned char* sO = sX + STAGES * 2 * CHUNK_BYTES;   // [4 warps][2][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 4 * 2 * OSTAGE);
+  uint64_t* full = bars;
+  uint64_t* ready = bars + STAGES;
+  uint64_t* empty = bars + 2 * STAGES;
+  uint64_t* tfull = bars + 3 * STAGES;
+  uint64_t* tempty = bars + 3 * STAGES + 2;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + TM - 1) / TM;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+  // F^T into TMEM: columns [0,128) = Fhi, [128,256) = Flo; lane j <- FT row j
+  if (warp >= 6) {
+    const int q = warp & 3;
+    const int j = q * 32 + lane;
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      const float* src = (part ? Flo_g : Fhi_g) + (int64_t)j * D;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t r[32];
+#pragma unroll
+        for (int v = 0; v < 32; ++v) r[v] = __float_as_uint(src[c0 + v]);
+        tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(part * D + c0), r);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tA_hi = tmem, tA_lo = tmem + D, tD = tmem + 2 * D;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          mbar_expect_tx(&full[s], CHUNK_BYTES);
+          tma_load_2d(sX + (size_t)s * 2 * CHUNK_BYTES, &xmap, kb * KC, (int)(t * TM), &full[s]);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // M = 128 (output columns), N = 128 (tile rows), A from TMEM, B K-major
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TM >> 3) << 17) |
+                                 ((uint32_t)(D >> 4) << 24);
+      uint32_t it = 0, tl = 0;
+      const uint32_t xbase = smem_u32(sX);
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        const int a = tl & 1;
+        if (tl >= 2) mbar_wait(&tempty[a], ((tl >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dtm = tD + (uint32_t)(a * TM);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&ready[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t xh = xbase + (uint32_t)s * 2 * CHUNK_BYTES, xl = xh + CHUNK_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < KC / 8; ++ks) {
+            const uint32_t kcol = (uint32_t)(kb * KC + ks * 8);  // A columns (K) in TMEM
+            const uint32_t ko = ks * 32;                         // B bytes within the atom
+            const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+            mma_tf32_ts(dtm, tA_hi + kcol, umma_desc(xh + ko), idesc, acc0);
+            mma_tf32_ts(dtm, tA_lo + kcol, umma_desc(xh + ko), idesc, 1u);
+            mma_tf32_ts(dtm, tA_hi + kcol, umma_desc(xl + ko), idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[a]);
+      }
+    }
+  } else if (warp < 6) {
+    const int st = threadIdx.x - 64;
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        float4* xh = reinterpret_cast<float4*>(sX + (size_t)s * 2 * CHUNK_BYTES);
+        float4* xl = reinterpret_cast<float4*>(sX + (size_t)s * 2 * CHUNK_BYTES + CHUNK_BYTES);
+#pragma unroll
+        for (int q = 0; q < CHUNK_BYTES / 16 / 128; ++q) {
+          const int i = st + q * 128;
+          float4 v = xh[i];
+          float4 h, l;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          xh[i] = h;
+          xl[i] = l;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[s]);
+      }
+  } else {
+    // epilogue: lane = output column j (quadrant q), TMEM column = tile row
+    const int q = warp & 3;
+    unsigned char* stg = sO + (size_t)(warp - 6) * 2 * OSTAGE;
+    uint32_t tl = 0, sb = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+      const int a = tl & 1;
+      mbar_wait(&tfull[a], (tl >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int r0 = 0; r0 < TM; r0 += 32, sb ^= 1) {
+        uint32_t r[32];
+        tmem_ld32(tD + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * TM + r0), r);
+        unsigned char* buf = stg + sb * OSTAGE;
+        if (lane == 0) tma_store_wait_read1();
+        __syncwarp();
+        // staging tile [32 rows][32 columns] in SW128 layout; this thread owns column `lane`
+#pragma unroll
+        for (int v = 0; v < 32; ++v) *reinterpret_cast<uint32_t*>(buf + sw128(v, lane)) = r[v];
+        fence_proxy_async();
+        __syncwarp();
+        const int64_t row0 = t * TM + r0;
+        if (lane == 0 && row0 < n) tma_store_2d(&zmap, q * 32, (int)row0, buf);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <int D>
+size_t tc_smem() {
+  return 1024 + 2 * (D / KC) * (D * KC * 4) + stages_for<D>() * 2 * CHUNK_BYTES + 8 * OSTAGE + 256;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int D>
+cudaError_t launch_tc(const float* X, int64_t n, int ldx, const float* Fhi, const float* Flo,
+                      float* Z, int ldz, cudaStream_t s, int nsm) {
+  auto encode = get_encode();
+  if (!encode) return cudaErrorNotSupported;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
+  cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)TM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides,
+                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  CUtensorMap zm;
+  cuuint64_t zdims[2] = {(cuuint64_t)D, (cuuint64_t)n};
+  cuuint64_t zstr[1] = {(cuuint64_t)ldz * 4};
+  cuuint32_t zbox[2] = {(cuuint32_t)KC, 32u};
+  r = encode(&zm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Z, zdims, zstr, zbox, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  const int64_t ntiles = (n + TM - 1) / TM;
+  const int grid = (int)(ntiles < nsm ? ntiles : nsm);
+  if (D == 128) {
+    const size_t smem = 1024 + TS_STAGES * 2 * CHUNK_BYTES + 8 * OSTAGE + 256;
+    static bool cfg128 = false;
+    if (!cfg128) {
+      cudaError_t e = cudaFuncSetAttribute(materialize_tc128_ts,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      cfg128 = true;
+    }
+    materialize_tc128_ts<<<grid, THREADS, smem, s>>>(map, zm, Fhi, Flo, n);
+    return cudaGetLastError();
+  }
+  const size_t smem = tc_smem<D>();
+  static bool cfg = false;
+  if (!cfg) {
+    cudaError_t e = cudaFuncSetAttribute(materialize_tc_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cfg = true;
+  }
+  materialize_tc_kernel<D><<<grid, THREADS, smem, s>>>(map, zm, Fhi, Flo, n);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool materialize_tc_supported(int k, int ldx, int ldz, const void* X, const void* Z) {
+  return (k == 32 || k == 64 || k == 128) && (ldx % 4) == 0 && (ldz % 4) == 0 &&
+         ((uintptr_t)X % 16) == 0 && ((uintptr_t)Z % 16) == 0;
+}
+
+// Fhi/Flo: device fp32 arrays of k*k, row j = output column j (FT layout).
+cudaError_t launch_materialize_tc(const float* X, int64_t n, int k, int ldx, const float* Fhi,
+                                  const float* Flo, float* Z, int ldz, cudaStream_t s, int nsm) {
+  if (n <= 0) return cudaSuccess;
+  switch (k) {
+    case 32: return launch_tc<32>(X, n, ldx, Fhi, Flo, Z, ldz, s, nsm);
+    case 64: return launch_tc<64>(X, n, ldx, Fhi, Flo, Z, ldz, s, nsm);
+    case 128: return launch_tc<128>(X, n, ldx, Fhi, Flo, Z, ldz, s, nsm);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dgpu
