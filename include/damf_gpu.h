@@ -211,6 +211,10 @@ int damf_gpu_push_counters(damf_gpu* h, int64_t* out4);
  * kernel (cluster rank 0), 32 slots (see event_kernel.cu PROF_MARK). */
 int damf_gpu_profile_counters(damf_gpu* h, uint64_t* out16);
 
+/* Development: per-round trace of the last whole-GPU push, 4 int64 per round
+ * [frontier size, dense round, P3 items, active heavy rows]; returns rounds. */
+int damf_gpu_ppr_trace(damf_gpu* h, int64_t* out, int cap);
+
 /* Standalone materialisation kernel, Z = X * F (cfg 4): x_dev/z_dev are
  * n x d fp32 device buffers (may alias for in-place), f_host is d x d fp64.
  * stream is a cudaStream_t passed as void* (NULL = default stream). The

@@ -202,8 +202,11 @@ struct damf_gpu {
         *key = nullptr;
   int *stamp = nullptr, *mark = nullptr, *listF = nullptr, *listL = nullptr, *blk = nullptr;
   long long* blk64 = nullptr;
-  int *heavy = nullptr, *hidx = nullptr, *hoff = nullptr, *hact = nullptr;
-  float* hpart = nullptr;
+  int *heavy = nullptr, *hidx = nullptr, *hoff = nullptr, *cidx = nullptr;
+  float* hacc = nullptr;
+  int *items0 = nullptr, *items1 = nullptr, *hdone = nullptr, *mitems = nullptr;
+  long long* ptrace = nullptr;
+  unsigned long long* wq = nullptr;
   double* PT[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   double* Q[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   double* sigma = nullptr;
@@ -319,8 +322,14 @@ PprArgs ppr_args(damf_gpu* h) {
   a.heavy = h->heavy;
   a.hidx = h->hidx;
   a.hoff = h->hoff;
-  a.hact = h->hact;
-  a.hpart = h->hpart;
+  a.cidx = h->cidx;
+  a.hacc = h->hacc;
+  a.wq = h->wq;
+  a.items[0] = h->items0;
+  a.items[1] = h->items1;
+  a.hdone = h->hdone;
+  a.mitems = h->mitems;
+  a.trace = h->ptrace;
   a.out = h->out;
   a.in = h->in;
   a.directed = h->directed;
@@ -592,19 +601,26 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
     CK(dalloc(h, &h->listL, (size_t)ncap + 16 * 32 * 2 + 4096));
     CK(dalloc(h, &h->blk, (size_t)4096));
     CK(dalloc(h, &h->blk64, (size_t)4096));
-    CK(dalloc(h, &h->heavy, (size_t)ncap));
-    CK(dalloc(h, &h->hidx, (size_t)ncap));
-    CK(dalloc(h, &h->hoff, (size_t)ncap + 1));
-    CK(dalloc(h, &h->hact, (size_t)ncap));
-    CK(cudaMemsetAsync(h->hidx, 0xff, (size_t)ncap * 4, h->st));
-    CK(cudaMemsetAsync(h->hact, 0, (size_t)ncap * 4, h->st));
     {
-      // chunk partials: every heavy row contributes ceil(cnt/1024) <= cnt/1024 + 1
-      // chunks; bounded by (pool slots / 1024 + heavy rows) with heavy rows
-      // having > 2048 arcs, i.e. <= pool/1024 + pool/2048.
-      const size_t chunks = (size_t)(h->out.pool_size / 1024 + h->out.pool_size / 2048 + 16);
-      CK(dalloc(h, &h->hpart, chunks * (size_t)d));
+      // heavy rows have > PPR_HEAVY arcs: at most pool/(PPR_HEAVY+1) of them;
+      // chunks of PPR_CH arcs: at most pool/PPR_CH + heavy rows
+      const size_t nh = (size_t)(h->out.pool_size / (PPR_HEAVY + 1) + 16);
+      const size_t chunks = (size_t)(h->out.pool_size / PPR_CH) + nh;
+      CK(dalloc(h, &h->heavy, nh));
+      CK(dalloc(h, &h->hoff, nh + 1));
+      CK(dalloc(h, &h->cidx, chunks));
+      CK(dalloc(h, &h->hacc, nh * (size_t)d));
+      CK(dalloc(h, &h->wq, (size_t)2048));
+      CK(dalloc(h, &h->ptrace, (size_t)4 * 1024 + 1));
+      CK(dalloc(h, &h->mitems, 2 * ((size_t)ncap + (size_t)(h->out.pool_size / 512) + 4096)));
+      CK(dalloc(h, &h->hdone, nh));
+      CK(cudaMemsetAsync(h->hdone, 0, nh * 4, h->st));
+      CK(dalloc(h, &h->items0, (size_t)ncap + chunks + 4096));
+      CK(dalloc(h, &h->items1, (size_t)ncap + chunks + 4096));
+      CK(cudaMemsetAsync(h->hacc, 0, nh * (size_t)d * 4, h->st));
     }
+    CK(dalloc(h, &h->hidx, (size_t)ncap));
+    CK(cudaMemsetAsync(h->hidx, 0xff, (size_t)ncap * 4, h->st));
     CK(cudaMemsetAsync(h->Zb, 0, (size_t)ncap * d * 4, h->st));
     CK(cudaMemsetAsync(h->rb, 0, (size_t)ncap * d * 4, h->st));
     CK(cudaMemsetAsync(h->key, 0, (size_t)ncap * 4, h->st));
@@ -1140,6 +1156,17 @@ int damf_gpu_diagnostics(damf_gpu* h, damf_diag* o) {
 }
 
 void* damf_gpu_stream(damf_gpu* h) { return (void*)h->st; }
+
+// Dev: per-round trace of the last whole-GPU push ([nF, dense, items, active
+// heavy] x rounds); returns the round count (or -1).
+int damf_gpu_ppr_trace(damf_gpu* h, int64_t* out, int cap) {
+  if (!h || !h->ptrace) return -1;
+  long long buf[4 * 1024 + 1];
+  if (cudaMemcpy(buf, h->ptrace, sizeof(buf), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  const int r = (int)std::min<long long>(buf[4 * 1024], 1024);
+  for (int i = 0; i < 4 * std::min(r, cap); ++i) out[i] = buf[i];
+  return r;
+}
 
 int damf_gpu_profile_counters(damf_gpu* h, uint64_t* out16) {
   if (int r = sync_ctl(h)) return r;

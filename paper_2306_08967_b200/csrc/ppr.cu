@@ -49,42 +49,11 @@ DAMF_D int block_scan(int flag, int* wsum, int* total) {
 }
 
 // Grid-wide, order-preserving compaction of items i in [0, count) with
-// pred(i) -> (keep, value). Each block owns a contiguous chunk.
+// pred(i) -> (keep, value). Each block owns a contiguous, tile-aligned range;
+// each thread evaluates IPT consecutive items per tile (independent loads in
+// flight), then a block scan of the per-thread counts places them in order.
 template <class Pred>
-DAMF_D int grid_compact(cg::grid_group& g, int count, Pred pred, int* out, int* blk) {
-  __shared__ int wsum[PW];
-  const int G = gridDim.x;
-  const int chunk = (count + G - 1) / G;
-  const int lo = min(count, (int)blockIdx.x * chunk), hi = min(count, lo + chunk);
-  int mine = 0;
-  for (int base = lo; base < hi; base += PT_) {
-    const int i = base + threadIdx.x;
-    int v;
-    const int f = (i < hi) && pred(i, v);
-    int tot;
-    block_scan(f, wsum, &tot);
-    mine += tot;
-  }
-  if (threadIdx.x == 0) blk[blockIdx.x] = mine;
-  g.sync();
-  int off = 0, total = 0;
-  for (int b = 0; b < G; ++b) {
-    const int c = blk[b];
-    if (b < (int)blockIdx.x) off += c;
-    total += c;
-  }
-  for (int base = lo; base < hi; base += PT_) {
-    const int i = base + threadIdx.x;
-    int v = 0;
-    const int f = (i < hi) && pred(i, v);
-    int tot;
-    const int pos = block_scan(f, wsum, &tot);
-    if (f) out[off + pos] = v;
-    off += tot;
-  }
-  g.sync();
-  return total;
-}
+DAMF_D int grid_compact(cg::grid_group& g, int count, Pred pred, int* out, int* blk);
 
 DAMF_D float row_key(const float* r, int k, double deg) {
   float m = 0.0f;
@@ -93,17 +62,212 @@ DAMF_D float row_key(const float* r, int k, double deg) {
   return (float)((double)m / fmax(deg, 1.0));
 }
 
-constexpr int HEAVY = 2048;  // rows with more out-arcs are pulled in chunks
-constexpr int CH = 1024;     // neighbours per chunk
-constexpr int HB = 8;        // delta rows gathered per batch (loads in flight)
+constexpr int HEAVY = PPR_HEAVY;
+constexpr int CH = PPR_CH;
+constexpr int G = 8;          // lanes per row group (4 groups per warp)
+constexpr int SMALL = 32;     // rows with <= SMALL arcs are pulled by one group
+constexpr int BIGMARK = 1024; // pushers with more in-arcs are marked grid-wide
 
-// Pull the stamped neighbours u in out(v)[beg, end) into acc (lane-parallel
-// over 32 ids/stamps per step, ballot of hits, then the hit rows gathered HB
-// at a time with all loads issued before the FMAs). Returns pulled arcs.
-template <int KPL>
-DAMF_D int pull_range(const PprArgs& A, int64_t base, int beg, int end, int R, int k,
-                      float (&acc)[KPL]) {
-  const int lane = threadIdx.x & 31;
+// Block-exclusive scan of one int per thread; block total in *total.
+DAMF_D int block_scan_val(int x, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  int off = 0, tot = 0;
+  for (int i = 0; i < PW; ++i) {
+    if (i < w) off += wsum[i];
+    tot += wsum[i];
+  }
+  __syncthreads();
+  *total = tot;
+  return off + inc - x;
+}
+
+// Grid-wide exclusive scan out[i] = sum_{j<i} val(j), out[count] = total.
+template <class Val>
+DAMF_D int grid_scan(cg::grid_group& g, int count, Val val, int* out, int* blk) {
+  __shared__ int wsum[PW];
+  const int GB = gridDim.x;
+  const int chunk = (count + GB - 1) / GB;
+  const int lo = min(count, (int)blockIdx.x * chunk), hi = min(count, lo + chunk);
+  int mine = 0;
+  for (int base = lo; base < hi; base += PT_) {
+    const int i = base + threadIdx.x;
+    int tot;
+    block_scan_val(i < hi ? val(i) : 0, wsum, &tot);
+    mine += tot;
+  }
+  if (threadIdx.x == 0) blk[blockIdx.x] = mine;
+  g.sync();
+  int off = 0, total = 0;
+  for (int b = 0; b < GB; ++b) {
+    const int c = blk[b];
+    if (b < (int)blockIdx.x) off += c;
+    total += c;
+  }
+  for (int base = lo; base < hi; base += PT_) {
+    const int i = base + threadIdx.x;
+    int tot;
+    const int pos = block_scan_val(i < hi ? val(i) : 0, wsum, &tot);
+    if (i < hi) out[i] = off + pos;
+    off += tot;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[count] = total;
+  g.sync();
+  return total;
+}
+
+template <class Pred>
+DAMF_D int grid_compact(cg::grid_group& g, int count, Pred pred, int* out, int* blk) {
+  constexpr int IPT = 8, TILE = PT_ * IPT;
+  __shared__ int wsum[PW];
+  const int GB = gridDim.x;
+  const long long per = ((long long)(count + GB - 1) / GB + TILE - 1) / TILE * TILE;
+  const int lo = (int)min((long long)count, (long long)blockIdx.x * per);
+  const int hi = (int)min((long long)count, (long long)lo + per);
+  int mine = 0;
+  for (int base = lo; base < hi; base += TILE) {
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const int i = base + threadIdx.x * IPT + j;
+      int v;
+      c += (i < hi) && pred(i, v);
+    }
+    int tot;
+    block_scan_val(c, wsum, &tot);
+    mine += tot;
+  }
+  if (threadIdx.x == 0) blk[blockIdx.x] = mine;
+  g.sync();
+  int off = 0, total = 0;
+  for (int b = 0; b < GB; ++b) {
+    const int c = blk[b];
+    if (b < (int)blockIdx.x) off += c;
+    total += c;
+  }
+  for (int base = lo; base < hi; base += TILE) {
+    int vals[IPT];
+    unsigned f = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const int i = base + threadIdx.x * IPT + j;
+      if ((i < hi) && pred(i, vals[j])) f |= 1u << j;
+    }
+    int tot;
+    int pos = off + block_scan_val(__popc(f), wsum, &tot);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j)
+      if (f >> j & 1u) out[pos++] = vals[j];
+    off += tot;
+  }
+  g.sync();
+  return total;
+}
+
+// Per-lane column slice of a row: VEC -> PER float4 at 4*gl + 32*t,
+// scalar -> PER floats at gl + 8*t. NE = elements per lane. Within a warp,
+// group q "owns" slice elements with (VEC ? t : e) % 4 == q for warp-wide
+// write-back after the cross-group reduction.
+template <int PER, bool VEC>
+struct Cols {
+  static constexpr int NE = VEC ? 4 * PER : PER;
+  DAMF_D static int col(int gl, int e) { return VEC ? 4 * gl + 32 * (e >> 2) + (e & 3) : gl + G * e; }
+  DAMF_D static bool owns(int grp, int e) { return (VEC ? (e >> 2) : e) % 4 == grp; }
+  template <bool CG = false>
+  DAMF_D static void load(const float* row, int gl, int k, float (&x)[NE]) {
+    if (VEC) {
+#pragma unroll
+      for (int t = 0; t < PER; ++t) {
+        const int j = 4 * gl + 32 * t;
+        const float4* p = reinterpret_cast<const float4*>(row + j);
+        float4 v = j < k ? (CG ? __ldcg(p) : *p) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[4 * t] = v.x;
+        x[4 * t + 1] = v.y;
+        x[4 * t + 2] = v.z;
+        x[4 * t + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int j = gl + G * e;
+        x[e] = j < k ? (CG ? __ldcg(row + j) : row[j]) : 0.0f;
+      }
+    }
+  }
+  DAMF_D static void store(float* row, int gl, int k, const float (&x)[NE]) {
+    if (VEC) {
+#pragma unroll
+      for (int t = 0; t < PER; ++t) {
+        const int j = 4 * gl + 32 * t;
+        if (j < k)
+          *reinterpret_cast<float4*>(row + j) = make_float4(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int j = gl + G * e;
+        if (j < k) row[j] = x[e];
+      }
+    }
+  }
+};
+
+// Group (8 lanes) pull of the stamped neighbours u in out(v)[beg, end) into
+// acc: 8 ids/stamps per step, group ballot, hit rows gathered two at a time.
+template <int PER, bool VEC>
+DAMF_D int pull_group(const PprArgs& A, int64_t base, int beg, int end, int R, int k, int gl,
+                      unsigned gm, float (&acc)[Cols<PER, VEC>::NE]) {
+  using CL = Cols<PER, VEC>;
+  int matched = 0;
+  const int shift = (threadIdx.x & 31) & ~(G - 1);
+  for (int p0 = beg; p0 < end; p0 += G) {
+    const int p = p0 + gl;
+    int u = -1;
+    float w = 0.0f;
+    if (p < end) {
+      u = A.out.ids[base + p];
+      w = A.out.wts ? (float)A.out.wts[base + p] : 1.0f;
+    }
+    const bool hit = u >= 0 && A.stamp[u] == R;
+    unsigned mask = (__ballot_sync(gm, hit) >> shift) & 0xFFu;
+    matched += __popc(mask);
+    while (mask) {
+      const int s0 = __ffs(mask) - 1;
+      mask &= mask - 1;
+      int s1 = s0;
+      const bool two = mask != 0;
+      if (two) {
+        s1 = __ffs(mask) - 1;
+        mask &= mask - 1;
+      }
+      const int u0 = __shfl_sync(gm, u, s0, G);
+      const float w0 = __shfl_sync(gm, w, s0, G);
+      const int u1 = __shfl_sync(gm, u, s1, G);
+      const float w1 = two ? __shfl_sync(gm, w, s1, G) : 0.0f;
+      float x0[CL::NE], x1[CL::NE];
+      CL::load(A.delta + (int64_t)u0 * A.d, gl, k, x0);
+      CL::load(A.delta + (int64_t)u1 * A.d, gl, k, x1);
+#pragma unroll
+      for (int e = 0; e < CL::NE; ++e) acc[e] = fmaf(w1, x1[e], fmaf(w0, x0[e], acc[e]));
+    }
+  }
+  return matched;
+}
+
+// Warp pull of out(v)[beg, end): 32 ids/stamps per step, hits compacted in
+// shared memory, each group gathers two hit rows per step (8 rows in flight
+// per warp). acc holds the group's partial (reduce across groups after).
+template <int PER, bool VEC>
+DAMF_D int pull_warp(const PprArgs& A, int64_t base, int beg, int end, int R, int k, int lane,
+                     int* sid, float* sw, float (&acc)[Cols<PER, VEC>::NE]) {
+  using CL = Cols<PER, VEC>;
+  const int grp = lane >> 3, gl = lane & (G - 1);
   int matched = 0;
   for (int p0 = beg; p0 < end; p0 += 32) {
     const int p = p0 + lane;
@@ -114,80 +278,238 @@ DAMF_D int pull_range(const PprArgs& A, int64_t base, int beg, int end, int R, i
       w = A.out.wts ? (float)A.out.wts[base + p] : 1.0f;
     }
     const bool hit = u >= 0 && A.stamp[u] == R;
-    unsigned mask = __ballot_sync(0xffffffffu, hit);
-    matched += __popc(mask);
-    while (mask) {
-      int ub[HB];
-      float wb[HB];
-#pragma unroll
-      for (int q = 0; q < HB; ++q) {
-        if (mask) {
-          const int s0 = __ffs(mask) - 1;
-          mask &= mask - 1;
-          ub[q] = __shfl_sync(0xffffffffu, u, s0);
-          wb[q] = __shfl_sync(0xffffffffu, w, s0);
-        } else {
-          ub[q] = -1;
-          wb[q] = 0.0f;
-        }
-      }
-      float x[HB][KPL];
-#pragma unroll
-      for (int q = 0; q < HB; ++q) {
-        const float* dq = A.delta + (int64_t)(ub[q] < 0 ? ub[0] : ub[q]) * A.d;
-#pragma unroll
-        for (int t = 0; t < KPL; ++t) {
-          const int j = lane + 32 * t;
-          x[q][t] = (j < k && ub[q] >= 0) ? dq[j] : 0.0f;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < HB; ++q)
-#pragma unroll
-        for (int t = 0; t < KPL; ++t) acc[t] = fmaf(wb[q], x[q][t], acc[t]);
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const int nh = __popc(m);
+    if (hit) {
+      const int pos = __popc(m & ((1u << lane) - 1u));
+      sid[pos] = u;
+      sw[pos] = w;
     }
+    __syncwarp();
+    for (int q = 2 * grp; q < nh; q += 8) {
+      const bool two = q + 1 < nh;
+      const int u0 = sid[q], u1 = two ? sid[q + 1] : u0;
+      const float w0 = sw[q], w1 = two ? sw[q + 1] : 0.0f;
+      float x0[CL::NE], x1[CL::NE];
+      CL::load(A.delta + (int64_t)u0 * A.d, gl, k, x0);
+      CL::load(A.delta + (int64_t)u1 * A.d, gl, k, x1);
+#pragma unroll
+      for (int e = 0; e < CL::NE; ++e) acc[e] = fmaf(w1, x1[e], fmaf(w0, x0[e], acc[e]));
+    }
+    __syncwarp();
+    matched += nh;
   }
   return matched;
 }
 
-// r[v] = [v not pushed] r[v] + (1-alpha)/max(deg v,1) * acc ; key[v]. Rows with
-// no pulled contribution that were not pushed are unchanged (skipped).
-template <int KPL>
-DAMF_D void finish_row(const PprArgs& A, int v, int R, int k, double om, const float (&acc)[KPL],
-                       bool any) {
-  const int lane = threadIdx.x & 31;
+// r[v] = [v pushed this round ? 0 : r[v]] + (1-alpha)/max(deg v,1) acc ; key[v].
+// Rows with no pulled arc that were not pushed are unchanged (skipped).
+template <int PER, bool VEC>
+DAMF_D void finish_group(const PprArgs& A, int v, int R, int k, double om, int gl, unsigned gm,
+                         const float (&acc)[Cols<PER, VEC>::NE], bool any) {
+  using CL = Cols<PER, VEC>;
+  const bool inF = A.stamp[v] == R;
+  if (!inF && !any) return;
+  const double degv = A.deg[v];
+  const float coef = (float)(om / fmax(degv, 1.0));
+  float* rv = A.rb + (int64_t)v * A.d;
+  float r[CL::NE];
+  if (inF) {
+#pragma unroll
+    for (int e = 0; e < CL::NE; ++e) r[e] = 0.0f;
+  } else {
+    CL::load(rv, gl, k, r);
+  }
+  float m = 0.0f;
+#pragma unroll
+  for (int e = 0; e < CL::NE; ++e) {
+    r[e] = fmaf(coef, acc[e], r[e]);
+    if (CL::col(gl, e) < k) m = fmaxf(m, fabsf(r[e]));
+  }
+  CL::store(rv, gl, k, r);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(gm, m, o, G));
+  if (gl == 0) A.key[v] = (float)((double)m / fmax(degv, 1.0));
+}
+
+// Warp-wide finish after the cross-group reduction (every group holds the
+// full sum; group q reads/writes the slice elements it owns).
+template <int PER, bool VEC>
+DAMF_D void finish_warp(const PprArgs& A, int v, int R, int k, double om, int lane,
+                        const float (&acc)[Cols<PER, VEC>::NE], bool any) {
+  using CL = Cols<PER, VEC>;
+  const int grp = lane >> 3, gl = lane & (G - 1);
   const bool inF = A.stamp[v] == R;
   if (!inF && !any) return;
   const double degv = A.deg[v];
   const float coef = (float)(om / fmax(degv, 1.0));
   float* rv = A.rb + (int64_t)v * A.d;
   float m = 0.0f;
+  if (VEC) {
 #pragma unroll
-  for (int t = 0; t < KPL; ++t) {
-    const int j = lane + 32 * t;
-    if (j < k) {
-      const float nr = (inF ? 0.0f : rv[j]) + coef * acc[t];
-      rv[j] = nr;
-      m = fmaxf(m, fabsf(nr));
+    for (int t = 0; t < PER; ++t) {
+      const int j = 4 * gl + 32 * t;
+      if (t % 4 != grp || j >= k) continue;
+      float4 r = inF ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(rv + j);
+      r.x = fmaf(coef, acc[4 * t], r.x);
+      r.y = fmaf(coef, acc[4 * t + 1], r.y);
+      r.z = fmaf(coef, acc[4 * t + 2], r.z);
+      r.w = fmaf(coef, acc[4 * t + 3], r.w);
+      *reinterpret_cast<float4*>(rv + j) = r;
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < CL::NE; ++e) {
+      const int j = gl + G * e;
+      if (e % 4 != grp || j >= k) continue;
+      const float r = fmaf(coef, acc[e], inF ? 0.0f : rv[j]);
+      rv[j] = r;
+      m = fmaxf(m, fabsf(r));
     }
   }
   m = warp_max(m);
   if (lane == 0) A.key[v] = (float)((double)m / fmax(degv, 1.0));
 }
 
-template <int KPL>
-__global__ void __launch_bounds__(PT_, 3) ppr_push_kernel(PprArgs A) {
+template <int PER, bool VEC>
+DAMF_D void reduce_groups(float (&acc)[Cols<PER, VEC>::NE]) {
+#pragma unroll
+  for (int e = 0; e < Cols<PER, VEC>::NE; ++e) {
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 8);
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+  }
+}
+
+// Heavy-row chunk partial -> hacc[h] (vector reductions, owned slice only).
+template <int PER, bool VEC>
+DAMF_D void chunk_accumulate(float* hrow, int k, int lane, const float (&acc)[Cols<PER, VEC>::NE]) {
+  const int grp = lane >> 3, gl = lane & (G - 1);
+  if (VEC) {
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int j = 4 * gl + 32 * t;
+      if (t % 4 != grp || j >= k) continue;
+      atomicAdd(reinterpret_cast<float4*>(hrow + j),
+                make_float4(acc[4 * t], acc[4 * t + 1], acc[4 * t + 2], acc[4 * t + 3]));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < Cols<PER, VEC>::NE; ++e) {
+      const int j = gl + G * e;
+      if (e % 4 != grp || j >= k) continue;
+      atomicAdd(hrow + j, acc[e]);
+    }
+  }
+}
+
+// ---- work distribution: NQ counters per phase, each on its own 128-byte
+// line, each owning a contiguous slice of the item space. A warp starts at
+// queue (warp id mod NQ), grabs batches there until the slice is drained
+// (checked with a plain load first, so drained queues cost no atomics), then
+// moves on. Same-address atomics serialise in L2; spreading them over NQ
+// lines and sizing batches to the remaining work keeps grabs cheap.
+constexpr int NQ = 32, QS = 16;  // queues per phase, u64 stride between counters
+constexpr int WQ_P1 = 0, WQ_P3 = NQ * QS, WQ_MK = 2 * NQ * QS, WQ_SC = 3 * NQ * QS;
+// scalar counters at WQ_SC + QS * i
+// (item counters alternate by round parity: reset after a round's last sync
+// while the next round may already append)
+constexpr int SC_MITEMS = 0 /* 0..1 */, SC_PUSH = 2 /* 2..4 */, SC_ITEMS = 5 /* 5..6 */,
+              SC_S = 7 /* 7..9 */, SC_ARCS = 10;
+
+struct Grabber {
+  unsigned long long* q;
+  int total, SB, dlo, len, q0, wpq, gw, nw, i;
+  // The first half of the items is dealt statically in SB-item batches
+  // strided over the warps (batch i of warp w = items [(i*nw + w)*SB, +SB)),
+  // which mixes expensive and cheap items evenly; the rest goes through NQ
+  // queues (dynamic, absorbs the imbalance).
+  DAMF_D Grabber(unsigned long long* qbase, int total_, int gw_, int nw_, int SB_)
+      : q(qbase), total(total_), SB(SB_), q0(gw_ % NQ), wpq(max(1, nw_ / NQ)), gw(gw_), nw(nw_),
+        i(0) {
+    const long long per = (long long)nw * SB;
+    dlo = (int)(total / (2 * per) * per);
+    if (total <= per) dlo = total;  // small: all static
+    len = (total - dlo + NQ - 1) / NQ;
+  }
+  // warp-uniform; returns false when every item is taken
+  DAMF_D bool next(int lane, int minB, int maxB, int& start, int& cnt) {
+    const long long s0 = ((long long)i * nw + gw) * SB;
+    if (s0 < dlo) {
+      ++i;
+      start = (int)s0;
+      cnt = (int)min((long long)SB, dlo - s0);
+      return true;
+    }
+    if (len == 0) return false;
+    for (;;) {
+      // lane l inspects queue (q0 + l) % NQ: one round trip for all queues
+      const int sl = (q0 + lane) % NQ;
+      const int lo = dlo + sl * len, hi = min(total, lo + len);
+      const int cur = (int)min((unsigned long long)len, *(volatile unsigned long long*)(q + sl * QS));
+      const unsigned m = __ballot_sync(0xffffffffu, lo + cur < hi);
+      if (!m) return false;
+      const int j = __ffs(m) - 1;
+      const int qs = __shfl_sync(0xffffffffu, sl, j);
+      const int qlo = __shfl_sync(0xffffffffu, lo, j), qhi = __shfl_sync(0xffffffffu, hi, j);
+      const int rem = __shfl_sync(0xffffffffu, hi - lo - cur, j);
+      const int B = (min(maxB, max(minB, rem / (2 * wpq))) + 3) & ~3;
+      int got = 0;
+      if (lane == 0) got = (int)min((unsigned long long)len, atomicAdd(q + qs * QS, (unsigned long long)B));
+      got = __shfl_sync(0xffffffffu, got, 0);
+      if (qlo + got >= qhi) continue;
+      start = qlo + got;
+      cnt = min(B, qhi - start);
+      return true;
+    }
+  }
+};
+
+constexpr int MCH = 512;  // in-arcs per scatter item
+
+// One cooperative kernel runs every round of the push with grid barriers.
+// Each round:
+//   P1  candidates (all rows after a pull round; the rows the previous
+//       scatter touched, with their key recomputed here from r, otherwise):
+//       key * s_max > alpha eps  ->  delta = r, Z += r, r = 0, key = 0,
+//       stamp = R; pushers append their in-arc chunks as scatter items and
+//       count S = sum of their in-degrees.
+//   --- barrier ---
+//   If S is large (S * 64 > arcs): PULL round (no atomics): every row v
+//       r[v] += (1-alpha)/max(deg v,1) sum_{u in out(v), stamp u = R} w delta[u],
+//       heavy rows (> HEAVY arcs) split into CH-arc chunks accumulated in
+//       hacc[h] and finished by the warp completing the last chunk.
+//   Else SCATTER round: for every pushed u and v in in(u):
+//       r[v] += (1-alpha) w / max(deg v,1) delta[u]   (red.global.add.v4.f32),
+//       the first toucher of v appends it to the next candidate list.
+//   --- barrier ---
+// The scatter makes the fp32 summation order of touched rows
+// nondeterministic (as in the fused per-event push); the defect bound, the
+// reference's contract (enhancer.cpp:98-157), is unaffected.
+template <int PER, bool VEC>
+__global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) ppr_push_kernel(PprArgs A) {
+  using CL = Cols<PER, VEC>;
   cg::grid_group g = cg::this_grid();
-  __shared__ long long red64[PW];
+  __shared__ int s_id[PW][32];
+  __shared__ float s_w[PW][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int gw = (blockIdx.x * PT_ + threadIdx.x) >> 5;  // global warp id
-  const int nwarps = gridDim.x * PW;
+  const int grp = lane >> 3, gl = lane & (G - 1);
+  const unsigned gm = 0xFFu << (grp * G);
+  const unsigned lt = (1u << lane) - 1u;
+  const int gw = blockIdx.x * PW + wib, nw = gridDim.x * PW;
+  int* sid = s_id[wib];
+  float* sw = s_w[wib];
+  unsigned long long* wq = A.wq;
+  unsigned long long* sc = wq + WQ_SC;
   const int k = A.ctl->k, d = A.d;
   const int n = (int)A.n;
   const float thr = (float)(A.alpha_eps / *A.smax);
   const double om = 1.0 - A.alpha;
+  const DevCSR& inC = A.directed ? A.in : A.out;
   int R = (int)A.stats[2];  // device-resident round stamp base (monotonic)
-  // ---- heavy rows (out-degree > HEAVY): list, chunk prefix, row -> index
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < WQ_SC + 16 * QS; i += PT_) wq[i] = 0;
+  // ---- heavy rows (> HEAVY out-arcs): list, chunk prefix, chunk -> row
   const int nH = grid_compact(
       g, n,
       [&](int i, int& v) {
@@ -195,90 +517,160 @@ __global__ void __launch_bounds__(PT_, 3) ppr_push_kernel(PprArgs A) {
         return A.out.cnt[i] > HEAVY;
       },
       A.heavy, A.blk);
-  if (blockIdx.x == 0) {
-    // exclusive prefix of chunk counts (block 0, fixed order)
-    __shared__ int wsum[PW];
-    int carry = 0;
-    for (int b0 = 0; b0 < nH; b0 += PT_) {
-      const int i = b0 + threadIdx.x;
-      const int c = i < nH ? (A.out.cnt[A.heavy[i]] + CH - 1) / CH : 0;
-      int x = c;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) wsum[wib] = x;
-      __syncthreads();
-      int pre = 0, tot = 0;
-      for (int w = 0; w < PW; ++w) {
-        if (w < wib) pre += wsum[w];
-        tot += wsum[w];
-      }
-      if (i < nH) A.hoff[i] = carry + pre + x - c;
-      carry += tot;
-      __syncthreads();
+  const int nchunks = grid_scan(
+      g, nH, [&](int h) { return (A.out.cnt[A.heavy[h]] + CH - 1) / CH; }, A.hoff, A.blk);
+  {
+    for (int h = blockIdx.x * PT_ + threadIdx.x; h < nH; h += gridDim.x * PT_) {
+      A.hidx[A.heavy[h]] = h;
+      for (int c = A.hoff[h]; c < A.hoff[h + 1]; ++c) A.cidx[c] = h;
     }
-    if (threadIdx.x == 0) A.hoff[nH] = carry;
+    unsigned long long arcs = 0;
+    for (int i = blockIdx.x * PT_ + threadIdx.x; i < n; i += gridDim.x * PT_) arcs += A.out.cnt[i];
+    for (int o = 16; o > 0; o >>= 1) arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
+    if (lane == 0 && arcs) atomicAdd(&sc[SC_ARCS * QS], arcs);
   }
-  for (int i = blockIdx.x * PT_ + threadIdx.x; i < nH; i += gridDim.x * PT_) A.hidx[A.heavy[i]] = i;
   g.sync();
-  const int nchunks = A.hoff[nH];
+  const long long narcs = (long long)*(volatile unsigned long long*)&sc[SC_ARCS * QS];
   // ---- rounds
-  const bool init_all = A.ncand < 0;
-  int ncand = init_all ? n : A.ncand;
-  const int* candL = init_all ? nullptr : A.cand;
-  bool cand_all = init_all;
-  bool mark_mode = true;
-  long long pushes = 0, pulled = 0, affected = 0, aff_arcs = 0;
+  bool cand_all = A.ncand < 0;
+  int ncand = cand_all ? n : A.ncand;
+  const int* candL = cand_all ? nullptr : A.cand;
+  bool fresh = false;  // candidates' keys must be recomputed from r
+  long long pushes = 0;
+  long long c_aff = 0, c_arcs = 0, c_pulled = 0;  // lane-0 accounting
   int rounds = 0;
+  int cur = 0;  // items[cur]: rows touched by this round's scatter
+  // per-phase wall time (block 0 thread 0, %globaltimer ns) -> ctl->prof[24..28]
+  const bool tl = blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long tp = tl ? globaltimer() : 0;
+  auto tmark = [&](int slot) {
+    if (tl) {
+      const unsigned long long t = globaltimer();
+      A.ctl->prof[slot] += t - tp;
+      tp = t;
+    }
+  };
   for (;;) {
     ++R;
-    // P1: push candidates over threshold (delta, Z, stamp, in-neighbour marks)
-    long long mine = 0;
-    for (int base = gw * 32; base < ncand; base += nwarps * 32) {
-      const int i = base + lane;
-      int v = -1;
-      if (i < ncand) v = cand_all ? i : candL[i];
-      const bool hit = v >= 0 && A.key[v] > thr;
-      unsigned mask = __ballot_sync(0xffffffffu, hit);
-      mine += __popc(mask);
-      while (mask) {
-        const int s0 = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int u = __shfl_sync(0xffffffffu, v, s0);
-        const float* ru = A.rb + (int64_t)u * d;
-        float* zu = A.Zb + (int64_t)u * d;
-        float* du = A.delta + (int64_t)u * d;
-        for (int j = lane; j < k; j += 32) {
-          const float r = ru[j];
-          du[j] = r;
-          zu[j] += r;
+    const int par = R & 1;
+    unsigned long long* pushc = &sc[(SC_PUSH + R % 3) * QS];
+    unsigned long long* sumS = &sc[(SC_S + R % 3) * QS];
+    // ---------------- P1: push
+    long long mine = 0, myS = 0;  // mine: warp-uniform; myS: per lane
+    // pushed row u (whole group): delta = r, Z += r, r = 0, key = 0, stamp;
+    // x = r slice already in registers
+    auto push_row = [&](int u, const float (&x)[CL::NE]) {
+      float z[CL::NE], zero[CL::NE];
+      CL::load(A.Zb + (int64_t)u * d, gl, k, z);
+      CL::store(A.delta + (int64_t)u * d, gl, k, x);
+#pragma unroll
+      for (int e = 0; e < CL::NE; ++e) {
+        z[e] += x[e];
+        zero[e] = 0.0f;
+      }
+      CL::store(A.Zb + (int64_t)u * d, gl, k, z);
+      CL::store(A.rb + (int64_t)u * d, gl, k, zero);
+      if (gl == 0) {
+        A.stamp[u] = R;
+        A.key[u] = 0.0f;
+      }
+    };
+    // scatter items of the pushed rows (uniform within the calling group set)
+    auto add_items = [&](int u, bool pushed) {
+      const int c = pushed ? inC.cnt[u] : 0;
+      const int nit = (c + MCH - 1) / MCH;
+      int tot = nit;  // warp-aggregate the reservations (one atomic per warp)
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, tot, o);
+        if (lane >= o) tot += y;
+      }
+      const int all = __shfl_sync(0xffffffffu, tot, 31);
+      if (all == 0) return 0;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&sc[(SC_MITEMS + par) * QS], (unsigned long long)all);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const unsigned long long pos = base + tot - nit;
+      for (int i = 0; i < nit; ++i) {
+        A.mitems[2 * (pos + i)] = u;
+        A.mitems[2 * (pos + i) + 1] = i;
+      }
+      return c;
+    };
+    if (!fresh) {
+      // keys are current: lane-per-candidate check, groups copy the pushers
+      Grabber gb(wq + WQ_P1, ncand, gw, nw, 32);
+      int start, cnt;
+      while (gb.next(lane, 32, 128, start, cnt)) {
+        for (int s0 = start; s0 < start + cnt; s0 += 32) {
+          const int q = s0 + lane;
+          int v = -1;
+          if (q < start + cnt) v = cand_all ? q : candL[q];
+          const bool push = v >= 0 && A.key[v] > thr;
+          const unsigned pm = __ballot_sync(0xffffffffu, push);
+          if (!pm) continue;
+          const int np = __popc(pm);
+          mine += np;
+          if (push) sid[__popc(pm & lt)] = v;
+          myS += add_items(v, push);
+          __syncwarp();
+          for (int j = grp; j < np; j += 4) {
+            const int u = sid[j];
+            float x[CL::NE];
+            CL::load(A.rb + (int64_t)u * d, gl, k, x);
+            push_row(u, x);
+          }
+          __syncwarp();
         }
-        if (lane == 0) {
-          A.stamp[u] = R;
-          if (mark_mode) A.mark[u] = R;
-        }
-        if (mark_mode) {
-          const DevCSR& in = A.directed ? A.in : A.out;
-          const int64_t ib = in.off[u];
-          const int c = in.cnt[u];
-          for (int p = lane; p < c; p += 32) A.mark[in.ids[ib + p]] = R;
+      }
+    } else {
+      // after a scatter: group per candidate, key from r, push if over
+      Grabber gb(wq + WQ_P1, ncand, gw, nw, 4);
+      int start, cnt;
+      while (gb.next(lane, 4, 32, start, cnt)) {
+        for (int base = start; base < start + cnt; base += 4) {
+          const int q = base + grp;
+          const int v = q < start + cnt ? candL[q] : -1;
+          bool push = false;
+          float x[CL::NE];
+          if (v >= 0) {
+            CL::load(A.rb + (int64_t)v * d, gl, k, x);
+            float m = 0.0f;
+#pragma unroll
+            for (int e = 0; e < CL::NE; ++e)
+              if (CL::col(gl, e) < k) m = fmaxf(m, fabsf(x[e]));
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(gm, m, o, G));
+            const float key = (float)((double)m / fmax(A.deg[v], 1.0));
+            push = key > thr;
+            if (push) push_row(v, x);
+            else if (gl == 0) A.key[v] = key;
+          }
+          const unsigned pm = __ballot_sync(0xffffffffu, push && gl == 0);
+          mine += __popc(pm);
+          myS += add_items(v, push && gl == 0);
         }
       }
     }
-    // grid-wide push count
-    mine = (lane == 0) ? mine : 0;
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if (lane == 0) red64[wib] = mine;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long t = 0;
-      for (int w = 0; w < PW; ++w) t += red64[w];
-      A.blk64[blockIdx.x] = t;
+    for (int o = 16; o > 0; o >>= 1) myS += __shfl_xor_sync(0xffffffffu, myS, o);
+    if (lane == 0 && mine) {
+      atomicAdd(pushc, (unsigned long long)mine);
+      atomicAdd(sumS, (unsigned long long)myS);
     }
     g.sync();
-    long long nF = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) nF += A.blk64[b];
+    tmark(24);
+    const long long nF = (long long)*(volatile unsigned long long*)pushc;
+    const long long S = (long long)*(volatile unsigned long long*)sumS;
+    const int nmi = (int)*(volatile unsigned long long*)&sc[(SC_MITEMS + par) * QS];
+    if (blockIdx.x == 0) {
+      if (threadIdx.x < NQ) wq[WQ_P1 + threadIdx.x * QS] = 0;
+      if (threadIdx.x == 0) {
+        sc[(SC_PUSH + (R + 1) % 3) * QS] = 0;
+        sc[(SC_S + (R + 1) % 3) * QS] = 0;
+        // the previous round's touched count: read by every thread before
+        // this round's P1 barrier, next appended in round R + 1
+        sc[(SC_ITEMS + (par ^ 1)) * QS] = 0;
+      }
+    }
     if (nF == 0) break;
     ++rounds;
     pushes += nF;
@@ -286,93 +678,202 @@ __global__ void __launch_bounds__(PT_, 3) ppr_push_kernel(PprArgs A) {
       if (blockIdx.x == 0 && threadIdx.x == 0) A.ctl->err = 9;  // NonConvergence
       break;
     }
-    const bool dense = !mark_mode || nF * 32 > (long long)n;
-    int nL = n;
-    if (!dense) {
-      // P2: affected rows (marked this round); heavy ones flagged active
-      nL = grid_compact(
-          g, n,
-          [&](int i, int& v) {
-            v = i;
-            const bool m = A.mark[i] == R;
-            if (m && A.hidx[i] >= 0) A.hact[A.hidx[i]] = R;
-            return m;
-          },
-          A.listL, A.blk);
+    const bool dense = S * 64 > narcs;
+    if (tl && A.trace && rounds <= 1024) {
+      long long* t = A.trace + 4 * (rounds - 1);
+      t[0] = nF;
+      t[1] = dense;
+      t[2] = S;
+      t[3] = nmi;
     }
-    affected += nL;
-    // P3a: light rows, one warp per row; P3b: heavy chunks, one warp per chunk
-    long long my_pulled = 0, my_arcs = 0;
-    for (int q = gw; q < nL; q += nwarps) {
-      const int v = dense ? q : A.listL[q];
-      if (A.hidx[v] >= 0) continue;
-      float acc[KPL];
+    if (dense) {
+      // ---------------- PULL: items = heavy chunks (-(c+1)) then light rows
+      const int nitems = nchunks + n;
+      Grabber gb(wq + WQ_P3, nitems, gw, nw, 4);
+      int start, cnt;
+      while (gb.next(lane, 4, 32, start, cnt)) {
+        const int stop = start + cnt;
+        for (int base = start; base < stop; base += 4) {
+          const int ii = base + grp;
+          int v = -1, h = -1, beg = 0, end = 0;
+          bool valid = ii < stop;
+          if (valid) {
+            if (ii < nchunks) {
+              const int c = ii;
+              h = A.cidx[c];
+              v = A.heavy[h];
+              beg = (c - A.hoff[h]) * CH;
+              end = min(beg + CH, A.out.cnt[v]);
+            } else {
+              v = ii - nchunks;
+              if (A.hidx[v] >= 0) valid = false;
+              else end = A.out.cnt[v];
+            }
+          }
+          const bool big = valid && (h >= 0 || end > SMALL);
+          if (valid && !big) {
+            float acc[CL::NE];
 #pragma unroll
-      for (int t = 0; t < KPL; ++t) acc[t] = 0.0f;
-      const int c = A.out.cnt[v];
-      const int got = pull_range<KPL>(A, A.out.off[v], 0, c, R, k, acc);
-      my_pulled += got;
-      my_arcs += c;
-      finish_row<KPL>(A, v, R, k, om, acc, got > 0);
-    }
-    for (int c = gw; c < nchunks; c += nwarps) {
-      int lo = 0, hi = nH;  // hub h with hoff[h] <= c < hoff[h+1]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (A.hoff[mid] <= c) lo = mid; else hi = mid;
-      }
-      const int h = lo;
-      if (!dense && A.hact[h] != R) continue;
-      const int v = A.heavy[h];
-      const int beg = (c - A.hoff[h]) * CH;
-      const int end = min(beg + CH, A.out.cnt[v]);
-      float acc[KPL];
+            for (int e = 0; e < CL::NE; ++e) acc[e] = 0.0f;
+            const int got = end ? pull_group<PER, VEC>(A, A.out.off[v], 0, end, R, k, gl, gm, acc) : 0;
+            if (gl == 0) {
+              c_aff += 1;
+              c_arcs += end;
+              c_pulled += got;
+            }
+            finish_group<PER, VEC>(A, v, R, k, om, gl, gm, acc, got > 0);
+          }
+          unsigned bm = __ballot_sync(0xffffffffu, big) & 0x01010101u;
+          while (bm) {
+            const int src = __ffs(bm) - 1;
+            bm &= bm - 1;
+            const int bv = __shfl_sync(0xffffffffu, v, src);
+            const int bh = __shfl_sync(0xffffffffu, h, src);
+            const int bb = __shfl_sync(0xffffffffu, beg, src);
+            const int be = __shfl_sync(0xffffffffu, end, src);
+            float acc[CL::NE];
 #pragma unroll
-      for (int t = 0; t < KPL; ++t) acc[t] = 0.0f;
-      my_pulled += pull_range<KPL>(A, A.out.off[v], beg, end, R, k, acc);
-      my_arcs += end - beg;
-      float* part = A.hpart + (int64_t)c * d;
+            for (int e = 0; e < CL::NE; ++e) acc[e] = 0.0f;
+            const int got = pull_warp<PER, VEC>(A, A.out.off[bv], bb, be, R, k, lane, sid, sw, acc);
+            if (lane == 0) {
+              c_aff += bh < 0;
+              c_arcs += be - bb;
+              c_pulled += got;
+            }
+            if (bh >= 0) {
+              // chunk partial -> hacc[bh]; the warp completing the row's last
+              // chunk finishes the row (threadfence-reduction pattern)
+              if (got) {
+                reduce_groups<PER, VEC>(acc);
+                chunk_accumulate<PER, VEC>(A.hacc + (int64_t)bh * d, k, lane, acc);
+              }
+              __threadfence();
+              __syncwarp();
+              int old = 0;
+              if (lane == 0) old = atomicAdd(&A.hdone[bh], 1);
+              old = __shfl_sync(0xffffffffu, old, 0);
+              if (old == A.hoff[bh + 1] - A.hoff[bh] - 1) {
+                __threadfence();
+                float* hrow = A.hacc + (int64_t)bh * d;
+                CL::template load<true>(hrow, gl, k, acc);
+                __syncwarp();
+                if (grp == 0) {
+                  float zero[CL::NE];
 #pragma unroll
-      for (int t = 0; t < KPL; ++t) {
-        const int j = lane + 32 * t;
-        if (j < k) part[j] = acc[t];
-      }
-    }
-    g.sync();
-    // P3c: heavy rows reduce their chunk partials in order
-    for (int h = gw; h < nH; h += nwarps) {
-      if (!dense && A.hact[h] != R) continue;
-      float acc[KPL];
-#pragma unroll
-      for (int t = 0; t < KPL; ++t) acc[t] = 0.0f;
-      for (int c = A.hoff[h]; c < A.hoff[h + 1]; ++c) {
-        const float* part = A.hpart + (int64_t)c * d;
-#pragma unroll
-        for (int t = 0; t < KPL; ++t) {
-          const int j = lane + 32 * t;
-          if (j < k) acc[t] += part[j];
+                  for (int e = 0; e < CL::NE; ++e) zero[e] = 0.0f;
+                  CL::store(hrow, gl, k, zero);
+                }
+                if (lane == 0) {
+                  A.hdone[bh] = 0;
+                  c_aff += 1;
+                }
+                finish_warp<PER, VEC>(A, bv, R, k, om, lane, acc, true);
+              }
+            } else {
+              reduce_groups<PER, VEC>(acc);
+              finish_warp<PER, VEC>(A, bv, R, k, om, lane, acc, got > 0);
+            }
+          }
         }
       }
-      finish_row<KPL>(A, A.heavy[h], R, k, om, acc, true);
-    }
-    if (lane == 0) {
-      atomicAdd((unsigned long long*)&A.stats[5], (unsigned long long)my_arcs);   // accounting only
-      atomicAdd((unsigned long long*)&A.stats[6], (unsigned long long)my_pulled);
+    } else {
+      // ---------------- SCATTER over the pushed rows' in-arc chunks
+      int* L = A.items[cur];
+      Grabber gb(wq + WQ_MK, nmi, gw, nw, 1);
+      int start, cnt;
+      while (gb.next(lane, 1, 4, start, cnt)) {
+        for (int it = start; it < start + cnt; ++it) {
+          const int u = A.mitems[2 * it], ci = A.mitems[2 * it + 1];
+          const int64_t ib = inC.off[u];
+          const int beg = ci * MCH, end = min(beg + MCH, inC.cnt[u]);
+          float x[CL::NE];
+          CL::load(A.delta + (int64_t)u * d, gl, k, x);
+          if (lane == 0) c_arcs += end - beg;
+          for (int p0 = beg; p0 < end; p0 += 32) {
+            const int p = p0 + lane;
+            const bool ok = p < end;
+            int v = 0;
+            float coef = 0.0f;
+            if (ok) {
+              v = inC.ids[ib + p];
+              const double w = inC.wts ? inC.wts[ib + p] : 1.0;
+              coef = (float)(om * w / fmax(A.deg[v], 1.0));
+            }
+            const bool t = ok && atomicExch(&A.mark[v], R) != R;
+            const unsigned tm = __ballot_sync(0xffffffffu, t);
+            if (tm) {
+              unsigned long long b0 = 0;
+              const int leader = __ffs(tm) - 1;
+              if (lane == leader)
+                b0 = atomicAdd(&sc[(SC_ITEMS + par) * QS], (unsigned long long)__popc(tm));
+              b0 = __shfl_sync(0xffffffffu, b0, leader);
+              if (t) L[b0 + __popc(tm & lt)] = v;
+              if (lane == 0) c_aff += __popc(tm);
+            }
+            const int na = min(32, end - p0);
+            for (int a0 = 0; a0 < na; a0 += 4) {
+              const int a = a0 + grp;
+              const int va = __shfl_sync(0xffffffffu, v, a);
+              const float ca = __shfl_sync(0xffffffffu, coef, a);
+              if (a >= na) continue;
+              float* rv = A.rb + (int64_t)va * d;
+              if (VEC) {
+#pragma unroll
+                for (int t4 = 0; t4 < PER; ++t4) {
+                  const int j = 4 * gl + 32 * t4;
+                  if (j < k)
+                    atomicAdd(reinterpret_cast<float4*>(rv + j),
+                              make_float4(ca * x[4 * t4], ca * x[4 * t4 + 1], ca * x[4 * t4 + 2],
+                                          ca * x[4 * t4 + 3]));
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < CL::NE; ++e) {
+                  const int j = gl + G * e;
+                  if (j < k) atomicAdd(rv + j, ca * x[e]);
+                }
+              }
+            }
+          }
+        }
+      }
     }
     g.sync();
-    // next candidates: every row (dense) or the affected list (sparse)
+    tmark(dense ? 26 : 27);
+    const int ntouched = dense ? 0 : (int)*(volatile unsigned long long*)&sc[(SC_ITEMS + par) * QS];
+    if (blockIdx.x == 0) {
+      if (threadIdx.x < NQ) {
+        wq[WQ_P3 + threadIdx.x * QS] = 0;
+        wq[WQ_MK + threadIdx.x * QS] = 0;
+      }
+      if (threadIdx.x == 0) {
+        sc[(SC_MITEMS + par) * QS] = 0;
+      }
+    }
     cand_all = dense;
-    ncand = dense ? n : nL;
-    candL = A.listL;
-    mark_mode = nF * 32 <= (long long)n;
+    fresh = !dense;
+    ncand = dense ? n : ntouched;
+    candL = A.items[cur];
+    cur ^= 1;
   }
-  for (int i = blockIdx.x * PT_ + threadIdx.x; i < nH; i += gridDim.x * PT_) A.hidx[A.heavy[i]] = -1;
+  for (int h = blockIdx.x * PT_ + threadIdx.x; h < nH; h += gridDim.x * PT_) A.hidx[A.heavy[h]] = -1;
+  // accounting (bench algorithmic bytes): lane-0 counters of groups/warps
+  for (int o = 16; o > 0; o >>= 1) {
+    c_aff += __shfl_xor_sync(0xffffffffu, c_aff, o);
+    c_arcs += __shfl_xor_sync(0xffffffffu, c_arcs, o);
+    c_pulled += __shfl_xor_sync(0xffffffffu, c_pulled, o);
+  }
+  if (lane == 0 && (c_aff | c_arcs | c_pulled)) {
+    atomicAdd((unsigned long long*)&A.stats[4], (unsigned long long)c_aff);
+    atomicAdd((unsigned long long*)&A.stats[5], (unsigned long long)c_arcs);
+    atomicAdd((unsigned long long*)&A.stats[6], (unsigned long long)c_pulled);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (A.trace) A.trace[4 * 1024] = rounds;
     A.stats[0] += pushes;
     A.stats[1] += rounds;
     A.stats[2] = R;  // next round base
     A.stats[3] += pushes;
-    A.stats[4] += affected;
     if (A.t_end) *A.t_end = globaltimer();
   }
 }
@@ -481,20 +982,43 @@ __global__ void smax_kernel(const double* PT0, const double* PT1, const DevCtl* 
 
 }  // namespace
 
-cudaError_t launch_ppr_push(const PprArgs& a, int grid, cudaStream_t s) {
+namespace {
+template <int PER, bool VEC>
+cudaError_t launch_push_t(const PprArgs& a, int grid, cudaStream_t s) {
   void* args[] = {(void*)&a};
-  if (a.d <= 128)
-    return cudaLaunchCooperativeKernel((void*)ppr_push_kernel<4>, dim3(grid), dim3(PT_), args, 0, s);
-  return cudaLaunchCooperativeKernel((void*)ppr_push_kernel<8>, dim3(grid), dim3(PT_), args, 0, s);
+  return cudaLaunchCooperativeKernel((void*)ppr_push_kernel<PER, VEC>, dim3(grid), dim3(PT_), args, 0, s);
+}
+template <int PER, bool VEC>
+int max_grid_t(int nsm) {
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ppr_push_kernel<PER, VEC>, PT_, 0);
+  return per * nsm;
+}
+}  // namespace
+
+// Vectorised kernels when rows are 16-byte aligned (d % 4 == 0), otherwise a
+// scalar column slice; PER sized to the row width d.
+cudaError_t launch_ppr_push(const PprArgs& a, int grid, cudaStream_t s) {
+  const int d = a.d;
+  if (d % 4 == 0) {
+    if (d <= 32) return launch_push_t<1, true>(a, grid, s);
+    if (d <= 64) return launch_push_t<2, true>(a, grid, s);
+    if (d <= 128) return launch_push_t<4, true>(a, grid, s);
+    return launch_push_t<8, true>(a, grid, s);
+  }
+  if (d <= 32) return launch_push_t<4, false>(a, grid, s);
+  return launch_push_t<32, false>(a, grid, s);
 }
 
 int ppr_push_max_grid(int nsm, int d) {
-  int per = 0;
-  if (d <= 128)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ppr_push_kernel<4>, PT_, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ppr_push_kernel<8>, PT_, 0);
-  return per * nsm;
+  if (d % 4 == 0) {
+    if (d <= 32) return max_grid_t<1, true>(nsm);
+    if (d <= 64) return max_grid_t<2, true>(nsm);
+    if (d <= 128) return max_grid_t<4, true>(nsm);
+    return max_grid_t<8, true>(nsm);
+  }
+  if (d <= 32) return max_grid_t<4, false>(nsm);
+  return max_grid_t<32, false>(nsm);
 }
 
 cudaError_t launch_ppr_absorb(const PprArgs& a, const int64_t* rows, int nrows, cudaStream_t s) {

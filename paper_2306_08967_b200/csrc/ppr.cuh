@@ -3,6 +3,9 @@
 
 namespace dgpu {
 
+constexpr int PPR_HEAVY = 256;  // rows with more out-arcs are pulled in chunks
+constexpr int PPR_CH = 256;     // arcs per chunk
+
 struct PprArgs {
   int64_t n;
   int d, k;
@@ -16,12 +19,18 @@ struct PprArgs {
   int* listF;
   int* listL;
   int* blk;
-  long long* blk64;   // per-block push counts (gridDim)
-  int* heavy;         // heavy-row list (n)
+  long long* blk64;   // scratch (gridDim)
+  int* heavy;         // heavy-row list (rows with > HEAVY out-arcs)
   int* hidx;          // row -> heavy index or -1 (n, kept at -1 between calls)
-  int* hoff;          // heavy chunk prefix (n+1)
-  int* hact;          // heavy row active stamp (n)
-  float* hpart;       // chunk partial sums (arcs/CH + n) x d
+  int* hoff;          // heavy chunk prefix (nH + 1)
+  int* cidx;          // chunk -> heavy index (arc pool / CH + nH)
+  float* hacc;        // heavy-row pull accumulators (nH x d, kept zero between rounds)
+  int* items[2];      // P3 work lists, alternating per round (n + chunks)
+  int* hdone;         // per heavy row: chunks finished this round (kept zero between rounds)
+  int* mitems;        // marking items (pusher, in-arc chunk) pairs
+  long long* trace;   // per-round [nF, dense, items, active heavy] of the last call (4 x 1024)
+  unsigned long long* wq;  // work counters [P1 grab, P3 grab, big-mark count, push count x3,
+                           //  item count, active heavy count]
   DevCSR out, in;
   int directed;
   double* deg;

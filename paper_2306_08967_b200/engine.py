@@ -175,7 +175,10 @@ class Engine:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: module globals already torn down
+            pass
 
     def _check(self, st, index=-1):
         if st:
