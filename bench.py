@@ -254,6 +254,31 @@ def run_ours(args):
     print(json.dumps(out))
 
 
+def ncu_traffic(fname, kernel_substr):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes) of the first
+    launch of `kernel_substr` in a committed `ncu --set full` raw capture under
+    profiles/ (per launch, like roofline.achieved), or None."""
+    import csv
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", fname)
+    if not os.path.exists(path):
+        return None
+    rows = list(csv.reader(open(path)))
+    if len(rows) < 3:
+        return None
+    head, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    for row in rows[2:]:
+        rec = dict(zip(head, row))
+        if kernel_substr not in rec.get("Kernel Name", ""):
+            continue
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = head.index(m)
+            tot += float(row[i].replace(",", "")) * scale.get(units[i], 1.0)
+        return int(tot)
+    return None
+
+
 def bench_materialize(args, hbm, peak_kind):
     """Z = X F on the cfg-4 shape (n = 2^23, X ~ N(0,1/d), F = Q diag(U[.5,2]))."""
     import torch
@@ -282,7 +307,10 @@ def bench_materialize(args, hbm, peak_kind):
         if d == 128:
             roof = {"kernel": "materialize (Z=X.F, n=8388608, d=128)", "bound": "hbm",
                     "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(gbs / hbm, 4), "traffic": None, "peak_kind": peak_kind,
+                    "frac": round(gbs / hbm, 4),
+                    "traffic": ncu_traffic("r1_mat128_raw.csv", "materialize_tc128"),
+                    "traffic_source": "profiles/r1_mat128_raw.csv (ncu --set full, same shape)",
+                    "peak_kind": peak_kind,
                     "algorithmic_bytes_per_launch": int(bytes_), "launch_ms": round(t, 4)}
         del X, Z
         torch.cuda.empty_cache()
@@ -380,7 +408,10 @@ def bench_ppr(args, hbm, peak_kind):
                                         "GBps": round(b_push / (ms_push * 1e-3) / 1e9, 1)},
             "roofline": {"kernel": "ppr_push_kernel (init_propagate)", "bound": "hbm",
                          "achieved": round(gbs_init, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(gbs_init / hbm, 4), "traffic": None,
+                         "frac": round(gbs_init / hbm, 4),
+                         "traffic": ncu_traffic("r1_ppr23_raw.csv", "ppr_push_kernel"),
+                         "traffic_source": "profiles/r1_ppr23_raw.csv (ncu --set full, init_propagate "
+                                           "on the same graph)",
                          "peak_kind": peak_kind}}
 
 
