@@ -212,6 +212,10 @@ def run_ours(args):
         sub["materialize"], roofline = bench_materialize(args, hbm, peak_kind)
         if not args.quick:
             sub["ppr_push"] = bench_ppr(args, hbm, peak_kind)
+        if args.cfg3_events > 0:
+            sub["cfg3"] = bench_cfg3(args)
+        if args.cfg5_events > 0:
+            sub["cfg5"] = bench_cfg5(args, hbm)
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(data, per, args)
@@ -415,6 +419,129 @@ def bench_ppr(args, hbm, peak_kind):
                          "peak_kind": peak_kind}}
 
 
+def stream_latencies(eng, ev, batch, max_events):
+    """Apply ev[:max_events] in batches of `batch` events (one apply call per
+    batch, sequential inside); per-event device latencies (us) and the wall
+    time of the calls."""
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    lat = []
+    t_wall = 0.0
+    rebases = folds = 0
+    m = min(len(ev), max_events)
+    for a in range(0, m, batch):
+        part = ev.slice(a, min(m, a + batch))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = eng.apply(part, mode=ge.APPLY_TIME_EVENTS)
+        rebases += st["rebases"]
+        folds += st["eager_folds"]
+        torch.cuda.synchronize()
+        t_wall += time.perf_counter() - t0
+        lat.extend(eng.latencies_us().tolist())
+    lat = np.array(lat)
+    return {"events": int(m), "batch": batch,
+            "p50_us": round(float(np.percentile(lat, 50)), 2),
+            "p90_us": round(float(np.percentile(lat, 90)), 2),
+            "p99_us": round(float(np.percentile(lat, 99)), 2),
+            "device_events_per_s": round(m / (lat.sum() * 1e-6), 1),
+            "e2e_events_per_s": round(m / t_wall, 1), "rebases": int(rebases),
+            "eager_folds": int(folds), "cond_end": float(eng.diag()["cond_estimate"])}
+
+
+def bench_cfg3(args):
+    """Config 3: R-MAT scale 22, ef 16 (seed 2), d = 128, all but 100,000
+    edges in the snapshot (randomized t-SVD on the device), held-out edges
+    streamed as insertions in batches of 1, 64 and 1024 (alpha = 1)."""
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    from paper_2306_08967_b200 import workloads as W
+    t0 = time.time()
+    scale, d = 22, 128
+    n = 1 << scale
+    keys = W.rmat_keys_device(scale, 16, 2)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(2)
+    held = torch.randperm(keys.numel(), generator=g, device="cuda")[:100_000]
+    drop = torch.zeros(keys.numel(), dtype=torch.bool, device="cuda")
+    drop[held] = True
+    off, tgt = W.csr_from_keys_device(n, keys, drop)
+    hk = keys[held]
+    su, sv = (hk >> 32).cpu().numpy(), (hk & 0xFFFFFFFF).cpu().numpy()
+    edges = int(keys.numel())
+    del keys, drop, hk, held
+    X, Y, s = W.tsvd_factors_device(n, off, tgt, d, seed=2)
+    gen_s = time.time() - t0
+    k = len(s)
+    eng = ge.Engine(n, off, tgt, None, d, k, X, Y, np.eye(k), np.eye(k), s, alpha=1.0,
+                    undirected=True, node_capacity=1024, arc_capacity=1 << 22)
+    del X, Y, off, tgt
+    torch.cuda.empty_cache()
+    ev = W.EventList.edges(ge.ADD_EDGE, su, sv)
+    res = {"graph": f"R-MAT scale 22 ef 16 (n={n}, edges={edges}), d=128, alpha=1",
+           "setup_s": round(gen_s, 1)}
+    a = 0
+    for batch, m in ((1, args.cfg3_events // 4), (64, args.cfg3_events // 2),
+                     (1024, args.cfg3_events)):
+        r = stream_latencies(eng, ev.slice(a, len(ev)), batch, m)
+        a += r["events"]
+        res[f"batch{batch}"] = r
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_cfg5(args, hbm):
+    """Config 5: R-MAT scale 26, ef 16 (seed 4), int32 ids / int64 offsets,
+    d = 128, U and V random orthonormal columns with sigma_i = i^-0.5 (34 GB
+    each, generated in place on the device), 10,000 degree-proportional
+    single-edge insertions, one full materialisation X = X_b P_X."""
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    from paper_2306_08967_b200 import workloads as W
+    t0 = time.time()
+    scale, d = 26, 128
+    n = 1 << scale
+    keys = W.rmat_keys_device(scale, 16, 4)
+    off, tgt = W.csr_from_keys_device(n, keys)
+    su, sv = W.degree_proportional_inserts(keys, tgt, args.cfg5_events, seed=4)
+    edges = int(keys.numel())
+    del keys
+    torch.cuda.empty_cache()
+    sig = np.arange(1, d + 1, dtype=np.float64) ** -0.5
+    eng = ge.Engine(n, off, tgt, None, d, d, None, None, np.eye(d), np.eye(d), sig, alpha=1.0,
+                    undirected=True, node_capacity=1024, arc_capacity=1 << 24)
+    arcs = int(tgt.numel())
+    del off, tgt
+    torch.cuda.empty_cache()
+    W.orthonormal_rows_into(eng, ge.XB, n, d, sig, seed=40)
+    W.orthonormal_rows_into(eng, ge.YB, n, d, sig, seed=41)
+    setup_s = time.time() - t0
+    ev = W.EventList.edges(ge.ADD_EDGE, su, sv)
+    r = stream_latencies(eng, ev, 1000, len(ev))
+    # one full materialisation X = X_b P_X into device memory
+    out = torch.empty(n, d, dtype=torch.float32, device="cuda")
+    es = torch.cuda.ExternalStream(eng.stream_ptr())
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(es)
+    eng.materialize(ge.X, out.data_ptr(), on_device=True)
+    e1.record(es)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    gbs = 8.0 * n * d / (ms * 1e-3) / 1e9
+    dg = eng.diag()
+    eng.close()
+    del eng, out
+    torch.cuda.empty_cache()
+    return {"graph": f"R-MAT scale 26 ef 16 (n={n}, edges={edges}, arcs={arcs}), d=128, alpha=1",
+            "setup_s": round(setup_s, 1), "updates": r,
+            "materialize": {"ms": round(ms, 3), "GBps": round(gbs, 1),
+                            "frac": round(gbs / hbm, 4)},
+            "device_bytes": dg["device_bytes"]}
+
+
 def cpu_baseline(data, per, args, max_events=None, budget_s=None):
     """The oracle port (fp64, 1 thread) on the same initial state and the
     first events of the same stream."""
@@ -489,6 +616,10 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ppr-scale", type=int, default=23)
+    ap.add_argument("--cfg3-events", type=int, default=4096,
+                    help="events per batch-size leg of config 3 (0 = skip)")
+    ap.add_argument("--cfg5-events", type=int, default=10000,
+                    help="insertions streamed at config 5 (0 = skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

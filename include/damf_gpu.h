@@ -83,7 +83,9 @@ typedef struct damf_config {
   int64_t arc_capacity;  /* arc slots to reserve beyond arcs (0=auto)     */
 } damf_config;
 
-/* Out-adjacency in CSR form (host memory). weights may be NULL (all 1.0). */
+/* Out-adjacency in CSR form. Arrays may be host or device memory (detected
+ * with cudaPointerGetAttributes; device arrays are consumed in place).
+ * weights may be NULL (all 1.0). */
 typedef struct damf_csr {
   int64_t n;
   int64_t arcs;
@@ -144,9 +146,11 @@ typedef struct damf_gpu damf_gpu; /* opaque handle: owns all device memory */
 /* Engine(g, fs, es, cfg, 0, 0) with fs = FactorState(xb, yb, px, py, sigma, d)
  * (factor_state.hpp:22-23, engine.hpp:32-34) followed by
  * EnhancerState::init_propagate (enhancer.cpp:26-47). xb/yb: n x k fp32
- * row-major host arrays; px/py: k x k fp64; sigma: k fp64, nonincreasing. */
+ * row-major arrays in host or device memory, or NULL for zero rows to be
+ * filled with damf_gpu_load_rows; px/py: k x k fp64 host; sigma: k fp64
+ * host, nonincreasing. */
 int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int64_t k,
-                                 const float* xb_host, const float* yb_host,
+                                 const float* xb, const float* yb,
                                  const double* px_host, const double* py_host,
                                  const double* sigma_host, damf_gpu** out);
 
@@ -164,12 +168,20 @@ int damf_gpu_sync(damf_gpu* h);
 int damf_gpu_apply(damf_gpu* h, const damf_event_batch* batch, int32_t mode,
                    damf_apply_stats* stats);
 
+/* FactorState(xb, yb, ...) row by row: copy m rows (m x k fp32, host or
+ * device memory) into X_b (which = DAMF_XB) or Y_b (DAMF_YB) starting at
+ * row0. Lets a caller build huge states (config 5: 34 GB per factor) in
+ * pieces after damf_gpu_create_from_factors(..., xb = yb = NULL, ...).
+ * With alpha != 1 call damf_gpu_ppr_init afterwards. */
+int damf_gpu_load_rows(damf_gpu* h, int32_t which, int64_t row0, int64_t m, const float* src);
+
 /* Per-event device latency (microseconds) of the last apply with
  * DAMF_APPLY_TIME_EVENTS: fills min(max, count) values, returns count. */
 int64_t damf_gpu_event_latencies(damf_gpu* h, double* out_us_host, int64_t max);
 
 /* Engine::context/content/enhanced (engine.hpp:45-47) for m rows:
- * out_host[m x k] fp32 (which = DAMF_X, DAMF_Y or DAMF_Z). */
+ * out_host[m x k] fp32 (which = DAMF_X, DAMF_Y or DAMF_Z). which = DAMF_XB /
+ * DAMF_YB / DAMF_ZB / DAMF_RB returns the raw base-coordinate rows. */
 int damf_gpu_query_rows(damf_gpu* h, int32_t which, const int64_t* ids_host, int64_t m,
                         float* out_host);
 

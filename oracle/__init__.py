@@ -55,6 +55,9 @@ def lib():
         L.oracle_edge_update_rowlocal.argtypes = [C.c_int64, C.c_int64, f64p, f64p, f64p, f64p,
                                                   f64p, C.c_double, C.c_int, f64p, f64p, f64p,
                                                   f64p, f64p, i64p]
+        L.oracle_edge_update_rowlocal_p.argtypes = [C.c_int64, C.c_int64, f64p, f64p, f64p,
+                                                    f64p, f64p, C.c_double, f64p, f64p, f64p,
+                                                    f64p, f64p, f64p, f64p, i64p]
         for fn in ("oracle_gen_mixed_stream", "oracle_gen_random_graph", "oracle_gen_sbm2"):
             getattr(L, fn).restype = C.c_void_p
         L.oracle_gen_mixed_stream.argtypes = [C.c_int64] * 4 + [C.c_uint64]
@@ -265,3 +268,27 @@ def edge_update_rowlocal(k, d, xu, yv, px, py, sigma, w):
     k2 = k2.value
     return dict(sigma2=s2[:k2], F=F[:k * k2].reshape(k, k2), G=G[:k * k2].reshape(k, k2),
                 xu=xn[:k2], yv=yn[:k2])
+
+
+def edge_update_rowlocal_p(k, d, xu, yv, px, py, sigma, w):
+    """edge_update_rowlocal, also returning the projections after
+    apply_update (eager fold possible): current rows = xu @ px, yv @ py."""
+    xu, yv, px, py, sigma = (np.ascontiguousarray(a, np.float64) for a in (xu, yv, px, py, sigma))
+    s2 = np.zeros(k + 1)
+    F = np.zeros((k + 1) * (k + 1))
+    G = np.zeros((k + 1) * (k + 1))
+    xn = np.zeros(k + 1)
+    yn = np.zeros(k + 1)
+    pxn = np.zeros((k + 1) * (k + 1))
+    pyn = np.zeros((k + 1) * (k + 1))
+    k2 = C.c_int64()
+    st = lib().oracle_edge_update_rowlocal_p(k, d, _p(xu, f64p), _p(yv, f64p), _p(px, f64p),
+                                             _p(py, f64p), _p(sigma, f64p), w, _p(s2, f64p),
+                                             _p(F, f64p), _p(G, f64p), _p(xn, f64p), _p(yn, f64p),
+                                             _p(pxn, f64p), _p(pyn, f64p), C.byref(k2))
+    if st:
+        raise OracleError(st, lib().oracle_last_error().decode())
+    k2 = k2.value
+    return dict(sigma2=s2[:k2], F=F[:k * k2].reshape(k, k2), G=G[:k * k2].reshape(k, k2),
+                xu=xn[:k2], yv=yn[:k2], px=pxn[:k2 * k2].reshape(k2, k2),
+                py=pyn[:k2 * k2].reshape(k2, k2))

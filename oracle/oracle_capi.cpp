@@ -287,6 +287,42 @@ int oracle_edge_update_rowlocal(int64_t k, int64_t d, const double* xu, const do
   }
 }
 
+// Same update, also returning the projections after apply_update (which may
+// have folded eagerly): current rows are xu_new * px_new, yv_new * py_new.
+int oracle_edge_update_rowlocal_p(int64_t k, int64_t d, const double* xu, const double* yv,
+                                  const double* px, const double* py, const double* sigma,
+                                  double w, double* sigma2, double* F, double* G, double* xu_new,
+                                  double* yv_new, double* px_new, double* py_new,
+                                  int64_t* k2_out) {
+  try {
+    Mat xb(2, k), yb(2, k);
+    for (int64_t j = 0; j < k; ++j) {
+      xb(0, j) = xu[j];
+      yb(1, j) = yv[j];
+    }
+    FactorState s(xb, yb, from_ptr(px, k, k), from_ptr(py, k, k), Vec(sigma, sigma + k), d);
+    ProjectionUpdate pu = update_embedding_e(s, SparseVec::unit(2, 0), SparseVec::unit(2, 1, w));
+    s.apply_update(pu);
+    const int64_t k2 = static_cast<int64_t>(pu.sigma2.size());
+    *k2_out = k2;
+    std::memcpy(sigma2, pu.sigma2.data(), sizeof(double) * k2);
+    std::memcpy(F, pu.F.a.data(), sizeof(double) * pu.F.a.size());
+    std::memcpy(G, pu.G.a.data(), sizeof(double) * pu.G.a.size());
+    for (int64_t j = 0; j < k2; ++j) {
+      xu_new[j] = s.xb()(0, j);
+      yv_new[j] = s.yb()(1, j);
+    }
+    for (int64_t i = 0; i < k2; ++i)
+      for (int64_t j = 0; j < k2; ++j) {
+        px_new[i * k2 + j] = s.px()(i, j);
+        py_new[i * k2 + j] = s.py()(i, j);
+      }
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
 // ---- generators (eval.cpp:616-705) -----------------------------------------
 struct OStream {
   StreamCase sc;

@@ -291,7 +291,17 @@ EventKernelArgs event_args(damf_gpu* h) {
       a.Q[s][p] = h->Q[s][p];
     }
   a.sigma = h->sigma;
+  // Base rows are fp32 (the reference keeps fp64): a row written through
+  // solve(P^T, .) carries components ~cond(P) larger than its current value,
+  // and the maintained P^-1 drifts in proportion to cond(P), so fp32 storage
+  // costs ~6e-8 * cond(P) relative accuracy. Rebasing (an exact change of
+  // representation, engine.cpp:38-47) when either projection's Frobenius
+  // condition bound passes kStorageSafeCond keeps current-coordinate results
+  // within the 1e-4 parity bar; the reference's own trigger (cond(P_X) >
+  // rebase_cond) applies as well.
+  constexpr double kStorageSafeCond = 1e4;
   a.rebase_cond = h->cfg.rebase_cond;
+  a.storage_cond = kStorageSafeCond;
   a.out = h->out;
   a.in = h->in;
   a.directed = h->directed;
@@ -301,6 +311,16 @@ EventKernelArgs event_args(damf_gpu* h) {
   a.ws_Q1T = h->ws;
   a.ws_priv = h->ws + m;
   return a;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
 PprArgs ppr_args(damf_gpu* h) {
@@ -415,6 +435,11 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
                                  const float* xb, const float* yb, const double* px,
                                  const double* py, const double* sigma, damf_gpu** outp) {
   *outp = nullptr;
+  // device-resident inputs may still be produced on other streams
+  if (is_device_ptr(g->offsets) || is_device_ptr(g->targets) || is_device_ptr(xb) ||
+      is_device_ptr(yb)) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return DAMF_E_CUDA;
+  }
   auto* h = new damf_gpu();
   h->cfg = *cfg;
   if (cfg->d < 1 || cfg->d > kMaxD || k < 1 || k > cfg->d) {
@@ -445,8 +470,10 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   CK(dalloc(h, &h->Yb, (size_t)ncap * d));
   CK(cudaMemsetAsync(h->Xb, 0, (size_t)ncap * d * 4, h->st));
   CK(cudaMemsetAsync(h->Yb, 0, (size_t)ncap * d * 4, h->st));
-  CK(cudaMemcpy2DAsync(h->Xb, d * 4, xb, k * 4, k * 4, n, cudaMemcpyHostToDevice, h->st));
-  CK(cudaMemcpy2DAsync(h->Yb, d * 4, yb, k * 4, k * 4, n, cudaMemcpyHostToDevice, h->st));
+  // xb / yb: host or device memory (cudaMemcpyDefault); NULL = zero rows,
+  // filled later with damf_gpu_load_rows
+  if (xb && n) CK(cudaMemcpy2DAsync(h->Xb, d * 4, xb, k * 4, k * 4, n, cudaMemcpyDefault, h->st));
+  if (yb && n) CK(cudaMemcpy2DAsync(h->Yb, d * 4, yb, k * 4, k * 4, n, cudaMemcpyDefault, h->st));
   for (int s = 0; s < 2; ++s)
     for (int p = 0; p < 2; ++p) {
       CK(dalloc(h, &h->PT[s][p], (size_t)ld * ld));
@@ -502,11 +529,36 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   // ---- graph (slack CSR)
   {
     const int64_t arcs = g->arcs;
+    // CSR arrays may live in host or device memory. Offsets are needed on the
+    // host for the slack layout; device targets are expanded in place; a
+    // directed graph's in-CSR transpose is built on the host.
+    std::vector<int64_t> hoff_v;
+    const int64_t* hoff = g->offsets;
+    if (is_device_ptr(g->offsets)) {
+      hoff_v.resize(n + 1);
+      CK(cudaMemcpy(hoff_v.data(), g->offsets, (n + 1) * 8, cudaMemcpyDeviceToHost));
+      hoff = hoff_v.data();
+    }
+    const bool tgt_dev = arcs > 0 && is_device_ptr(g->targets);
+    std::vector<int32_t> htgt_v;
+    std::vector<double> hw_v;
+    const int32_t* htgt = g->targets;
+    const double* hw = g->weights;
+    if (h->directed && tgt_dev) {
+      htgt_v.resize(arcs);
+      CK(cudaMemcpy(htgt_v.data(), g->targets, arcs * 4, cudaMemcpyDeviceToHost));
+      htgt = htgt_v.data();
+      if (g->weights) {
+        hw_v.resize(arcs);
+        CK(cudaMemcpy(hw_v.data(), g->weights, arcs * 8, cudaMemcpyDeviceToHost));
+        hw = hw_v.data();
+      }
+    }
     std::vector<int64_t> noff(n + 1);
     int64_t pos = 0;
     for (int64_t u = 0; u < n; ++u) {
       noff[u] = pos;
-      const int64_t c = g->offsets[u + 1] - g->offsets[u];
+      const int64_t c = hoff[u + 1] - hoff[u];
       pos += c + std::max<int64_t>(4, c >> 3);
     }
     noff[n] = pos;
@@ -531,14 +583,20 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
       int64_t *d_coff = nullptr, *d_noff = nullptr;
       int32_t* d_cids = nullptr;
       double* d_cw = nullptr;
+      const bool dev_in = arcs > 0 && is_device_ptr(cids);
       CK(cudaMalloc(&d_coff, (n + 1) * 8));
       CK(cudaMalloc(&d_noff, (n + 1) * 8));
-      CK(cudaMalloc(&d_cids, std::max<int64_t>(arcs, 1) * 4));
-      if (cw) CK(cudaMalloc(&d_cw, std::max<int64_t>(arcs, 1) * 8));
+      if (dev_in) {
+        d_cids = const_cast<int32_t*>(cids);
+        d_cw = const_cast<double*>(cw);
+      } else {
+        CK(cudaMalloc(&d_cids, std::max<int64_t>(arcs, 1) * 4));
+        if (cw) CK(cudaMalloc(&d_cw, std::max<int64_t>(arcs, 1) * 8));
+        if (arcs) CK(cudaMemcpyAsync(d_cids, cids, arcs * 4, cudaMemcpyHostToDevice, h->st));
+        if (cw && arcs) CK(cudaMemcpyAsync(d_cw, cw, arcs * 8, cudaMemcpyHostToDevice, h->st));
+      }
       CK(cudaMemcpyAsync(d_coff, coff.data(), (n + 1) * 8, cudaMemcpyHostToDevice, h->st));
       CK(cudaMemcpyAsync(d_noff, slack_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, h->st));
-      if (arcs) CK(cudaMemcpyAsync(d_cids, cids, arcs * 4, cudaMemcpyHostToDevice, h->st));
-      if (cw && arcs) CK(cudaMemcpyAsync(d_cw, cw, arcs * 8, cudaMemcpyHostToDevice, h->st));
       if (n > 0)
         csr_expand_kernel<<<(int)std::min<int64_t>(n, 65535), 128, 0, h->st>>>(
             n, d_coff, d_cids, d_cw, d_noff, c.ids, c.wts, c.cnt, c.cap, c.off);
@@ -548,26 +606,30 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
       CK(cudaStreamSynchronize(h->st));
       cudaFree(d_coff);
       cudaFree(d_noff);
-      cudaFree(d_cids);
-      if (d_cw) cudaFree(d_cw);
+      if (!dev_in) {
+        cudaFree(d_cids);
+        if (d_cw) cudaFree(d_cw);
+      }
       return 0;
     };
-    std::vector<int64_t> coff(g->offsets, g->offsets + n + 1);
-    if (int r = build(h->out, coff, g->targets, g->weights, noff)) return r;
+    std::vector<int64_t> coff(hoff, hoff + n + 1);
+    if (int r = build(h->out, coff, tgt_dev && !h->directed ? g->targets : htgt,
+                      tgt_dev && !h->directed ? g->weights : hw, noff))
+      return r;
     if (h->directed) {
       // in-CSR by counting transpose (host; directed graphs are the small
       // reference-test configurations)
       std::vector<int64_t> ioff(n + 1, 0);
-      for (int64_t p = 0; p < arcs; ++p) ioff[g->targets[p] + 1]++;
+      for (int64_t p = 0; p < arcs; ++p) ioff[htgt[p] + 1]++;
       for (int64_t u = 0; u < n; ++u) ioff[u + 1] += ioff[u];
       std::vector<int32_t> iids(std::max<int64_t>(arcs, 1));
       std::vector<double> iw(weighted ? std::max<int64_t>(arcs, 1) : 0);
       std::vector<int64_t> fill(ioff.begin(), ioff.end() - 1);
       for (int64_t u = 0; u < n; ++u)
-        for (int64_t p = g->offsets[u]; p < g->offsets[u + 1]; ++p) {
-          const int64_t at = fill[g->targets[p]]++;
+        for (int64_t p = hoff[u]; p < hoff[u + 1]; ++p) {
+          const int64_t at = fill[htgt[p]]++;
           iids[at] = (int32_t)u;
-          if (weighted) iw[at] = g->weights[p];
+          if (weighted) iw[at] = hw[p];
         }
       std::vector<int64_t> inoff(n + 1);
       int64_t ip = 0;
@@ -675,13 +737,15 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
 int damf_gpu_rebase(damf_gpu* h) {
   if (int r = sync_ctl(h)) return r;
   const int k = h->k, d = h->d, ld = h->ld;
+  // folds use fp64 accumulation: P may be ill-conditioned here (cond up to
+  // rebase_cond = 1e8), where fp32 / 3xTF32 products lose the digits
   float* tmp = nullptr;
   if (k > 128) CK(cudaMalloc(&tmp, (size_t)h->n * d * 4));
   auto fold = [&](float* base, const double* PT) -> int {
     if (!tmp) {
-      CK(launch_materialize(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
+      CK(launch_materialize_precise(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
     } else {
-      CK(launch_materialize(base, h->n, k, d, PT, ld, k, tmp, d, h->st, h->nsm));
+      CK(launch_materialize_precise(base, h->n, k, d, PT, ld, k, tmp, d, h->st, h->nsm));
       CK(cudaMemcpyAsync(base, tmp, (size_t)h->n * d * 4, cudaMemcpyDeviceToDevice, h->st));
     }
     return 0;
@@ -933,17 +997,24 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         }
       }
     }
-    for (int64_t e = i; e < j; ++e)
-      if (h->ev.h[e].kind == DAMF_ADD_NODE) h->n = h->ev.h[e].u + 1;
     if (int r = sync_ctl(h)) return r;
+    // a batch kernel stops right after an event that requested a rebase
+    // (cond trigger, storage bound or an exact-inverse step): rebase over the
+    // whole GPU and resume with the next event, as engine.cpp:38-40 orders it
+    int64_t done = j;
+    const bool stopped = (!ppr || fused) && !h->h_ctl->err && h->h_ctl->need_rebase &&
+                         h->h_ctl->stop_event > i && h->h_ctl->stop_event < j;
+    if (stopped) done = h->h_ctl->stop_event;
+    for (int64_t e = i; e < done; ++e)
+      if (h->ev.h[e].kind == DAMF_ADD_NODE) h->n = h->ev.h[e].u + 1;
     if (h->h_ctl->err) break;
-    h->events_applied += (uint64_t)(j - i);
-    h->since_rebase += (j - i);
-    if (h->cfg.rebase_every > 0 && h->since_rebase >= h->cfg.rebase_every) {
+    h->events_applied += (uint64_t)(done - i);
+    h->since_rebase += (done - i);
+    if (stopped || (h->cfg.rebase_every > 0 && h->since_rebase >= h->cfg.rebase_every)) {
       if (int r = damf_gpu_rebase(h)) return r;
       ++rebases;
     }
-    i = j;
+    i = done;
   }
   if (int r = sync_ctl(h)) return r;
   int status = 0;
@@ -1005,10 +1076,38 @@ int64_t damf_gpu_event_latencies(damf_gpu* h, double* out, int64_t max) {
   return m;
 }
 
+int damf_gpu_load_rows(damf_gpu* h, int32_t which, int64_t row0, int64_t m, const float* src) {
+  if (!h) return DAMF_E_SHAPE_MISMATCH;
+  if (which != DAMF_XB && which != DAMF_YB)
+    return fail(h, DAMF_E_SHAPE_MISMATCH, "load_rows: which must be DAMF_XB or DAMF_YB");
+  if (row0 < 0 || m < 0 || row0 + m > h->n)
+    return fail(h, DAMF_E_UNKNOWN_NODE, "load_rows: rows out of range");
+  if (m == 0) return 0;
+  float* dst = (which == DAMF_XB ? h->Xb : h->Yb) + row0 * h->d;
+  // device sources may still be written by work on other streams (the
+  // caller's framework stream): order against all prior device work
+  if (is_device_ptr(src)) CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy2DAsync(dst, (size_t)h->d * 4, src, (size_t)h->k * 4, (size_t)h->k * 4, m,
+                       cudaMemcpyDefault, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (h->alpha1 && which == DAMF_XB) return 0;  // Z_b aliases X_b
+  return 0;
+}
+
 int damf_gpu_query_rows(damf_gpu* h, int32_t which, const int64_t* ids, int64_t m, float* out) {
   if (int r = sync_ctl(h)) return r;
   for (int64_t q = 0; q < m; ++q)
     if (ids[q] < 0 || ids[q] >= h->n) return fail(h, DAMF_E_UNKNOWN_NODE, "query: unknown node " + std::to_string(ids[q]));
+  if (which == DAMF_XB || which == DAMF_YB || which == DAMF_ZB || which == DAMF_RB) {
+    // raw base-coordinate rows (no projection)
+    const float* src = which == DAMF_XB ? h->Xb : which == DAMF_YB ? h->Yb
+                     : which == DAMF_ZB ? h->Zb : h->rb;
+    if (!src) return fail(h, DAMF_E_SHAPE_MISMATCH, "matrix not allocated (alpha == 1)");
+    for (int64_t q = 0; q < m; ++q)
+      CK(cudaMemcpyAsync(out + q * h->k, src + ids[q] * h->d, (size_t)h->k * 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return 0;
+  }
   const float* base = which == DAMF_Y ? h->Yb : which == DAMF_Z ? h->Zb : h->Xb;
   const double* PT = live_PT(h, which == DAMF_Y ? 1 : 0);
   int64_t* dids = nullptr;
@@ -1057,7 +1156,14 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
   const double* PT = live_PT(h, which == DAMF_Y ? 1 : 0);
   float* out = dst;
   if (!dst_is_device) CK(cudaMalloc(&out, (size_t)std::max<int64_t>(h->n, 1) * h->k * 4));
-  CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
+  // The fast paths (3xTF32 tensor cores / fp32 SIMT) lose ~log10(cond P)
+  // digits to cancellation; above kPreciseCond the fp64-accumulating fold
+  // keeps query_all at fp32 storage accuracy.
+  constexpr double kPreciseCond = 100.0;
+  if (h->h_ctl->cond_est > kPreciseCond)
+    CK(launch_materialize_precise(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
+  else
+    CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
   if (!dst_is_device) {
     CK(cudaMemcpyAsync(dst, out, (size_t)h->n * h->k * 4, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));

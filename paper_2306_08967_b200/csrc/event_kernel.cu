@@ -212,6 +212,100 @@ DAMF_D void rows_gemm(Smem<C>& S, double* Out, int ldo, int o0, const double* Co
   if (fro) *fro = total;
 }
 
+// ---------------------------------------------- exact inverse (one CTA)
+// Q = P^-1 (row-major, ld) for P given transposed (PT[j][i] = P[i][j]):
+// Gauss-Jordan with partial pivoting in place in Q, pivot row and column
+// factors staged in shared memory (prow, fcol, perm: >= k doubles each).
+// Used for the rare steps whose closed-form inverse would be ill-conditioned
+// (1 - |d|^2 below 1e-10); returns false if P is singular.
+DAMF_D bool gj_inverse_cta(const double* PT, double* Q, int k, int ld, double* prow, double* fcol,
+                           double* perm, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int x = tid; x < k * k; x += NT) {
+    const int i = x / k, j = x % k;
+    Q[(int64_t)i * ld + j] = PT[(int64_t)j * ld + i];
+  }
+  __syncthreads();
+  __shared__ int s_piv;
+  __shared__ int s_bad;
+  if (tid == 0) s_bad = 0;
+  for (int c = 0; c < k; ++c) {
+    // pivot: argmax_{r >= c} |W[r][c]|
+    double bv = -1.0;
+    int br = c;
+    for (int r = c + tid; r < k; r += NT) {
+      const double v = fabs(Q[(int64_t)r * ld + c]);
+      if (v > bv) {
+        bv = v;
+        br = r;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+      if (ov > bv || (ov == bv && orr < br)) {
+        bv = ov;
+        br = orr;
+      }
+    }
+    if (lane == 0) {
+      red[2 * warp] = bv;
+      red[2 * warp + 1] = (double)br;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b = -1.0;
+      int r0 = c;
+      for (int w = 0; w < NW; ++w)
+        if (red[2 * w] > b) {
+          b = red[2 * w];
+          r0 = (int)red[2 * w + 1];
+        }
+      s_piv = r0;
+      perm[c] = (double)r0;
+      if (!(b > 0.0)) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) return false;
+    const int p = s_piv;
+    // swap rows c <-> p, stage the pivot row
+    for (int j = tid; j < k; j += NT) {
+      const double a = Q[(int64_t)c * ld + j], b = Q[(int64_t)p * ld + j];
+      prow[j] = b;
+      if (p != c) Q[(int64_t)p * ld + j] = a;
+    }
+    __syncthreads();
+    const double ip = 1.0 / prow[c];
+    for (int j = tid; j < k; j += NT) {
+      const double v = j == c ? ip : prow[j] * ip;
+      Q[(int64_t)c * ld + j] = v;
+    }
+    for (int r = tid; r < k; r += NT) fcol[r] = r == c ? 0.0 : Q[(int64_t)r * ld + c];
+    __syncthreads();
+    for (int j = tid; j < k; j += NT) prow[j] = j == c ? ip : prow[j] * ip;
+    __syncthreads();
+    for (int x = tid; x < k * k; x += NT) {
+      const int r = x / k, j = x % k;
+      if (r == c) continue;
+      const double w = j == c ? 0.0 : Q[(int64_t)r * ld + j];
+      Q[(int64_t)r * ld + j] = w - fcol[r] * prow[j];
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, last first
+  for (int c = k - 1; c >= 0; --c) {
+    const int p = (int)perm[c];
+    if (p != c)
+      for (int i = tid; i < k; i += NT) {
+        const double a = Q[(int64_t)i * ld + c];
+        Q[(int64_t)i * ld + c] = Q[(int64_t)i * ld + p];
+        Q[(int64_t)i * ld + p] = a;
+      }
+    __syncthreads();
+  }
+  return true;
+}
+
 // ------------------------------------------------------------ secular solver
 // Root j of 1 + rho * sum_i kz2[i] / (kd[i] - lambda) = 0 (kd ascending,
 // rho > 0, sum kz2 <= 1), one warp. Returns tau and the origin pole o with
@@ -831,6 +925,12 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       *cl.map_shared_rank(S.dE + t, lane) = dEt;
     }
   }
+  // gE = 1 - |d_E|^2 equals E[k][k]^2 for the dropped column (E orthogonal);
+  // the direct form keeps its relative accuracy when |d_E| -> 1, where the
+  // subtraction cancels and the closed-form G^-1 (and with it the maintained
+  // P_Y^-1) would drift event by event.
+  if (edge && k2 == k && k >= olo && k < ohi && warp == 0 && lane < C)
+    *cl.map_shared_rank(S.dE + k, lane) = prow(1, k)[k];
   __syncthreads();
   // partial column sums over this CTA's kept columns (local smem):
   //  0: sum_t H[i][t] dH_t          (A_H d_H)
@@ -899,8 +999,15 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   }
   nH = block_sum(S, nH);
   nE = block_sum(S, nE);
-  const double gH = 1.0 - nH, gE = 1.0 - nE;
-  const bool lazy = k2 == k && gH > 1e-10 && (!edge || gE > 1e-10);
+  const double gH = 1.0 - nH;
+  const double gE = edge && k2 == k ? S.dE[k] * S.dE[k] : 1.0 - nE;
+  // Closed-form inverses need 1 - |d|^2 well away from 0; otherwise the step
+  // stays lazy but P^-1 is recomputed exactly (Gauss-Jordan) and a rebase is
+  // requested (the reference folds eagerly when its LU is unreliable,
+  // factor_state.cpp:168-177; a rebase is the grid-wide equivalent here).
+  // Eager folds remain for rank changes (k2 != k).
+  const bool lazy = k2 == k;
+  const bool exact = lazy && !(gH > 1e-10 && (!edge || gE > 1e-10));
   const int npp = 1 - S.pp[sA], nppB = 1 - S.pp[sB];
   double* PTA_n = A.PT[sA][npp];
   double* PTB_n = A.PT[sB][nppB];
@@ -908,6 +1015,8 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   double* QB_n = A.Q[sB][nppB];
   if (lazy) {
     const double igH = 1.0 / gH, igE = 1.0 / gE;
+    const int fbuf = edge ? 2 : 1, gbuf = edge ? 1 : 2;
+    if (!exact) {
     // ---- 5. row fixes from the OLD inverse: y = (ex F^-1) P_old^-1 ----------
     //   ex F^-1 [m] = (1/sqrt(sig_m)) (sum_t ex_t sqrt(s_t) H[m][t]
     //                                  + (A_H d_H)[m] / gH * sum_t ex_t sqrt(s_t) dH_t)
@@ -947,7 +1056,6 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     //   F^-1[t][m] = sqrt(s_t) (H[m][t] + dH_t (A_H d_H)[m]/gH) / sqrt(sig_m)
     //   edge: G^-1[t][m] = sqrt(s_t) (E[m][t] + dE_t (A_E d_E)[m]/gE) / sqrt(sig_m)
     //   node: G^-1[t][m] = (H[m][t] + dH_t (A_H d_H)[m]/gH) sqrt(sig_m) / sqrt(s_t)
-    const int fbuf = edge ? 2 : 1, gbuf = edge ? 1 : 2;
     for (int x = tid; x < (kohi - olo) * k; x += NT) {
       const int t = olo + x / k, m = x % k;
       const double rst = sqrt(S.s2[t]), rsm = sqrt(S.sig[m]);
@@ -961,14 +1069,52 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       prow(gbuf, t)[m] = gi;                 // edge: over E (read above); node: over H
     }
     __syncthreads();
+    }  // !exact
     PROF_MARK(8);
     // ---- the four GEMMs on the FP64 tensor cores (owned rows t) -------------
     const int nt = kohi - olo;
-    double fro[4];
+    double fro[4] = {0.0, 0.0, 0.0, 0.0};
     rows_gemm<C>(S, PTA_n, ld, olo, prow(0, olo), pld, nt, PTA, ld, k, k, &fro[0]);
-    rows_gemm<C>(S, QA_n, ld, olo, prow(fbuf, olo), pld, nt, QA, ld, k, k, &fro[1]);
     rows_gemm<C>(S, PTB_n, ld, olo, prow(3, olo), pld, nt, PTB, ld, k, k, &fro[2]);
-    rows_gemm<C>(S, QB_n, ld, olo, prow(gbuf, olo), pld, nt, QB, ld, k, k, &fro[3]);
+    if (!exact) {
+      rows_gemm<C>(S, QA_n, ld, olo, prow(fbuf, olo), pld, nt, QA, ld, k, k, &fro[1]);
+      rows_gemm<C>(S, QB_n, ld, olo, prow(gbuf, olo), pld, nt, QB, ld, k, k, &fro[3]);
+    } else {
+      // exact inverses of the new projections (rank 0: side A, rank 1: side B),
+      // then the row fixes y = x_cur P_new^-1 with x_cur = ex / ey / new row
+      cl.sync();  // new P^T rows visible
+      if (rank < 2) {
+        const bool ok = gj_inverse_cta(rank == 0 ? PTA_n : PTB_n, rank == 0 ? QA_n : QB_n, k, ld,
+                                       S.yA1, S.yB1, S.AHdH, S.AEdE);
+        if (!ok && tid == 0) {
+          A.ctl->err = 8;  // SingularProjection (factor_state.cpp:21-36)
+        }
+      }
+      cl.sync();  // exact inverses visible
+      int jlo, jhi;
+      block_range(k, C, rank, jlo, jhi);
+      for (int j = jlo + warp; j < jhi; j += NW) {
+        double ya = 0, yb = 0;
+        for (int t = lane; t < k; t += 32) {
+          ya += S.exv[t] * QA_n[(int64_t)t * ld + j];
+          yb += S.eyv[t] * QB_n[(int64_t)t * ld + j];
+        }
+        ya = warp_sum(ya);
+        yb = warp_sum(yb);
+        if (lane == 0) {
+          for (int q = 0; q < st.nb; ++q) {
+            float* r = baseA + A.sp_rows[st.b_off + q] * (int64_t)d + j;
+            *r = (float)((double)*r + A.sp_vals[st.b_off + q] * ya);
+          }
+          if (edge) {
+            float* r = baseB + st.c_row * (int64_t)d + j;
+            *r = (float)((double)*r + st.c_val * yb);
+          } else {
+            baseB[st.c_row * (int64_t)d + j] = (float)yb;  // appended row
+          }
+        }
+      }
+    }
     if (tid < 4) *cl.map_shared_rank(&S.pnorm[rank][tid], 0) = fro[tid];
     if (rank == 0)
       for (int t = tid; t < k; t += NT) A.sigma[t] = S.s2[t];
@@ -990,6 +1136,15 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       }
       A.ctl->cond_est = sqrt(p2) * sqrt(q2);
       if (A.ctl->cond_est > A.rebase_cond) A.ctl->need_rebase = 1;
+      // fp32 base rows: both projections must stay well conditioned (the
+      // reference watches P_X only, engine.cpp:38-40, with fp64 rows)
+      double p2o = 0, q2o = 0;
+      for (int r = 0; r < C; ++r) {
+        p2o += S.pnorm[r][xA ? 2 : 0];
+        q2o += S.pnorm[r][xA ? 3 : 1];
+      }
+      if (fmax(A.ctl->cond_est, sqrt(p2o) * sqrt(q2o)) > A.storage_cond) A.ctl->need_rebase = 1;
+      if (exact) A.ctl->need_rebase = 1;
     }
   } else {
     // ---- eager fold (rank change or ill-conditioned step) ------------------
@@ -1506,6 +1661,13 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
       ppr_event<C>(A, S, cl, ev);
     }
     if (A.t_end && rank == 0 && threadIdx.x == 0) A.t_end[e] = globaltimer();
+    // a rebase was requested: stop after this event; the host rebases over
+    // the whole GPU and resumes the batch (engine.cpp:38-40 per-event order)
+    cl.sync();
+    if (*(volatile int*)&A.ctl->need_rebase || *(volatile int*)&A.ctl->err) {
+      if (rank == 0 && threadIdx.x == 0) A.ctl->stop_event = e + 1;
+      break;
+    }
   }
 }
 

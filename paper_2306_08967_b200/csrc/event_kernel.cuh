@@ -42,6 +42,7 @@ struct EventKernelArgs {
   double* Q[2][2];   // [side][ping-pong]      P^-1
   double* sigma;
   double rebase_cond;
+  double storage_cond;  // rebase when either projection's |P|_F |P^-1|_F exceeds this
   // graph
   DevCSR out, in;
   int directed, undirected;

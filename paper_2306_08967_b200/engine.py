@@ -100,6 +100,8 @@ def lib():
         L.damf_gpu_event_latencies.argtypes = [vp, f64p, C.c_int64]
         L.damf_gpu_event_latencies.restype = C.c_int64
         L.damf_gpu_query_rows.argtypes = [vp, C.c_int32, i64p, C.c_int64, f32p]
+        L.damf_gpu_load_rows.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, vp]
+        L.damf_gpu_ppr_trace.argtypes = [vp, vp, C.c_int]
         L.damf_gpu_score.argtypes = [vp, C.c_int64, C.c_int64, C.c_int32, f64p]
         L.damf_gpu_materialize.argtypes = [vp, C.c_int32, vp, C.c_int32]
         L.damf_gpu_get_state.argtypes = [vp, C.c_int32, vp]
@@ -147,23 +149,39 @@ class Engine:
                  eps=1e-5, undirected=False, rebase_cond=1e8, rebase_every=50000, seed=0,
                  node_capacity=0, arc_capacity=0):
         L = lib()
-        self._offsets = np.ascontiguousarray(offsets, np.int64)
-        self._targets = np.ascontiguousarray(targets, np.int32)
-        self._weights = None if weights is None else np.ascontiguousarray(weights, np.float64)
-        csr = Csr(n, len(self._targets), _p(self._offsets, i64p), _p(self._targets, i32p),
-                  _p(self._weights, f64p))
+        # arrays may be numpy (host) or torch tensors (host or CUDA; device
+        # arrays are consumed in place by the library); xb / yb may be None
+        keep = []
+
+        def arg(a, np_dtype, ctype, torch_dtype):
+            if a is None:
+                return ctype()
+            if hasattr(a, "data_ptr"):
+                import torch
+                assert a.is_contiguous() and a.dtype == getattr(torch, torch_dtype), \
+                    f"expected contiguous {torch_dtype} tensor"
+                keep.append(a)
+                return C.cast(C.c_void_p(a.data_ptr()), ctype)
+            arr = np.ascontiguousarray(a, np_dtype)
+            keep.append(arr)
+            return _p(arr, ctype)
+
+        arcs = int(targets.numel() if hasattr(targets, "numel") else len(targets))
+        csr = Csr(n, arcs, arg(offsets, np.int64, i64p, "int64"),
+                  arg(targets, np.int32, i32p, "int32"),
+                  arg(weights, np.float64, f64p, "float64"))
         cfg = Config(d, alpha, eps, seed, rebase_cond, rebase_every, int(undirected), 0,
                      node_capacity, arc_capacity)
-        xb = np.ascontiguousarray(xb, np.float32)
-        yb = np.ascontiguousarray(yb, np.float32)
+        xb_p = arg(xb, np.float32, f32p, "float32")
+        yb_p = arg(yb, np.float32, f32p, "float32")
         px = np.ascontiguousarray(px, np.float64)
         py = np.ascontiguousarray(py, np.float64)
         sigma = np.ascontiguousarray(sigma, np.float64)
         self.h = C.c_void_p()
-        st = L.damf_gpu_create_from_factors(C.byref(csr), C.byref(cfg), k, _p(xb, f32p),
-                                            _p(yb, f32p), _p(px, f64p), _p(py, f64p),
-                                            _p(sigma, f64p), C.byref(self.h))
-        del self._offsets, self._targets, self._weights
+        st = L.damf_gpu_create_from_factors(C.byref(csr), C.byref(cfg), k, xb_p, yb_p,
+                                            _p(px, f64p), _p(py, f64p), _p(sigma, f64p),
+                                            C.byref(self.h))
+        del keep
         if st:
             raise DamfError(st, "create_from_factors failed")
         self.d = d
@@ -223,6 +241,18 @@ class Engine:
         self._check(lib().damf_gpu_get_state(self.h, which, out.ctypes.data_as(C.c_void_p)))
         return out
 
+    def load_rows(self, which, row0, rows):
+        """Copy rows (m x k fp32; numpy or torch, host or CUDA) into X_b / Y_b
+        at row0 (damf_gpu_load_rows)."""
+        if hasattr(rows, "data_ptr"):
+            assert rows.is_contiguous()
+            m, ptr, keep = rows.shape[0], rows.data_ptr(), rows
+        else:
+            keep = np.ascontiguousarray(rows, np.float32)
+            m, ptr = keep.shape[0], keep.ctypes.data
+        self._check(lib().damf_gpu_load_rows(self.h, which, row0, m, C.c_void_p(ptr)))
+        del keep
+
     def query(self, which, ids):
         ids = np.ascontiguousarray(ids, np.int64)
         out = np.zeros((len(ids), self.k), np.float32)
@@ -243,8 +273,13 @@ class Engine:
         self._check(lib().damf_gpu_score(self.h, u, v, int(enhanced), C.byref(out)))
         return out.value
 
-    def materialize(self, which=X):
-        return self.get(which)
+    def materialize(self, which=X, dst_ptr=None, on_device=False):
+        """FactorState::query_all (factor_state.cpp:120-123). Without dst_ptr
+        returns a host array; with dst_ptr (int, n x k fp32) writes there
+        (device memory when on_device)."""
+        if dst_ptr is None:
+            return self.get(which)
+        self._check(lib().damf_gpu_materialize(self.h, which, C.c_void_p(dst_ptr), int(on_device)))
 
     def graph_sets(self):
         n = self.n

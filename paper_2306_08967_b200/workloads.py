@@ -201,32 +201,41 @@ def cfg2(seed=1, blocks=20, bsize=5000, n_ins=10_000, n_del=2_000, n_nodes=500, 
 
 
 # ---------------------------------------------------------------- R-MAT
+def rmat_keys_device(scale, ef, seed, a=0.57, b=0.19, c=0.19, device="cuda"):
+    """R-MAT edges on the GPU as sorted unique int64 keys (lo << 32) | hi,
+    lo < hi (symmetrised, self loops and duplicates removed)."""
+    import torch
+    m = ef << scale
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = torch.zeros(m, dtype=torch.int64, device=device)
+    v = torch.zeros(m, dtype=torch.int64, device=device)
+    ab, abc = a + b, a + b + c
+    for _ in range(scale):
+        r = torch.rand(m, generator=g, device=device)
+        u <<= 1
+        u |= (r >= ab).to(torch.int64)
+        v <<= 1
+        v |= (((r >= a) & (r < ab)) | (r >= abc)).to(torch.int64)
+        del r
+    lo = torch.minimum(u, v)
+    hi = torch.maximum(u, v)
+    del u, v
+    keep = lo != hi
+    key = lo[keep]
+    key <<= 32
+    key |= hi[keep]
+    del lo, hi, keep
+    return torch.unique(key)  # sorted
+
+
 def rmat_edges(scale, ef, seed, a=0.57, b=0.19, c=0.19, device=None):
     """R-MAT (recursive quadrant sampling, no noise), symmetrised, self loops
     and duplicates removed. Returns (u, v) with u < v, sorted. Runs on the GPU
     with torch when `device` is given, else numpy."""
     m = ef << scale
     if device is not None:
-        import torch
-        g = torch.Generator(device=device)
-        g.manual_seed(seed)
-        u = torch.zeros(m, dtype=torch.int64, device=device)
-        v = torch.zeros(m, dtype=torch.int64, device=device)
-        ab, abc = a + b, a + b + c
-        for _ in range(scale):
-            r = torch.rand(m, generator=g, device=device)
-            bu = (r >= ab).to(torch.int64)
-            bv = ((r >= a) & (r < ab)) | (r >= abc)
-            u = (u << 1) | bu
-            v = (v << 1) | bv.to(torch.int64)
-            del r, bu, bv
-        lo = torch.minimum(u, v)
-        hi = torch.maximum(u, v)
-        del u, v
-        keep = lo != hi
-        key = (lo[keep] << 32) | hi[keep]
-        del lo, hi, keep
-        key = torch.unique(key)  # sorted
+        key = rmat_keys_device(scale, ef, seed, a, b, c, device)
         return (key >> 32), (key & 0xFFFFFFFF)
     rng = np.random.Generator(np.random.PCG64(seed))
     u = np.zeros(m, np.int64)
@@ -301,3 +310,106 @@ def tsvd_factors(n, offsets, targets, d, seed=0, oversample=10, power=4):
     V = Q2 @ Vct.T[:, :k]
     s = s[:k]
     return U * np.sqrt(s), V * np.sqrt(s), s
+
+
+# ------------------------------------------------ device builders (cfg 3-5)
+def csr_from_keys_device(n, keys, drop=None):
+    """Symmetric CSR (offsets int64, targets int32; rows sorted) as CUDA
+    tensors from unique edge keys (lo << 32) | hi; `drop` = boolean mask of
+    keys to leave out (held-out stream edges)."""
+    import torch
+    k = keys if drop is None else keys[~drop]
+    lo = k >> 32
+    hi = k & 0xFFFFFFFF
+    both = torch.cat([k, (hi << 32) | lo])
+    del k, lo, hi
+    both = torch.sort(both).values
+    src = both >> 32
+    cnt = torch.bincount(src, minlength=n)
+    del src
+    off = torch.zeros(n + 1, dtype=torch.int64, device=both.device)
+    torch.cumsum(cnt, 0, out=off[1:])
+    del cnt
+    tgt = (both & 0xFFFFFFFF).to(torch.int32)
+    del both
+    return off, tgt
+
+
+def orthonormal_rows_into(eng, which, n, d, sigma, seed, chunk=1 << 22):
+    """X_b (or Y_b) = U diag(sqrt sigma) with U random orthonormal columns
+    (Cholesky-QR of a seeded Gaussian, generated chunk by chunk on the GPU and
+    loaded in place with Engine.load_rows), SURVEY 8(d) cfg 5."""
+    import torch
+    gen = torch.Generator(device="cuda")
+    gram = torch.zeros(d, d, dtype=torch.float64, device="cuda")
+    for c0 in range(0, n, chunk):
+        gen.manual_seed(seed * 1000003 + c0 // chunk)
+        blk = torch.randn(min(chunk, n - c0), d, generator=gen, device="cuda").double()
+        gram += blk.T @ blk
+        del blk
+    R = torch.linalg.cholesky(gram, upper=True)
+    T = torch.linalg.inv(R) * torch.as_tensor(np.sqrt(sigma), device="cuda")[None, :]
+    for c0 in range(0, n, chunk):
+        gen.manual_seed(seed * 1000003 + c0 // chunk)
+        blk = torch.randn(min(chunk, n - c0), d, generator=gen, device="cuda").double()
+        eng.load_rows(which, c0, (blk @ T).float().contiguous())
+        del blk
+    torch.cuda.synchronize()
+
+
+def degree_proportional_inserts(keys, tgt, m, seed):
+    """m new undirected edges whose endpoints are uniformly random arc
+    endpoints (degree-proportional), no loops, no existing or repeated edge."""
+    import torch
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    arcs = tgt.numel()
+    out_u, out_v, seen = [], [], set()
+    while len(out_u) < m:
+        i = torch.randint(arcs, (4 * m,), generator=g, device="cuda")
+        j = torch.randint(arcs, (4 * m,), generator=g, device="cuda")
+        u = tgt[i].long()
+        v = tgt[j].long()
+        lo, hi = torch.minimum(u, v), torch.maximum(u, v)
+        key = (lo << 32) | hi
+        pos = torch.searchsorted(keys, key).clamp(max=keys.numel() - 1)
+        ok = (lo != hi) & (keys[pos] != key)
+        for a, b in zip(u[ok].tolist(), v[ok].tolist()):
+            kk = (min(a, b), max(a, b))
+            if kk in seen:
+                continue
+            seen.add(kk)
+            out_u.append(a)
+            out_v.append(b)
+            if len(out_u) == m:
+                break
+    return np.array(out_u, np.int64), np.array(out_v, np.int64)
+
+
+def tsvd_factors_device(n, off, tgt, d, seed=0, oversample=10, power=4):
+    """Randomized truncated SVD of the symmetric adjacency on the GPU
+    (torch / cuSPARSE; the reference's init rule, svd.cpp:47-96) used to set
+    up the cfg-3 state for the bench: X_b = U sqrt(S), Y_b = V sqrt(S)."""
+    import torch
+    A = torch.sparse_csr_tensor(off, tgt.long(), torch.ones(tgt.numel(), device="cuda"),
+                                size=(n, n))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    l = min(n, d + oversample)
+
+    def orth(y):
+        q, _ = torch.linalg.qr(y)
+        return q
+
+    Q = orth(A @ torch.randn(n, l, generator=gen, device="cuda"))
+    for _ in range(power):
+        Q = orth(A @ Q)  # A symmetric: A^T Q == A Q
+        Q = orth(A @ Q)
+    Bt = A @ Q
+    Q2, R2 = torch.linalg.qr(Bt)
+    Uc, s, Vct = torch.linalg.svd(R2.T.double())
+    k = min(d, int((s > 1e-12 * s[0]).sum()))
+    sq = torch.sqrt(s[:k])
+    X = (Q.double() @ Uc[:, :k] * sq).float()
+    Y = (Q2.double() @ Vct.T[:, :k] * sq).float()
+    return X.contiguous(), Y.contiguous(), s[:k].cpu().numpy()

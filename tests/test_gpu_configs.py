@@ -1,0 +1,214 @@
+"""Parity on the BASELINE configurations.
+
+cfg 1 and a scaled cfg 3 run the full fp64 oracle beside the device on the
+same seeded inputs; cfg 5 (and a small replica of its construction) is
+checked with the row-local oracle: before each insertion the touched base
+rows, P_X, P_Y and sigma are read back, the two rank-1 updates are replayed
+in fp64 (oracle.edge_update_rowlocal_p, update_engine.cpp:144-204 +
+factor_state.cpp:158-213), and the device state after the event is compared
+in current coordinates (sign-invariant products)."""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import gpu_from_oracle, product, rel_frob, sampled_product_rel, sigma_rel
+from paper_2306_08967_b200 import engine as ge
+from paper_2306_08967_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def z_star(n, off, ids, deg, x, alpha, iters=400):
+    """Tight fixed point of Z = alpha X + (1-alpha) D^-1 A Z (Jacobi, fp64)."""
+    import scipy.sparse as sp
+    src = np.repeat(np.arange(n), np.diff(off))
+    A = sp.csr_matrix((np.ones(len(ids)), (src, ids.astype(np.int64))), shape=(n, n))
+    dinv = 1.0 / np.maximum(deg, 1.0)
+    z = alpha * x
+    for _ in range(iters):
+        z = alpha * x + (1 - alpha) * (dinv[:, None] * (A @ z))
+    return z
+
+
+def defect_rows(n, off, ids, deg, x, z, alpha):
+    import scipy.sparse as sp
+    src = np.repeat(np.arange(n), np.diff(off))
+    A = sp.csr_matrix((np.ones(len(ids)), (src, ids.astype(np.int64))), shape=(n, n))
+    dfc = alpha * x - z + (1 - alpha) * (1.0 / np.maximum(deg, 1.0))[:, None] * (A @ z)
+    return np.abs(dfc).max(1) / np.maximum(deg, 1.0)
+
+
+def test_cfg1_stream_prefix_matches_oracle():
+    # cfg 1: BA n = 10,000, m = 5, half the edges factorised (reference t-SVD,
+    # d = 32), the rest streamed; PPR alpha 0.15, eps 1e-4. First 1,500 events.
+    w = W.cfg1()
+    eu, ev = w["init"]
+    g = oracle.Graph(w["n"], np.concatenate([eu, ev]), np.concatenate([ev, eu]), None, True)
+    oe = oracle.OracleEngine(g, d=32, alpha=w["alpha"], eps=w["eps"], seed=0)
+    e = gpu_from_oracle(g, oe, d=32, alpha=w["alpha"], eps=w["eps"])
+    worst_p = worst_s = 0.0
+    for a in range(0, 1500, 250):
+        part = w["stream"].slice(a, a + 250)
+        oe.apply(part)
+        e.apply(part)
+        worst_p = max(worst_p, sampled_product_rel(e.get(ge.X), e.get(ge.Y),
+                                                   oe.get(oe.X), oe.get(oe.Y), seed=a))
+        worst_s = max(worst_s, sigma_rel(e.get(ge.SIGMA), oe.get(oe.SIGMA)))
+    print("cfg1 worst sampled product", worst_p, "worst sigma", worst_s)
+    assert worst_p <= 1e-4 and worst_s <= 1e-6
+    # bookkeeping bit-exact
+    off_o, ids_o, deg_o = oe.graph_sets()
+    off_g, ids_g, deg_g = e.graph_sets()
+    assert np.array_equal(off_o, off_g) and np.array_equal(deg_o, deg_g)
+    assert np.array_equal(ids_o, ids_g.astype(np.int64))
+    # PPR: the defect bound (the reference's contract) and the distance to the
+    # tight fixed point within 1.5x the oracle's (SURVEY 8(d) PPR gates)
+    n = e.n
+    x = e.get(ge.X).astype(np.float64)
+    zg = e.get(ge.Z).astype(np.float64)
+    d_rows = defect_rows(n, off_g, ids_g, deg_g, x, zg, w["alpha"])
+    assert d_rows.max() <= w["eps"] * (1 + 1e-3)
+    zs = z_star(n, off_g, ids_g, deg_g, x, w["alpha"])
+    err_g = np.linalg.norm(zg - zs)
+    err_o = np.linalg.norm(oe.get(oe.Z) - z_star(n, off_o, ids_o, deg_o, oe.get(oe.X), w["alpha"]))
+    print("cfg1 |Z-Z*| gpu", err_g, "oracle", err_o)
+    assert err_g <= 1.5 * err_o + 1e-6 * np.linalg.norm(zs)
+
+
+@pytest.mark.parametrize("batch", [1, 64, 1024])
+def test_cfg3_shape_batches_match_oracle(batch):
+    # cfg 3 scaled to R-MAT scale 13 (same a/b/c/d, ef 16), d = 64, alpha = 1:
+    # held-out edges inserted in batches of 1 / 64 / 1024, sequential inside.
+    scale, d = 13, 64
+    n = 1 << scale
+    u, v = W.rmat_edges(scale, 16, 2)
+    rng = np.random.default_rng(2)
+    held = rng.permutation(len(u))[:2048]
+    keep = np.ones(len(u), bool)
+    keep[held] = False
+    g = oracle.Graph(n, np.concatenate([u[keep], v[keep]]), np.concatenate([v[keep], u[keep]]),
+                     None, True)
+    oe = oracle.OracleEngine(g, d=d, alpha=1.0, seed=2)
+    e = gpu_from_oracle(g, oe, d=d, alpha=1.0, eps=1e-5)
+    stream = W.EventList.edges(ge.ADD_EDGE, u[held], v[held])
+    m = 2048 if batch > 1 else 256
+    for a in range(0, m, batch):
+        part = stream.slice(a, min(m, a + batch))
+        oe.apply(part)
+        e.apply(part)
+    wp = rel_frob(product(e.get(ge.X), e.get(ge.Y)), product(oe.get(oe.X), oe.get(oe.Y)))
+    ws = sigma_rel(e.get(ge.SIGMA), oe.get(oe.SIGMA))
+    print(f"cfg3-shape batch {batch}: product {wp:.3e} sigma {ws:.3e}")
+    assert wp <= 1e-4 and ws <= 1e-6
+    off_o, ids_o, deg_o = oe.graph_sets()
+    off_g, ids_g, deg_g = e.graph_sets()
+    assert np.array_equal(off_o, off_g) and np.array_equal(ids_o, ids_g.astype(np.int64))
+
+
+def rowlocal_insert_check(e, u, v, sample, d):
+    """Replay one undirected insertion (two rank-1 updates) in the fp64
+    row-local oracle from the device's pre-state, apply it on the device and
+    return (product rel. error over rows {u,v} + sample, sigma rel. error)."""
+    k = e.k
+    px, py, sig = e.get(ge.PX), e.get(ge.PY), e.get(ge.SIGMA)
+    rows = np.concatenate([[u, v], sample]).astype(np.int64)
+    xb = e.query(ge.XB, rows).astype(np.float64)
+    yb = e.query(ge.YB, rows).astype(np.float64)
+    # step 1: b = e_u, c = e_v ; step 2: b = e_v, c = e_u (graph.cpp:95-108)
+    r1 = oracle.edge_update_rowlocal_p(k, d, xb[0], yb[1], px, py, sig, 1.0)
+    # base rows after step 1 in the coordinates of r1["px"]: untouched rows
+    # keep their current coordinates X_cur = X_b P_old F
+    P1x, P1y = px @ r1["F"], py @ r1["G"]
+    xv_cur = xb[1] @ P1x          # X[v] current (unchanged by step 1)
+    yu_cur = yb[0] @ P1y          # Y[u] current
+    xv1 = xv_cur @ np.linalg.inv(r1["px"])
+    yu1 = yu_cur @ np.linalg.inv(r1["py"])
+    r2 = oracle.edge_update_rowlocal_p(len(r1["sigma2"]), d, xv1, yu1, r1["px"], r1["py"],
+                                       r1["sigma2"], 1.0)
+    # oracle current rows after both steps
+    Xo = (xb @ px) @ r1["F"] @ r2["F"]
+    Yo = (yb @ py) @ r1["G"] @ r2["G"]
+    Xo[0] = r1["xu"] @ r1["px"] @ r2["F"]          # X[u] after step 1, carried by step 2
+    Xo[1] = r2["xu"] @ r2["px"]                    # X[v] after step 2
+    Yo[1] = r1["yv"] @ r1["py"] @ r2["G"]          # Y[v] after step 1
+    Yo[0] = r2["yv"] @ r2["py"]                    # Y[u] after step 2
+    e.apply(W.EventList.edges(ge.ADD_EDGE, [u], [v]))
+    Xg = e.query(ge.X, rows).astype(np.float64)
+    Yg = e.query(ge.Y, rows).astype(np.float64)
+    return rel_frob(Xg @ Yg.T, Xo @ Yo.T), sigma_rel(e.get(ge.SIGMA), r2["sigma2"])
+
+
+def cfg5_like(scale, d, n_events, seed):
+    import torch
+    n = 1 << scale
+    keys = W.rmat_keys_device(scale, 16, seed)
+    off, tgt = W.csr_from_keys_device(n, keys)
+    su, sv = W.degree_proportional_inserts(keys, tgt, n_events, seed=seed)
+    del keys
+    torch.cuda.empty_cache()  # the engine allocates with cudaMalloc
+    sig = np.arange(1, d + 1, dtype=np.float64) ** -0.5
+    e = ge.Engine(n, off, tgt, None, d, d, None, None, np.eye(d), np.eye(d), sig, alpha=1.0,
+                  undirected=True, node_capacity=1024, arc_capacity=1 << 22)
+    del off, tgt
+    torch.cuda.empty_cache()
+    W.orthonormal_rows_into(e, ge.XB, n, d, sig, seed=10 * seed)
+    W.orthonormal_rows_into(e, ge.YB, n, d, sig, seed=10 * seed + 1)
+    return e, su, sv
+
+
+def run_rowlocal(e, su, sv, d, n_check, seed):
+    rng = np.random.default_rng(seed)
+    worst_p = worst_s = 0.0
+    for i in range(n_check):
+        sample = rng.integers(0, e.n, 62)
+        sample = sample[(sample != su[i]) & (sample != sv[i])]
+        wp, ws = rowlocal_insert_check(e, int(su[i]), int(sv[i]), sample, d)
+        dg = e.diag()
+        print(f"  event {i}: ({su[i]}, {sv[i]}) product {wp:.2e} sigma {ws:.2e} "
+              f"cond {dg['cond_estimate']:.3e} rebases {dg['events_since_rebase']}")
+        worst_p, worst_s = max(worst_p, wp), max(worst_s, ws)
+    return worst_p, worst_s
+
+
+def test_rowlocal_small_replica_of_cfg5():
+    e, su, sv = cfg5_like(16, 128, 24, seed=7)
+    wp, ws = run_rowlocal(e, su, sv, 128, 24, 7)
+    print("cfg5-replica row-local: product", wp, "sigma", ws)
+    e.close()
+    assert wp <= 1e-4 and ws <= 1e-6
+
+
+def test_cfg5_rowlocal_at_scale():
+    import gc
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+    free, total = torch.cuda.mem_get_info()
+    if total < 150e9:
+        pytest.skip("config 5 needs ~120 GB of device memory")
+    e, su, sv = cfg5_like(26, 128, 8, seed=4)
+    wp, ws = run_rowlocal(e, su, sv, 128, 8, 4)
+    print("cfg5 row-local: product", wp, "sigma", ws)
+    e.close()
+    assert wp <= 1e-4 and ws <= 1e-6
+
+
+@pytest.mark.parametrize("k", [64, 128, 256])
+def test_rebase_fold_is_fp64_accurate(k):
+    # rebase X_b <- X_b P_X with cond(P) = 1e6 (factor_state.cpp:215-222): the
+    # fold must keep fp32 storage accuracy (fp64 products on the tensor cores)
+    rng = np.random.default_rng(k)
+    n = 20_000
+    xb = rng.standard_normal((n, k)).astype(np.float32)
+    U, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    V, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    P = U @ np.diag(np.logspace(0, -6, k)) @ V.T
+    off = np.zeros(n + 1, np.int64)
+    e = ge.Engine(n, off, np.zeros(0, np.int32), None, k, k, xb, xb, P, P,
+                  np.linspace(2, 1, k), alpha=1.0, eps=1e-5)
+    truth = xb.astype(np.float64) @ P
+    e.rebase()
+    got = e.get(ge.XB).astype(np.float64)
+    err = np.abs(got - truth).max(1) / np.maximum(np.abs(truth).max(1), 1e-30)
+    print(f"k={k}: worst row rel err {err.max():.2e}")
+    assert err.max() <= 5e-6
