@@ -29,6 +29,7 @@ struct DevCtl {
   double smax;        // proj_row_bound(P_X) at the end of the last step
   unsigned long long t_begin, t_end;  // %globaltimer stamps of the last event
   long long stop_event;               // first event not processed by a stopped batch
+  long long dirty_n[2];               // rows of X_b / Y_b written through P^-1 since the last fold
   unsigned long long prof[32];        // per-phase SM cycles (rank 0), dev profiling
 };
 

@@ -20,6 +20,7 @@
 using namespace dgpu;
 
 namespace {
+constexpr long long kDirtyCap = 1 << 16;  // dirty rows tracked per side between folds
 
 #define CK(expr)                                                                       \
   do {                                                                                 \
@@ -206,6 +207,8 @@ struct damf_gpu {
   float* hacc = nullptr;
   int *items0 = nullptr, *items1 = nullptr, *hdone = nullptr, *mitems = nullptr;
   long long* ptrace = nullptr;
+  int64_t* dirty[2] = {nullptr, nullptr};  // rows written through P^-1 (see rebase)
+  float* dirty_tmp = nullptr;              // gathered dirty rows (kDirtyCap x d)
   unsigned long long* wq = nullptr;
   double* PT[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   double* Q[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -302,6 +305,9 @@ EventKernelArgs event_args(damf_gpu* h) {
   constexpr double kStorageSafeCond = 1e4;
   a.rebase_cond = h->cfg.rebase_cond;
   a.storage_cond = kStorageSafeCond;
+  a.dirty[0] = h->dirty[0];
+  a.dirty[1] = h->dirty[1];
+  a.dirty_cap = kDirtyCap;
   a.out = h->out;
   a.in = h->in;
   a.directed = h->directed;
@@ -311,6 +317,20 @@ EventKernelArgs event_args(damf_gpu* h) {
   a.ws_Q1T = h->ws;
   a.ws_priv = h->ws + m;
   return a;
+}
+
+// rows[i] of `base` (k of ld floats) <-> packed tmp rows
+__global__ void gather_rows_kernel(const float* base, int ld, int k, const int64_t* rows,
+                                   int64_t m, float* tmp) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m * k;
+       x += (int64_t)gridDim.x * blockDim.x)
+    tmp[x] = base[rows[x / k] * ld + x % k];
+}
+__global__ void scatter_rows_kernel(float* base, int ld, int k, const int64_t* rows, int64_t m,
+                                    const float* tmp) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m * k;
+       x += (int64_t)gridDim.x * blockDim.x)
+    base[rows[x / k] * ld + x % k] = tmp[x];
 }
 
 bool is_device_ptr(const void* p) {
@@ -466,6 +486,8 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   const int64_t n = g->n, ncap = h->n_cap, d = h->d, ld = h->ld;
   // ---- factor state
   CK(dalloc(h, &h->ctl, 1));
+  for (int sd = 0; sd < 2; ++sd) CK(dalloc(h, &h->dirty[sd], (size_t)kDirtyCap));
+  CK(dalloc(h, &h->dirty_tmp, (size_t)kDirtyCap * cfg->d));
   CK(dalloc(h, &h->Xb, (size_t)ncap * d));
   CK(dalloc(h, &h->Yb, (size_t)ncap * d));
   CK(cudaMemsetAsync(h->Xb, 0, (size_t)ncap * d * 4, h->st));
@@ -741,8 +763,23 @@ int damf_gpu_rebase(damf_gpu* h) {
   // rebase_cond = 1e8), where fp32 / 3xTF32 products lose the digits
   float* tmp = nullptr;
   if (k > 128) CK(cudaMalloc(&tmp, (size_t)h->n * d * 4));
-  auto fold = [&](float* base, const double* PT) -> int {
-    if (!tmp) {
+  // Two tiers: rows whose base value was written through P^-1 since the last
+  // fold (the dirty lists the event kernel keeps) carry components ~cond(P)
+  // larger than their current value and are folded in fp64 (DMMA); every
+  // other row is benign and takes the fast HBM-bound path. Without usable
+  // dirty lists (overflow, PPR state, k > 128) everything is folded in fp64.
+  auto fold = [&](float* base, const double* PT, int side) -> int {
+    const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
+    if (nd >= 0 && nd <= kDirtyCap && k <= 128) {
+      const int g = (int)std::min<long long>(std::max<long long>(nd * k / 256, 1), 4096);
+      if (nd > 0) gather_rows_kernel<<<g, 256, 0, h->st>>>(base, d, k, h->dirty[side], nd, h->dirty_tmp);
+      CK(launch_materialize(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
+      if (nd > 0) {
+        CK(launch_materialize_precise(h->dirty_tmp, nd, k, k, PT, ld, k, h->dirty_tmp, k, h->st, h->nsm));
+        scatter_rows_kernel<<<g, 256, 0, h->st>>>(base, d, k, h->dirty[side], nd, h->dirty_tmp);
+      }
+      CK(cudaGetLastError());
+    } else if (!tmp) {
       CK(launch_materialize_precise(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
     } else {
       CK(launch_materialize_precise(base, h->n, k, d, PT, ld, k, tmp, d, h->st, h->nsm));
@@ -750,12 +787,14 @@ int damf_gpu_rebase(damf_gpu* h) {
     }
     return 0;
   };
-  if (int r = fold(h->Xb, live_PT(h, 0))) return r;
-  if (int r = fold(h->Yb, live_PT(h, 1))) return r;
+  if (int r = fold(h->Xb, live_PT(h, 0), 0)) return r;
+  if (int r = fold(h->Yb, live_PT(h, 1), 1)) return r;
   if (!h->alpha1) {
-    if (int r = fold(h->Zb, live_PT(h, 0))) return r;
-    if (int r = fold(h->rb, live_PT(h, 0))) return r;
+    if (int r = fold(h->Zb, live_PT(h, 0), -1)) return r;
+    if (int r = fold(h->rb, live_PT(h, 0), -1)) return r;
   }
+  h->h_ctl->dirty_n[0] = h->h_ctl->dirty_n[1] = 0;
+  CK(cudaMemcpyAsync(h->ctl->dirty_n, h->h_ctl->dirty_n, sizeof(h->h_ctl->dirty_n), cudaMemcpyHostToDevice, h->st));
   for (int s = 0; s < 2; ++s) {
     identity_kernel<<<64, 256, 0, h->st>>>(live_PT(h, s), k, ld);
     identity_kernel<<<64, 256, 0, h->st>>>(live_Q(h, s), k, ld);
@@ -1159,11 +1198,27 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
   // The fast paths (3xTF32 tensor cores / fp32 SIMT) lose ~log10(cond P)
   // digits to cancellation; above kPreciseCond the fp64-accumulating fold
   // keeps query_all at fp32 storage accuracy.
+  // (benign rows) and, above kPreciseCond, the dirty rows (written through
+  // P^-1 since the last fold) are recomputed in fp64 and patched in; without
+  // a usable dirty list (PPR state, overflow) the whole fold is fp64.
   constexpr double kPreciseCond = 100.0;
-  if (h->h_ctl->cond_est > kPreciseCond)
-    CK(launch_materialize_precise(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
-  else
+  const int side = which == DAMF_Y ? 1 : (which == DAMF_Z && !h->alpha1) ? -1 : 0;
+  const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
+  if (h->h_ctl->cond_est <= kPreciseCond) {
     CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
+  } else if (nd >= 0 && nd <= kDirtyCap) {
+    const int k = h->k;
+    CK(launch_materialize(base, h->n, k, h->d, PT, h->ld, k, out, k, h->st, h->nsm));
+    if (nd > 0) {
+      const int g = (int)std::min<long long>(std::max<long long>(nd * k / 256, 1), 4096);
+      gather_rows_kernel<<<g, 256, 0, h->st>>>(base, h->d, k, h->dirty[side], nd, h->dirty_tmp);
+      CK(launch_materialize_precise(h->dirty_tmp, nd, k, k, PT, h->ld, k, h->dirty_tmp, k, h->st, h->nsm));
+      scatter_rows_kernel<<<g, 256, 0, h->st>>>(out, k, k, h->dirty[side], nd, h->dirty_tmp);
+      CK(cudaGetLastError());
+    }
+  } else {
+    CK(launch_materialize_precise(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
+  }
   if (!dst_is_device) {
     CK(cudaMemcpyAsync(dst, out, (size_t)h->n * h->k * 4, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));

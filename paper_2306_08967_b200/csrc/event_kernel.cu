@@ -1145,6 +1145,14 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       }
       if (fmax(A.ctl->cond_est, sqrt(p2o) * sqrt(q2o)) > A.storage_cond) A.ctl->need_rebase = 1;
       if (exact) A.ctl->need_rebase = 1;
+      // rows whose base value was written through P^-1: the next fold
+      // recomputes them in fp64 (their base components carry cond(P))
+      auto mark = [&](int side, int64_t row) {
+        const long long at = A.ctl->dirty_n[side]++;
+        if (at < A.dirty_cap) A.dirty[side][at] = row;
+      };
+      for (int q = 0; q < st.nb; ++q) mark(sA, A.sp_rows[st.b_off + q]);
+      mark(sB, st.c_row);
     }
   } else {
     // ---- eager fold (rank change or ill-conditioned step) ------------------
@@ -1231,6 +1239,7 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       A.ctl->rank1 += 1;
       A.ctl->folds += 1;
       A.ctl->cond_est = 1.0;
+      A.ctl->dirty_n[0] = A.ctl->dirty_n[1] = 0;  // folded in fp64, P = I
     }
   }
   // appended rows (node steps)

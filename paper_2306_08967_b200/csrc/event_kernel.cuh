@@ -42,7 +42,9 @@ struct EventKernelArgs {
   double* Q[2][2];   // [side][ping-pong]      P^-1
   double* sigma;
   double rebase_cond;
-  double storage_cond;  // rebase when either projection's |P|_F |P^-1|_F exceeds this
+  double storage_cond;
+  int64_t* dirty[2];    // row ids of X_b / Y_b written through P^-1 (capacity dirty_cap)
+  long long dirty_cap;  // rebase when either projection's |P|_F |P^-1|_F exceeds this
   // graph
   DevCSR out, in;
   int directed, undirected;
