@@ -315,7 +315,7 @@ cudaError_t launch_materialize(const float* X, int64_t n, int k, int ldx, const 
   if (n <= 0 || k2 <= 0) return cudaSuccess;
   if (k2 == k && materialize_tc_supported(k, ldx, ldz, X, Z)) {
     if (!g_fsplit) {
-      cudaError_t e = cudaMalloc(&g_fsplit, 2 * 128 * 128 * sizeof(float));
+      cudaError_t e = cudaMalloc(&g_fsplit, 2 * kMaxD * kMaxD * sizeof(float));
       if (e != cudaSuccess) return e;
     }
     split_f_kernel<<<64, 256, 0, s>>>(FT, ldf, k, g_fsplit, g_fsplit + k * k);

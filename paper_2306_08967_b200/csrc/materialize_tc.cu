@@ -1,4 +1,4 @@
-// K5 on the 5th-generation tensor cores: Z = X * F for d in {32, 64, 128}
+// K5 on the 5th-generation tensor cores: Z = X * F for d in {32, 64, 128, 256}
 // (factor_state.cpp:120-123 query_all, :215-222 rebase, enhancer.cpp:196-206).
 //
 // Precision: single-pass TF32 misses the 1e-4 contract (SURVEY hard part 3),
@@ -491,6 +491,169 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// d = 256: F (hi + lo = 512 KB) fits neither shared memory nor TMEM, so it
+// streams with X: each stage holds one 32-wide K slice of the X tile (raw ->
+// hi in place, lo) and the matching K slice of F^T for all 256 output
+// columns (hi, lo; 256 rows x 128 B each, SW128), loaded by TMA from L2
+// (F stays L2-resident: 512 KB). Per slice 4 x 3 kind::tf32 MMAs with
+// N = 256; the 128 x 256 fp32 accumulator is double-buffered in TMEM (512
+// columns).
+constexpr int T256_STAGES = 2;
+constexpr int F256_BYTES = 256 * 128;  // one K slice of F^T (256 rows x 128 B)
+constexpr int T256_STAGE = 2 * CHUNK_BYTES + 2 * F256_BYTES;  // 96 KB
+
+__global__ void __launch_bounds__(THREADS, 1)
+    materialize_tc256(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap zmap,
+                      const __grid_constant__ CUtensorMap fhmap, const __grid_constant__ CUtensorMap flmap,
+                      int64_t n) {
+  constexpr int D = 256, KB = D / KC, STAGES = T256_STAGES;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sS = sm;                                   // [STAGES][Xhi|Xlo|Fhi|Flo]
+  unsigned char* sO = sS + STAGES * T256_STAGE;             // [4 warps][2][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 4 * 2 * OSTAGE);
+  uint64_t* full = bars;
+  uint64_t* ready = bars + STAGES;
+  uint64_t* empty = bars + 2 * STAGES;
+  uint64_t* tfull = bars + 3 * STAGES;
+  uint64_t* tempty = bars + 3 * STAGES + 2;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + TM - 1) / TM;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          unsigned char* st = sS + (size_t)s * T256_STAGE;
+          mbar_expect_tx(&full[s], CHUNK_BYTES + 2 * F256_BYTES);
+          tma_load_2d(st, &xmap, kb * KC, (int)(t * TM), &full[s]);
+          tma_load_2d(st + 2 * CHUNK_BYTES, &fhmap, kb * KC, 0, &full[s]);
+          tma_load_2d(st + 2 * CHUNK_BYTES + F256_BYTES, &flmap, kb * KC, 0, &full[s]);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(D >> 3) << 17) |
+                                 ((uint32_t)(TM >> 4) << 24);
+      uint32_t it = 0, tl = 0;
+      const uint32_t sbase = smem_u32(sS);
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        const int a = tl & 1;
+        if (tl >= 2) mbar_wait(&tempty[a], ((tl >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + (uint32_t)(a * D);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&ready[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t xh = sbase + (uint32_t)s * T256_STAGE, xl = xh + CHUNK_BYTES;
+          const uint32_t fh = xh + 2 * CHUNK_BYTES, fl = fh + F256_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < KC / 8; ++ks) {
+            const uint32_t ko = ks * 32;
+            const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+            mma_tf32(dtm, umma_desc(xh + ko), umma_desc(fh + ko), idesc, acc0);
+            mma_tf32(dtm, umma_desc(xh + ko), umma_desc(fl + ko), idesc, 1u);
+            mma_tf32(dtm, umma_desc(xl + ko), umma_desc(fh + ko), idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[a]);
+      }
+    }
+  } else if (warp < 6) {
+    const int st = threadIdx.x - 64;
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        float4* xh = reinterpret_cast<float4*>(sS + (size_t)s * T256_STAGE);
+        float4* xl = reinterpret_cast<float4*>(sS + (size_t)s * T256_STAGE + CHUNK_BYTES);
+#pragma unroll
+        for (int q = 0; q < CHUNK_BYTES / 16 / 128; ++q) {
+          const int i = st + q * 128;
+          float4 v = xh[i];
+          float4 h, l;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          xh[i] = h;
+          xl[i] = l;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[s]);
+      }
+  } else {
+    const int q = warp & 3;
+    unsigned char* stg = sO + (size_t)(warp - 6) * 2 * OSTAGE;
+    uint32_t tl = 0, sb = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+      const int a = tl & 1;
+      mbar_wait(&tfull[a], (tl >> 1) & 1);
+      tc_fence_after();
+      const int64_t row0 = t * TM + q * 32;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32, sb ^= 1) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * D + c0), r);
+        unsigned char* buf = stg + sb * OSTAGE;
+        if (lane == 0) tma_store_wait_read1();
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4*>(buf + sw128(lane, 4 * v)) =
+              make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                          __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && row0 < n) tma_store_2d(&zmap, c0, (int)row0, buf);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 template <int D>
 size_t tc_smem() {
   return 1024 + 2 * (D / KC) * (D * KC * 4) + stages_for<D>() * 2 * CHUNK_BYTES + 8 * OSTAGE + 256;
@@ -532,6 +695,30 @@ cudaError_t launch_tc(const float* X, int64_t n, int ldx, const float* Fhi, cons
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const int64_t ntiles = (n + TM - 1) / TM;
   const int grid = (int)(ntiles < nsm ? ntiles : nsm);
+  if (D == 256) {
+    CUtensorMap fh, fl;
+    cuuint64_t fdims[2] = {256, 256};
+    cuuint64_t fstr[1] = {256 * 4};
+    cuuint32_t fbox[2] = {(cuuint32_t)KC, 256u};
+    r = encode(&fh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Fhi), fdims, fstr, fbox,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    r = encode(&fl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Flo), fdims, fstr, fbox,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    const size_t smem = 1024 + T256_STAGES * T256_STAGE + 8 * OSTAGE + 256;
+    static bool cfg256 = false;
+    if (!cfg256) {
+      cudaError_t e = cudaFuncSetAttribute(materialize_tc256,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      cfg256 = true;
+    }
+    materialize_tc256<<<grid, THREADS, smem, s>>>(map, zm, fh, fl, n);
+    return cudaGetLastError();
+  }
   if (D == 128) {
     const size_t smem = 1024 + TS_STAGES * 2 * CHUNK_BYTES + 8 * OSTAGE + 256;
     static bool cfg128 = false;
@@ -559,7 +746,7 @@ cudaError_t launch_tc(const float* X, int64_t n, int ldx, const float* Fhi, cons
 }  // namespace
 
 bool materialize_tc_supported(int k, int ldx, int ldz, const void* X, const void* Z) {
-  return (k == 32 || k == 64 || k == 128) && (ldx % 4) == 0 && (ldz % 4) == 0 &&
+  return (k == 32 || k == 64 || k == 128 || k == 256) && (ldx % 4) == 0 && (ldz % 4) == 0 &&
          ((uintptr_t)X % 16) == 0 && ((uintptr_t)Z % 16) == 0;
 }
 
@@ -571,6 +758,7 @@ cudaError_t launch_materialize_tc(const float* X, int64_t n, int k, int ldx, con
     case 32: return launch_tc<32>(X, n, ldx, Fhi, Flo, Z, ldz, s, nsm);
     case 64: return launch_tc<64>(X, n, ldx, Fhi, Flo, Z, ldz, s, nsm);
     case 128: return launch_tc<128>(X, n, ldx, Fhi, Flo, Z, ldz, s, nsm);
+    case 256: return launch_tc<256>(X, n, ldx, Fhi, Flo, Z, ldz, s, nsm);
   }
   return cudaErrorInvalidValue;
 }

@@ -18,6 +18,6 @@ elif a.which == "cfg5":
 elif a.which == "ppr":
     r = bench.bench_ppr(a, hbm, kind)
 else:
-    r = bench.bench_materialize(a, hbm, kind)
+    r = dict(zip(("sweep", "roofline"), bench.bench_materialize(a, hbm, kind)))
 r["wall_s"] = round(time.time() - t0, 1)
 print(json.dumps(r))
