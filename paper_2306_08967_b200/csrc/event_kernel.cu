@@ -34,6 +34,9 @@
 
 #include "common.cuh"
 #include "event_kernel.cuh"
+#ifndef DAMF_PROF_RANK
+#define DAMF_PROF_RANK 0  // CTA whose clock feeds the phase counters (dev profiling)
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -418,7 +421,7 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   long long _pt = clock64();
 #define EPROF(slot)                                                        \
   do {                                                                     \
-    if (rank == 0 && threadIdx.x == 0) {                                   \
+    if (rank == DAMF_PROF_RANK && threadIdx.x == 0) {                        \
       const long long _t = clock64();                                      \
       A_prof[slot] += (unsigned long long)(_t - _pt);                      \
       _pt = _t;                                                            \
@@ -727,7 +730,7 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
 // ------------------------------------------------------------ rank-1 step
 #define PROF_MARK(slot)                                                   \
   do {                                                                    \
-    if (rank == 0 && threadIdx.x == 0) {                                  \
+    if (rank == DAMF_PROF_RANK && threadIdx.x == 0) {                     \
       const long long _t = clock64();                                     \
       A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
       _pt = _t;                                                           \
@@ -737,7 +740,7 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
 // ------------------------------------------------------------ rank-1 step
 #define PROF_MARK(slot)                                                   \
   do {                                                                    \
-    if (rank == 0 && threadIdx.x == 0) {                                  \
+    if (rank == DAMF_PROF_RANK && threadIdx.x == 0) {                     \
       const long long _t = clock64();                                     \
       A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
       _pt = _t;                                                           \

@@ -27,8 +27,9 @@ for alpha in alphas:
         if np.any(kinds == kk):
             out[nm + "_p50_us"] = float(np.median(lat[kinds == kk]))
     pc = e.profile_counters().astype(np.float64)
-    names = ["gather+w", "prep", "eigA", "z2", "eigB", "E-gemm", "cols", "inv-rows", "gemms",
-             "sync9", "rowfix", "tail", "graph"]
+    # slot i accumulates the phase ENDING at PROF_MARK(i)
+    names = ["gather+w", "B1+prep", "eigA", "z2+B4", "eigB", "E-gemm", "cols", "B7-reduce",
+             "rowfix+inv-rows", "gemms(4)", "B8", "tail", "graph"]
     out["phase_us_per_event"] = {nm: round(pc[i] / 1.965e3 / (nev + 50), 2) for i, nm in enumerate(names)}
     en = ["eig.prep", "eig.roots", "eig.sync1", "eig.zhat", "eig.sync2", "eig.order", "eig.vecs"]
     out["eig_us_per_event"] = {nm: round(pc[16 + i] / 1.965e3 / (nev + 50), 2) for i, nm in enumerate(en)}
