@@ -3,7 +3,7 @@
 NVCC      ?= nvcc
 CXX       ?= g++
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -diag-suppress 177
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -diag-suppress 177 $(EXTRA)
 PKG       := paper_2306_08967_b200
 CSRC      := $(PKG)/csrc
 CU        := $(CSRC)/event_kernel.cu $(CSRC)/materialize.cu $(CSRC)/materialize_tc.cu $(CSRC)/ppr.cu $(CSRC)/engine.cu

@@ -207,6 +207,8 @@ struct damf_gpu {
   float* hacc = nullptr;
   int *items0 = nullptr, *items1 = nullptr, *hdone = nullptr, *mitems = nullptr;
   long long* ptrace = nullptr;
+  PprState* pst = nullptr;
+  PprState* h_pst = nullptr;  // pinned mirror
   int64_t* dirty[2] = {nullptr, nullptr};  // rows written through P^-1 (see rebase)
   float* dirty_tmp = nullptr;              // gathered dirty rows (kDirtyCap x d)
   unsigned long long* wq = nullptr;
@@ -370,6 +372,8 @@ PprArgs ppr_args(damf_gpu* h) {
   a.hdone = h->hdone;
   a.mitems = h->mitems;
   a.trace = h->ptrace;
+  a.pst = h->pst;
+  a.split = 0;
   a.out = h->out;
   a.in = h->in;
   a.directed = h->directed;
@@ -402,13 +406,28 @@ double* live_Q(damf_gpu* h, int side) { return h->Q[side][h->h_ctl->pp[side]]; }
 
 // PPR push with the current s_max (computed and consumed on the device: no
 // host round trip per event); grid sized to the expected work.
-int run_push(damf_gpu* h, int grid, unsigned long long* t_end) {
+// split = 1 (whole-graph calls): dense pull rounds run as a standalone
+// kernel with more warps per SM; the cooperative kernel exits before such a
+// round and is relaunched after it (one small host read per dense round).
+int run_push(damf_gpu* h, int grid, unsigned long long* t_end, int split = 0) {
   h->launches += 2;
   CK(launch_smax(h->PT[0][0], h->PT[0][1], h->ctl, h->ld, h->smax, h->st));
   PprArgs a = ppr_args(h);
   a.t_end = t_end;
+  a.split = split;
   const int gmax = ppr_push_max_grid(h->nsm, h->d);
-  CK(launch_ppr_push(a, std::min(grid, gmax), h->st));
+  for (;;) {
+    CK(launch_ppr_push(a, std::min(grid, gmax), h->st));
+    if (!split) break;
+    CK(cudaMemcpyAsync(h->h_pst, h->pst, sizeof(PprState), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (!h->h_pst->pull_pending) break;
+    h->h_pst->pull_pending = 0;
+    CK(cudaMemcpyAsync(&h->pst->pull_pending, &h->h_pst->pull_pending, sizeof(int),
+                       cudaMemcpyHostToDevice, h->st));
+    CK(launch_ppr_pull(a, h->nsm, h->st));
+    h->launches += 2;
+  }
   return 0;
 }
 
@@ -430,6 +449,7 @@ void damf_gpu_destroy(damf_gpu* h) {
   cudaStreamSynchronize(h->st);
   for (void* p : h->allocs) cudaFree(p);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
+  if (h->h_pst) cudaFreeHost(h->h_pst);
   if (h->h_pstats) cudaFreeHost(h->h_pstats);
   h->ev.release();
   h->steps.release();
@@ -696,6 +716,9 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
       CK(dalloc(h, &h->hacc, nh * (size_t)d));
       CK(dalloc(h, &h->wq, (size_t)2048));
       CK(dalloc(h, &h->ptrace, (size_t)4 * 1024 + 1));
+      CK(dalloc(h, &h->pst, (size_t)1));
+      CK(cudaMemsetAsync(h->pst, 0, sizeof(PprState), h->st));
+      CK(cudaMallocHost(&h->h_pst, sizeof(PprState)));
       CK(dalloc(h, &h->mitems, 2 * ((size_t)ncap + (size_t)(h->out.pool_size / 512) + 4096)));
       CK(dalloc(h, &h->hdone, nh));
       CK(cudaMemsetAsync(h->hdone, 0, nh * 4, h->st));
@@ -732,7 +755,7 @@ int damf_gpu_ppr_init(damf_gpu* h, damf_apply_stats* stats) {
   CK(launch_ppr_init(a, h->nsm, h->st));
   CK(launch_ppr_keys(a, h->nsm, h->st));
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
-  if (int r = run_push(h, 1 << 20, nullptr)) return r;
+  if (int r = run_push(h, 1 << 20, nullptr, 1)) return r;
   if (int r = sync_ctl(h)) return r;
   if (h->h_ctl->err) return fail(h, h->h_ctl->err, "push_to_tolerance: push budget exceeded");
   if (stats) {
@@ -746,7 +769,7 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
   if (h->alpha1) return 0;
   if (int r = sync_ctl(h)) return r;
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
-  if (int r = run_push(h, 1 << 20, nullptr)) return r;
+  if (int r = run_push(h, 1 << 20, nullptr, 1)) return r;
   if (int r = sync_ctl(h)) return r;
   if (h->h_ctl->err) return fail(h, h->h_ctl->err, "push_to_tolerance: push budget exceeded");
   if (stats) {

@@ -19,6 +19,8 @@
 // preserving, deterministic).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "ppr.cuh"
 
@@ -64,7 +66,13 @@ DAMF_D float row_key(const float* r, int k, double deg) {
 
 constexpr int HEAVY = PPR_HEAVY;
 constexpr int CH = PPR_CH;
-constexpr int G = 8;          // lanes per row group (4 groups per warp)
+#ifndef PPR_G
+#define PPR_G 16
+#endif
+constexpr int G = PPR_G;      // lanes per row group
+constexpr int NG = 32 / G;    // row groups per warp
+constexpr unsigned GMASK = (1u << G) - 1u;
+constexpr unsigned GLEADS = G == 8 ? 0x01010101u : 0x00010001u;
 constexpr int SMALL = 32;     // rows with <= SMALL arcs are pulled by one group
 constexpr int BIGMARK = 1024; // pushers with more in-arcs are marked grid-wide
 
@@ -177,14 +185,14 @@ DAMF_D int grid_compact(cg::grid_group& g, int count, Pred pred, int* out, int* 
 template <int PER, bool VEC>
 struct Cols {
   static constexpr int NE = VEC ? 4 * PER : PER;
-  DAMF_D static int col(int gl, int e) { return VEC ? 4 * gl + 32 * (e >> 2) + (e & 3) : gl + G * e; }
-  DAMF_D static bool owns(int grp, int e) { return (VEC ? (e >> 2) : e) % 4 == grp; }
+  DAMF_D static int col(int gl, int e) { return VEC ? 4 * gl + 4 * G * (e >> 2) + (e & 3) : gl + G * e; }
+  DAMF_D static bool owns(int grp, int e) { return (VEC ? (e >> 2) : e) % NG == grp; }
   template <bool CG = false>
   DAMF_D static void load(const float* row, int gl, int k, float (&x)[NE]) {
     if (VEC) {
 #pragma unroll
       for (int t = 0; t < PER; ++t) {
-        const int j = 4 * gl + 32 * t;
+        const int j = 4 * gl + 4 * G * t;
         const float4* p = reinterpret_cast<const float4*>(row + j);
         float4 v = j < k ? (CG ? __ldcg(p) : *p) : make_float4(0.f, 0.f, 0.f, 0.f);
         x[4 * t] = v.x;
@@ -204,7 +212,7 @@ struct Cols {
     if (VEC) {
 #pragma unroll
       for (int t = 0; t < PER; ++t) {
-        const int j = 4 * gl + 32 * t;
+        const int j = 4 * gl + 4 * G * t;
         if (j < k)
           *reinterpret_cast<float4*>(row + j) = make_float4(x[4 * t], x[4 * t + 1], x[4 * t + 2], x[4 * t + 3]);
       }
@@ -235,7 +243,7 @@ DAMF_D int pull_group(const PprArgs& A, int64_t base, int beg, int end, int R, i
       w = A.out.wts ? (float)A.out.wts[base + p] : 1.0f;
     }
     const bool hit = u >= 0 && A.stamp[u] == R;
-    unsigned mask = (__ballot_sync(gm, hit) >> shift) & 0xFFu;
+    unsigned mask = (__ballot_sync(gm, hit) >> shift) & GMASK;
     matched += __popc(mask);
     while (mask) {
       const int s0 = __ffs(mask) - 1;
@@ -267,7 +275,7 @@ template <int PER, bool VEC>
 DAMF_D int pull_warp(const PprArgs& A, int64_t base, int beg, int end, int R, int k, int lane,
                      int* sid, float* sw, float (&acc)[Cols<PER, VEC>::NE]) {
   using CL = Cols<PER, VEC>;
-  const int grp = lane >> 3, gl = lane & (G - 1);
+  const int grp = lane / G, gl = lane & (G - 1);
   int matched = 0;
   for (int p0 = beg; p0 < end; p0 += 32) {
     const int p = p0 + lane;
@@ -286,7 +294,7 @@ DAMF_D int pull_warp(const PprArgs& A, int64_t base, int beg, int end, int R, in
       sw[pos] = w;
     }
     __syncwarp();
-    for (int q = 2 * grp; q < nh; q += 8) {
+    for (int q = 2 * grp; q < nh; q += 2 * NG) {
       const bool two = q + 1 < nh;
       const int u0 = sid[q], u1 = two ? sid[q + 1] : u0;
       const float w0 = sw[q], w1 = two ? sw[q + 1] : 0.0f;
@@ -338,7 +346,7 @@ template <int PER, bool VEC>
 DAMF_D void finish_warp(const PprArgs& A, int v, int R, int k, double om, int lane,
                         const float (&acc)[Cols<PER, VEC>::NE], bool any) {
   using CL = Cols<PER, VEC>;
-  const int grp = lane >> 3, gl = lane & (G - 1);
+  const int grp = lane / G, gl = lane & (G - 1);
   const bool inF = A.stamp[v] == R;
   if (!inF && !any) return;
   const double degv = A.deg[v];
@@ -348,8 +356,8 @@ DAMF_D void finish_warp(const PprArgs& A, int v, int R, int k, double om, int la
   if (VEC) {
 #pragma unroll
     for (int t = 0; t < PER; ++t) {
-      const int j = 4 * gl + 32 * t;
-      if (t % 4 != grp || j >= k) continue;
+      const int j = 4 * gl + 4 * G * t;
+      if (t % NG != grp || j >= k) continue;
       float4 r = inF ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(rv + j);
       r.x = fmaf(coef, acc[4 * t], r.x);
       r.y = fmaf(coef, acc[4 * t + 1], r.y);
@@ -362,7 +370,7 @@ DAMF_D void finish_warp(const PprArgs& A, int v, int R, int k, double om, int la
 #pragma unroll
     for (int e = 0; e < CL::NE; ++e) {
       const int j = gl + G * e;
-      if (e % 4 != grp || j >= k) continue;
+      if (e % NG != grp || j >= k) continue;
       const float r = fmaf(coef, acc[e], inF ? 0.0f : rv[j]);
       rv[j] = r;
       m = fmaxf(m, fabsf(r));
@@ -376,20 +384,20 @@ template <int PER, bool VEC>
 DAMF_D void reduce_groups(float (&acc)[Cols<PER, VEC>::NE]) {
 #pragma unroll
   for (int e = 0; e < Cols<PER, VEC>::NE; ++e) {
-    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 8);
-    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
   }
 }
 
 // Heavy-row chunk partial -> hacc[h] (vector reductions, owned slice only).
 template <int PER, bool VEC>
 DAMF_D void chunk_accumulate(float* hrow, int k, int lane, const float (&acc)[Cols<PER, VEC>::NE]) {
-  const int grp = lane >> 3, gl = lane & (G - 1);
+  const int grp = lane / G, gl = lane & (G - 1);
   if (VEC) {
 #pragma unroll
     for (int t = 0; t < PER; ++t) {
-      const int j = 4 * gl + 32 * t;
-      if (t % 4 != grp || j >= k) continue;
+      const int j = 4 * gl + 4 * G * t;
+      if (t % NG != grp || j >= k) continue;
       atomicAdd(reinterpret_cast<float4*>(hrow + j),
                 make_float4(acc[4 * t], acc[4 * t + 1], acc[4 * t + 2], acc[4 * t + 3]));
     }
@@ -397,7 +405,7 @@ DAMF_D void chunk_accumulate(float* hrow, int k, int lane, const float (&acc)[Co
 #pragma unroll
     for (int e = 0; e < Cols<PER, VEC>::NE; ++e) {
       const int j = gl + G * e;
-      if (e % 4 != grp || j >= k) continue;
+      if (e % NG != grp || j >= k) continue;
       atomicAdd(hrow + j, acc[e]);
     }
   }
@@ -465,6 +473,107 @@ struct Grabber {
   }
 };
 
+// One dense PULL round over every item (heavy-row chunks encoded -(c+1)
+// first, then light rows), used both inside the cooperative kernel and by
+// the lean standalone pull kernel. Items come from the grabber; small rows
+// go to 8-lane groups, long rows and chunks to whole warps.
+template <int PER, bool VEC>
+DAMF_D void dense_pull(const PprArgs& A, unsigned long long* wq, int R, int nchunks, int n, int k,
+                       double om, int lane, int grp, int gl, unsigned gm, int gw, int nw, int* sid,
+                       float* sw, long long& c_aff, long long& c_arcs, long long& c_pulled) {
+  using CL = Cols<PER, VEC>;
+  const int d = A.d;
+    // ---------------- PULL: items = heavy chunks (-(c+1)) then light rows
+    const int nitems = nchunks + n;
+    Grabber gb(wq + WQ_P3, nitems, gw, nw, NG);
+    int start, cnt;
+    while (gb.next(lane, NG, 32, start, cnt)) {
+      const int stop = start + cnt;
+      for (int base = start; base < stop; base += NG) {
+        const int ii = base + grp;
+        int v = -1, h = -1, beg = 0, end = 0;
+        bool valid = ii < stop;
+        if (valid) {
+          if (ii < nchunks) {
+            const int c = ii;
+            h = A.cidx[c];
+            v = A.heavy[h];
+            beg = (c - A.hoff[h]) * CH;
+            end = min(beg + CH, A.out.cnt[v]);
+          } else {
+            v = ii - nchunks;
+            if (A.hidx[v] >= 0) valid = false;
+            else end = A.out.cnt[v];
+          }
+        }
+        const bool big = valid && (h >= 0 || end > SMALL);
+        if (valid && !big) {
+          float acc[CL::NE];
+#pragma unroll
+          for (int e = 0; e < CL::NE; ++e) acc[e] = 0.0f;
+          const int got = end ? pull_group<PER, VEC>(A, A.out.off[v], 0, end, R, k, gl, gm, acc) : 0;
+          if (gl == 0) {
+            c_aff += 1;
+            c_arcs += end;
+            c_pulled += got;
+          }
+          finish_group<PER, VEC>(A, v, R, k, om, gl, gm, acc, got > 0);
+        }
+        unsigned bm = __ballot_sync(0xffffffffu, big) & GLEADS;
+        while (bm) {
+          const int src = __ffs(bm) - 1;
+          bm &= bm - 1;
+          const int bv = __shfl_sync(0xffffffffu, v, src);
+          const int bh = __shfl_sync(0xffffffffu, h, src);
+          const int bb = __shfl_sync(0xffffffffu, beg, src);
+          const int be = __shfl_sync(0xffffffffu, end, src);
+          float acc[CL::NE];
+#pragma unroll
+          for (int e = 0; e < CL::NE; ++e) acc[e] = 0.0f;
+          const int got = pull_warp<PER, VEC>(A, A.out.off[bv], bb, be, R, k, lane, sid, sw, acc);
+          if (lane == 0) {
+            c_aff += bh < 0;
+            c_arcs += be - bb;
+            c_pulled += got;
+          }
+          if (bh >= 0) {
+            // chunk partial -> hacc[bh]; the warp completing the row's last
+            // chunk finishes the row (threadfence-reduction pattern)
+            if (got) {
+              reduce_groups<PER, VEC>(acc);
+              chunk_accumulate<PER, VEC>(A.hacc + (int64_t)bh * d, k, lane, acc);
+            }
+            __threadfence();
+            __syncwarp();
+            int old = 0;
+            if (lane == 0) old = atomicAdd(&A.hdone[bh], 1);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == A.hoff[bh + 1] - A.hoff[bh] - 1) {
+              __threadfence();
+              float* hrow = A.hacc + (int64_t)bh * d;
+              CL::template load<true>(hrow, gl, k, acc);
+              __syncwarp();
+              if (grp == 0) {
+                float zero[CL::NE];
+#pragma unroll
+                for (int e = 0; e < CL::NE; ++e) zero[e] = 0.0f;
+                CL::store(hrow, gl, k, zero);
+              }
+              if (lane == 0) {
+                A.hdone[bh] = 0;
+                c_aff += 1;
+              }
+              finish_warp<PER, VEC>(A, bv, R, k, om, lane, acc, true);
+            }
+          } else {
+            reduce_groups<PER, VEC>(acc);
+            finish_warp<PER, VEC>(A, bv, R, k, om, lane, acc, got > 0);
+          }
+        }
+      }
+    }
+}
+
 constexpr int MCH = 512;  // in-arcs per scatter item
 
 // One cooperative kernel runs every round of the push with grid barriers.
@@ -487,14 +596,14 @@ constexpr int MCH = 512;  // in-arcs per scatter item
 // nondeterministic (as in the fused per-event push); the defect bound, the
 // reference's contract (enhancer.cpp:98-157), is unaffected.
 template <int PER, bool VEC>
-__global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) ppr_push_kernel(PprArgs A) {
+__global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) ppr_push_kernel(PprArgs A) {
   using CL = Cols<PER, VEC>;
   cg::grid_group g = cg::this_grid();
   __shared__ int s_id[PW][32];
   __shared__ float s_w[PW][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int grp = lane >> 3, gl = lane & (G - 1);
-  const unsigned gm = 0xFFu << (grp * G);
+  const int grp = lane / G, gl = lane & (G - 1);
+  const unsigned gm = GMASK << (grp * G);
   const unsigned lt = (1u << lane) - 1u;
   const int gw = blockIdx.x * PW + wib, nw = gridDim.x * PW;
   int* sid = s_id[wib];
@@ -506,18 +615,27 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
   const float thr = (float)(A.alpha_eps / *A.smax);
   const double om = 1.0 - A.alpha;
   const DevCSR& inC = A.directed ? A.in : A.out;
-  int R = (int)A.stats[2];  // device-resident round stamp base (monotonic)
+  const bool resume = A.split && A.pst->phase == 1;
+  int R = resume ? A.pst->R : (int)A.stats[2];  // device-resident round stamp base (monotonic)
   if (blockIdx.x == 0)
     for (int i = threadIdx.x; i < WQ_SC + 16 * QS; i += PT_) wq[i] = 0;
+  int nH, nchunks;
+  long long narcs;
+  if (resume) {
+    nH = A.pst->nH;
+    nchunks = A.pst->nchunks;
+    narcs = A.pst->narcs;
+    g.sync();  // counters zeroed
+  } else {
   // ---- heavy rows (> HEAVY out-arcs): list, chunk prefix, chunk -> row
-  const int nH = grid_compact(
+  nH = grid_compact(
       g, n,
       [&](int i, int& v) {
         v = i;
         return A.out.cnt[i] > HEAVY;
       },
       A.heavy, A.blk);
-  const int nchunks = grid_scan(
+  nchunks = grid_scan(
       g, nH, [&](int h) { return (A.out.cnt[A.heavy[h]] + CH - 1) / CH; }, A.hoff, A.blk);
   {
     for (int h = blockIdx.x * PT_ + threadIdx.x; h < nH; h += gridDim.x * PT_) {
@@ -530,16 +648,18 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
     if (lane == 0 && arcs) atomicAdd(&sc[SC_ARCS * QS], arcs);
   }
   g.sync();
-  const long long narcs = (long long)*(volatile unsigned long long*)&sc[SC_ARCS * QS];
+  narcs = (long long)*(volatile unsigned long long*)&sc[SC_ARCS * QS];
+  }
   // ---- rounds
-  bool cand_all = A.ncand < 0;
+  bool cand_all = resume || A.ncand < 0;
   int ncand = cand_all ? n : A.ncand;
   const int* candL = cand_all ? nullptr : A.cand;
   bool fresh = false;  // candidates' keys must be recomputed from r
-  long long pushes = 0;
+  long long pushes = resume ? A.pst->pushes : 0;
   long long c_aff = 0, c_arcs = 0, c_pulled = 0;  // lane-0 accounting
-  int rounds = 0;
-  int cur = 0;  // items[cur]: rows touched by this round's scatter
+  int rounds = resume ? A.pst->rounds : 0;
+  int cur = resume ? A.pst->cur : 0;  // items[cur]: rows touched by this round's scatter
+  bool split_exit = false;
   // per-phase wall time (block 0 thread 0, %globaltimer ns) -> ctl->prof[24..28]
   const bool tl = blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long tp = tl ? globaltimer() : 0;
@@ -613,7 +733,7 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
           if (push) sid[__popc(pm & lt)] = v;
           myS += add_items(v, push);
           __syncwarp();
-          for (int j = grp; j < np; j += 4) {
+          for (int j = grp; j < np; j += NG) {
             const int u = sid[j];
             float x[CL::NE];
             CL::load(A.rb + (int64_t)u * d, gl, k, x);
@@ -624,10 +744,10 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
       }
     } else {
       // after a scatter: group per candidate, key from r, push if over
-      Grabber gb(wq + WQ_P1, ncand, gw, nw, 4);
+      Grabber gb(wq + WQ_P1, ncand, gw, nw, NG);
       int start, cnt;
-      while (gb.next(lane, 4, 32, start, cnt)) {
-        for (int base = start; base < start + cnt; base += 4) {
+      while (gb.next(lane, NG, 32, start, cnt)) {
+        for (int base = start; base < start + cnt; base += NG) {
           const int q = base + grp;
           const int v = q < start + cnt ? candL[q] : -1;
           bool push = false;
@@ -686,96 +806,26 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
       t[2] = S;
       t[3] = nmi;
     }
-    if (dense) {
-      // ---------------- PULL: items = heavy chunks (-(c+1)) then light rows
-      const int nitems = nchunks + n;
-      Grabber gb(wq + WQ_P3, nitems, gw, nw, 4);
-      int start, cnt;
-      while (gb.next(lane, 4, 32, start, cnt)) {
-        const int stop = start + cnt;
-        for (int base = start; base < stop; base += 4) {
-          const int ii = base + grp;
-          int v = -1, h = -1, beg = 0, end = 0;
-          bool valid = ii < stop;
-          if (valid) {
-            if (ii < nchunks) {
-              const int c = ii;
-              h = A.cidx[c];
-              v = A.heavy[h];
-              beg = (c - A.hoff[h]) * CH;
-              end = min(beg + CH, A.out.cnt[v]);
-            } else {
-              v = ii - nchunks;
-              if (A.hidx[v] >= 0) valid = false;
-              else end = A.out.cnt[v];
-            }
-          }
-          const bool big = valid && (h >= 0 || end > SMALL);
-          if (valid && !big) {
-            float acc[CL::NE];
-#pragma unroll
-            for (int e = 0; e < CL::NE; ++e) acc[e] = 0.0f;
-            const int got = end ? pull_group<PER, VEC>(A, A.out.off[v], 0, end, R, k, gl, gm, acc) : 0;
-            if (gl == 0) {
-              c_aff += 1;
-              c_arcs += end;
-              c_pulled += got;
-            }
-            finish_group<PER, VEC>(A, v, R, k, om, gl, gm, acc, got > 0);
-          }
-          unsigned bm = __ballot_sync(0xffffffffu, big) & 0x01010101u;
-          while (bm) {
-            const int src = __ffs(bm) - 1;
-            bm &= bm - 1;
-            const int bv = __shfl_sync(0xffffffffu, v, src);
-            const int bh = __shfl_sync(0xffffffffu, h, src);
-            const int bb = __shfl_sync(0xffffffffu, beg, src);
-            const int be = __shfl_sync(0xffffffffu, end, src);
-            float acc[CL::NE];
-#pragma unroll
-            for (int e = 0; e < CL::NE; ++e) acc[e] = 0.0f;
-            const int got = pull_warp<PER, VEC>(A, A.out.off[bv], bb, be, R, k, lane, sid, sw, acc);
-            if (lane == 0) {
-              c_aff += bh < 0;
-              c_arcs += be - bb;
-              c_pulled += got;
-            }
-            if (bh >= 0) {
-              // chunk partial -> hacc[bh]; the warp completing the row's last
-              // chunk finishes the row (threadfence-reduction pattern)
-              if (got) {
-                reduce_groups<PER, VEC>(acc);
-                chunk_accumulate<PER, VEC>(A.hacc + (int64_t)bh * d, k, lane, acc);
-              }
-              __threadfence();
-              __syncwarp();
-              int old = 0;
-              if (lane == 0) old = atomicAdd(&A.hdone[bh], 1);
-              old = __shfl_sync(0xffffffffu, old, 0);
-              if (old == A.hoff[bh + 1] - A.hoff[bh] - 1) {
-                __threadfence();
-                float* hrow = A.hacc + (int64_t)bh * d;
-                CL::template load<true>(hrow, gl, k, acc);
-                __syncwarp();
-                if (grp == 0) {
-                  float zero[CL::NE];
-#pragma unroll
-                  for (int e = 0; e < CL::NE; ++e) zero[e] = 0.0f;
-                  CL::store(hrow, gl, k, zero);
-                }
-                if (lane == 0) {
-                  A.hdone[bh] = 0;
-                  c_aff += 1;
-                }
-                finish_warp<PER, VEC>(A, bv, R, k, om, lane, acc, true);
-              }
-            } else {
-              reduce_groups<PER, VEC>(acc);
-              finish_warp<PER, VEC>(A, bv, R, k, om, lane, acc, got > 0);
-            }
-          }
-        }
+    if (dense && A.split) {
+      // hand the round to the lean pull kernel (more warps per SM than this
+      // cooperative kernel's register budget allows) and resume after it
+      if (tl) {
+        A.pst->R = R;
+        A.pst->rounds = rounds;
+        A.pst->pushes = pushes;
+        A.pst->nH = nH;
+        A.pst->nchunks = nchunks;
+        A.pst->narcs = narcs;
+        A.pst->cur = cur ^ 1;
+        A.pst->phase = 1;
+        A.pst->pull_pending = 1;
       }
+      split_exit = true;
+      break;
+    }
+    if (dense) {
+      dense_pull<PER, VEC>(A, wq, R, nchunks, n, k, om, lane, grp, gl, gm, gw, nw, sid, sw, c_aff,
+                           c_arcs, c_pulled);
     } else {
       // ---------------- SCATTER over the pushed rows' in-arc chunks
       int* L = A.items[cur];
@@ -811,7 +861,7 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
               if (lane == 0) c_aff += __popc(tm);
             }
             const int na = min(32, end - p0);
-            for (int a0 = 0; a0 < na; a0 += 4) {
+            for (int a0 = 0; a0 < na; a0 += NG) {
               const int a = a0 + grp;
               const int va = __shfl_sync(0xffffffffu, v, a);
               const float ca = __shfl_sync(0xffffffffu, coef, a);
@@ -820,7 +870,7 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
               if (VEC) {
 #pragma unroll
                 for (int t4 = 0; t4 < PER; ++t4) {
-                  const int j = 4 * gl + 32 * t4;
+                  const int j = 4 * gl + 4 * G * t4;
                   if (j < k)
                     atomicAdd(reinterpret_cast<float4*>(rv + j),
                               make_float4(ca * x[4 * t4], ca * x[4 * t4 + 1], ca * x[4 * t4 + 2],
@@ -856,7 +906,8 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
     candL = A.items[cur];
     cur ^= 1;
   }
-  for (int h = blockIdx.x * PT_ + threadIdx.x; h < nH; h += gridDim.x * PT_) A.hidx[A.heavy[h]] = -1;
+  if (!split_exit)
+    for (int h = blockIdx.x * PT_ + threadIdx.x; h < nH; h += gridDim.x * PT_) A.hidx[A.heavy[h]] = -1;
   // accounting (bench algorithmic bytes): lane-0 counters of groups/warps
   for (int o = 16; o > 0; o >>= 1) {
     c_aff += __shfl_xor_sync(0xffffffffu, c_aff, o);
@@ -868,13 +919,47 @@ __global__ void __launch_bounds__(PT_, (PER >= 4 && VEC) || PER >= 32 ? 2 : 3) p
     atomicAdd((unsigned long long*)&A.stats[5], (unsigned long long)c_arcs);
     atomicAdd((unsigned long long*)&A.stats[6], (unsigned long long)c_pulled);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !split_exit) {
     if (A.trace) A.trace[4 * 1024] = rounds;
     A.stats[0] += pushes;
     A.stats[1] += rounds;
     A.stats[2] = R;  // next round base
     A.stats[3] += pushes;
+    if (A.split) {
+      A.pst->phase = 0;
+      A.pst->pull_pending = 0;
+    }
     if (A.t_end) *A.t_end = globaltimer();
+  }
+}
+
+// Dense PULL round as a standalone (non-cooperative) kernel: same work as the
+// in-kernel round, but with a register budget that fits 4 CTAs (32 warps)
+// per SM — random 512-byte gathers need ~24-32 warps per SM to approach HBM
+// peak (tools/micro_gather.cu). Round state comes from PprState.
+template <int PER, bool VEC>
+#ifndef PPR_PULL_MINB
+#define PPR_PULL_MINB 8
+#endif
+__global__ void __launch_bounds__(PT_, PPR_PULL_MINB) ppr_pull_kernel(PprArgs A) {
+  __shared__ int s_id[PW][32];
+  __shared__ float s_w[PW][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int grp = lane / G, gl = lane & (G - 1);
+  const unsigned gm = GMASK << (grp * G);
+  const int gw = blockIdx.x * PW + wib, nw = gridDim.x * PW;
+  long long c_aff = 0, c_arcs = 0, c_pulled = 0;
+  dense_pull<PER, VEC>(A, A.wq, A.pst->R, A.pst->nchunks, (int)A.n, A.ctl->k, 1.0 - A.alpha, lane,
+                       grp, gl, gm, gw, nw, s_id[wib], s_w[wib], c_aff, c_arcs, c_pulled);
+  for (int o = 16; o > 0; o >>= 1) {
+    c_aff += __shfl_xor_sync(0xffffffffu, c_aff, o);
+    c_arcs += __shfl_xor_sync(0xffffffffu, c_arcs, o);
+    c_pulled += __shfl_xor_sync(0xffffffffu, c_pulled, o);
+  }
+  if (lane == 0 && (c_aff | c_arcs | c_pulled)) {
+    atomicAdd((unsigned long long*)&A.stats[4], (unsigned long long)c_aff);
+    atomicAdd((unsigned long long*)&A.stats[5], (unsigned long long)c_arcs);
+    atomicAdd((unsigned long long*)&A.stats[6], (unsigned long long)c_pulled);
   }
 }
 
@@ -1001,23 +1086,48 @@ int max_grid_t(int nsm) {
 cudaError_t launch_ppr_push(const PprArgs& a, int grid, cudaStream_t s) {
   const int d = a.d;
   if (d % 4 == 0) {
-    if (d <= 32) return launch_push_t<1, true>(a, grid, s);
-    if (d <= 64) return launch_push_t<2, true>(a, grid, s);
-    if (d <= 128) return launch_push_t<4, true>(a, grid, s);
+    const int per = (d + 4 * G - 1) / (4 * G);
+    if (per <= 1) return launch_push_t<1, true>(a, grid, s);
+    if (per <= 2) return launch_push_t<2, true>(a, grid, s);
+    if (per <= 4) return launch_push_t<4, true>(a, grid, s);
     return launch_push_t<8, true>(a, grid, s);
   }
-  if (d <= 32) return launch_push_t<4, false>(a, grid, s);
+  if (d <= 4 * G) return launch_push_t<4, false>(a, grid, s);
   return launch_push_t<32, false>(a, grid, s);
+}
+
+namespace {
+template <int PER, bool VEC>
+cudaError_t launch_pull_t(const PprArgs& a, int nsm, cudaStream_t s) {
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ppr_pull_kernel<PER, VEC>, PT_, 0);
+  ppr_pull_kernel<PER, VEC><<<std::max(per, 1) * nsm, PT_, 0, s>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_ppr_pull(const PprArgs& a, int nsm, cudaStream_t s) {
+  const int d = a.d;
+  if (d % 4 == 0) {
+    const int per = (d + 4 * G - 1) / (4 * G);
+    if (per <= 1) return launch_pull_t<1, true>(a, nsm, s);
+    if (per <= 2) return launch_pull_t<2, true>(a, nsm, s);
+    if (per <= 4) return launch_pull_t<4, true>(a, nsm, s);
+    return launch_pull_t<8, true>(a, nsm, s);
+  }
+  if (d <= 4 * G) return launch_pull_t<4, false>(a, nsm, s);
+  return launch_pull_t<32, false>(a, nsm, s);
 }
 
 int ppr_push_max_grid(int nsm, int d) {
   if (d % 4 == 0) {
-    if (d <= 32) return max_grid_t<1, true>(nsm);
-    if (d <= 64) return max_grid_t<2, true>(nsm);
-    if (d <= 128) return max_grid_t<4, true>(nsm);
+    const int per = (d + 4 * G - 1) / (4 * G);
+    if (per <= 1) return max_grid_t<1, true>(nsm);
+    if (per <= 2) return max_grid_t<2, true>(nsm);
+    if (per <= 4) return max_grid_t<4, true>(nsm);
     return max_grid_t<8, true>(nsm);
   }
-  if (d <= 32) return max_grid_t<4, false>(nsm);
+  if (d <= 4 * G) return max_grid_t<4, false>(nsm);
   return max_grid_t<32, false>(nsm);
 }
 

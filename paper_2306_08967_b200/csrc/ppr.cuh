@@ -6,6 +6,15 @@ namespace dgpu {
 constexpr int PPR_HEAVY = 256;  // rows with more out-arcs are pulled in chunks
 constexpr int PPR_CH = 256;     // arcs per chunk
 
+// Cross-launch state of a push split into cooperative rounds + standalone
+// dense-pull launches (damf_gpu_ppr_init / _push).
+struct PprState {
+  int phase;         // 0: fresh call, 1: resume after a dense pull
+  int pull_pending;  // set when the cooperative kernel exits for a dense pull
+  int R, rounds, nH, nchunks, cur, pad;
+  long long pushes, narcs;
+};
+
 struct PprArgs {
   int64_t n;
   int d, k;
@@ -28,6 +37,8 @@ struct PprArgs {
   int* items[2];      // P3 work lists, alternating per round (n + chunks)
   int* hdone;         // per heavy row: chunks finished this round (kept zero between rounds)
   int* mitems;        // marking items (pusher, in-arc chunk) pairs
+  PprState* pst;      // split-mode state (device)
+  int split;          // 1: exit the cooperative kernel for dense pull rounds
   long long* trace;   // per-round [nF, dense, items, active heavy] of the last call (4 x 1024)
   unsigned long long* wq;  // work counters [P1 grab, P3 grab, big-mark count, push count x3,
                            //  item count, active heavy count]
@@ -48,6 +59,7 @@ struct PprArgs {
 };
 
 cudaError_t launch_ppr_push(const PprArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_ppr_pull(const PprArgs& a, int nsm, cudaStream_t s);
 int ppr_push_max_grid(int nsm, int d);
 cudaError_t launch_ppr_absorb(const PprArgs& a, const int64_t* rows, int nrows, cudaStream_t s);
 cudaError_t launch_ppr_keys(const PprArgs& a, int nsm, cudaStream_t s);
