@@ -283,6 +283,16 @@ def ncu_traffic(fname, kernel_substr):
     return None
 
 
+def ppr_traffic():
+    """DRAM bytes of one init_propagate (all push / pull launches) from the
+    committed ncu launch list summary, or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "r1_ppr23_traffic.json")
+    if not os.path.exists(path):
+        return None
+    return int(json.load(open(path))["dram_bytes_per_init"])
+
+
 def bench_materialize(args, hbm, peak_kind):
     """Z = X F on the cfg-4 shape (n = 2^23, X ~ N(0,1/d), F = Q diag(U[.5,2]))."""
     import torch
@@ -413,9 +423,9 @@ def bench_ppr(args, hbm, peak_kind):
             "roofline": {"kernel": "ppr_push_kernel (init_propagate)", "bound": "hbm",
                          "achieved": round(gbs_init, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(gbs_init / hbm, 4),
-                         "traffic": ncu_traffic("r1_ppr23_raw.csv", "ppr_push_kernel"),
-                         "traffic_source": "profiles/r1_ppr23_raw.csv (ncu --set full, init_propagate "
-                                           "on the same graph)",
+                         "traffic": ppr_traffic(),
+                         "traffic_source": "profiles/r1_ppr23_traffic.json (ncu DRAM bytes summed "
+                                           "over every launch of one init_propagate, same graph)",
                          "peak_kind": peak_kind}}
 
 
