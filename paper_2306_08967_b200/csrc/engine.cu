@@ -202,6 +202,7 @@ struct damf_gpu {
   float *Xb = nullptr, *Yb = nullptr, *Zb = nullptr, *rb = nullptr, *delta = nullptr,
         *key = nullptr;
   int *stamp = nullptr, *mark = nullptr, *listF = nullptr, *listL = nullptr, *blk = nullptr;
+  int* listG = nullptr;
   long long* blk64 = nullptr;
   int *heavy = nullptr, *hidx = nullptr, *hoff = nullptr, *cidx = nullptr;
   float* hacc = nullptr;
@@ -287,6 +288,7 @@ EventKernelArgs event_args(damf_gpu* h) {
   a.stamp = h->stamp;
   a.mark = h->mark;
   a.listF = h->listF;
+  a.listG = h->listG;
   a.listL = h->listL;
   a.touched = h->touched.d;
   a.pstats = h->pstats;
@@ -702,6 +704,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
     CK(dalloc(h, &h->mark, (size_t)ncap));
     // fused in-cluster lists: C regions of (ceil(ceil(n/32)/C)*32/NW + 1)*NW
     CK(dalloc(h, &h->listF, (size_t)ncap + 16 * 32 * 2 + 4096));
+    CK(dalloc(h, &h->listG, (size_t)ncap + 16 * 32 * 2 + 4096));
     CK(dalloc(h, &h->listL, (size_t)ncap + 16 * 32 * 2 + 4096));
     CK(dalloc(h, &h->blk, (size_t)4096));
     CK(dalloc(h, &h->blk64, (size_t)4096));

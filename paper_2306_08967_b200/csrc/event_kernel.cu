@@ -37,6 +37,12 @@
 #ifndef DAMF_PROF_RANK
 #define DAMF_PROF_RANK 0  // CTA whose clock feeds the phase counters (dev profiling)
 #endif
+// Phase counters (ctl->prof) cost a global read-modify-write on the
+// critical path of every phase; they are compiled in only with -DDAMF_PROF=1
+// (tools/prof_events.py builds that way).
+#ifndef DAMF_PROF
+#define DAMF_PROF 0
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -50,6 +56,7 @@ constexpr int NMAX = kMaxD + 1;    // k + 1 <= 257
 constexpr int NPAD = kMaxD + 4;
 constexpr double EPS = DBL_EPSILON;
 constexpr int PLD = 132;           // private-matrix row stride (d <= 128 in smem)
+constexpr int PCAP = 2048;         // fused-PPR candidate list entries kept in shared memory
 
 template <int C>
 struct Smem {
@@ -71,6 +78,8 @@ struct Smem {
   double vscr[NW][NPAD];          // per-warp eigenvector scratch (rare deflation path)
   double bred[NW];
   long long found[C][2];          // graph row-scan results
+  int lcnt3[3];                   // fused PPR: rows in this CTA's candidate lists (round mod 3)
+  int plist[3][PCAP];             // fused PPR: candidate lists (round mod 3); overflow in global
   int K, nrot, need;
   int k, pp[2];
   int err;
@@ -421,7 +430,7 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   long long _pt = clock64();
 #define EPROF(slot)                                                        \
   do {                                                                     \
-    if (rank == DAMF_PROF_RANK && threadIdx.x == 0) {                        \
+    if (DAMF_PROF && rank == DAMF_PROF_RANK && threadIdx.x == 0) {           \
       const long long _t = clock64();                                      \
       A_prof[slot] += (unsigned long long)(_t - _pt);                      \
       _pt = _t;                                                            \
@@ -523,9 +532,9 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
     double t;
     int o;
     const int its = secular_root(S.kd, S.kz2, K, rhoN, sz2, j, t, o);
-    if (gl == 0 && rank == 0) atomicAdd(&A_prof[13], (unsigned long long)its);
-    if (gl == 0 && rank == 0) atomicAdd(&A_prof[14], 1ull);
-    if (gl == 0) atomicMax(&A_prof[15], (unsigned long long)its);
+    if (DAMF_PROF && gl == 0 && rank == 0) atomicAdd(&A_prof[13], (unsigned long long)its);
+    if (DAMF_PROF && gl == 0 && rank == 0) atomicAdd(&A_prof[14], 1ull);
+    if (DAMF_PROF && gl == 0) atomicMax(&A_prof[15], (unsigned long long)its);
     if (gl < C) {
       *cl.map_shared_rank(S.tau + j, gl) = t;
       *cl.map_shared_rank(S.org + j, gl) = o;
@@ -730,7 +739,7 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
 // ------------------------------------------------------------ rank-1 step
 #define PROF_MARK(slot)                                                   \
   do {                                                                    \
-    if (rank == DAMF_PROF_RANK && threadIdx.x == 0) {                     \
+    if (DAMF_PROF && rank == DAMF_PROF_RANK && threadIdx.x == 0) {        \
       const long long _t = clock64();                                     \
       A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
       _pt = _t;                                                           \
@@ -740,7 +749,7 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
 // ------------------------------------------------------------ rank-1 step
 #define PROF_MARK(slot)                                                   \
   do {                                                                    \
-    if (rank == DAMF_PROF_RANK && threadIdx.x == 0) {                     \
+    if (DAMF_PROF && rank == DAMF_PROF_RANK && threadIdx.x == 0) {        \
       const long long _t = clock64();                                     \
       A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
       _pt = _t;                                                           \
@@ -1418,62 +1427,110 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
   };
   cl.sync();  // touched-row residuals and keys visible
   // first candidates: own rows whose stored key is over threshold
-  int ncand = compact([&](int v) { return A.key[v] > thr; }, Ll);
-  bool first = true;
+  // round-0 candidates: own rows whose stored key is over threshold, in this
+  // CTA's region of list 0; rounds r >= 1 read list r % 3, which the pushes
+  // of round r - 1 filled (owner CTA region, DSMEM counters)
+  {
+    const int c0 = compact([&](int v) { return A.key[v] > thr; }, Ll);
+    if (tid == 0) S.lcnt3[0] = c0;
+  }
+  cl.sync();  // round-0 lists and counts visible cluster-wide
   PROF_MARK(25);
-  for (;;) {
-    // P1: evaluate candidates (warp per row, 2 rows in flight), push the ones
-    // over threshold into this warp's segment of Fl
+  const DevCSR& in = A.directed ? A.in : A.out;
+  int* lists[3] = {A.listL, A.listF, A.listG};
+  for (int rr = 0;; ++rr) {
+    const int cur = rr % 3, nxt = (rr + 1) % 3, old = (rr + 2) % 3;
+    // One phase per round. Each CTA evaluates the candidates of its own
+    // list (filled by the previous round's pushes, shared memory with a
+    // global overflow); a candidate over threshold is pushed at once: r[u]
+    // read-and-zeroed with atomicExch (concurrent contributions are either in
+    // this push or stay in r), Z[u] += delta, key = 0, and delta is scattered
+    // from registers into r[v], v in in(u) (red.global.add); the first
+    // toucher of v appends it to its owner's next list over DSMEM. An
+    // asynchronous push in rounds: the contract is the defect bound
+    // (enhancer.cpp:98-157); the summation order is nondeterministic.
+    const int mycnt = S.lcnt3[cur];
+    __syncthreads();
+    if (tid == 0) S.lcnt3[old] = 0;  // next filled in round rr + 1 (after this round's barrier)
     int myF = 0;
-    for (int q = warp; q < ncand; q += 2 * NW) {
-      int vv[2];
-      float rj[2][kMaxD / 32];
+    for (int q = warp; q < mycnt; q += NW) {
+      const int v = (rr > 0 && q < PCAP) ? S.plist[cur][q] : lists[cur][(int64_t)rank * stride + q];
+      // independent loads of the candidate, issued together
+      const float* rv0 = A.rb + (int64_t)v * d;
+      float* zu = A.Zb + (int64_t)v * d;
+      float rj[kMaxD / 32], zj[kMaxD / 32];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int qq = q + h * NW;
-        vv[h] = qq < ncand ? Ll[qq] : -1;
-        const float* rv = A.rb + (int64_t)(vv[h] < 0 ? 0 : vv[h]) * d;
+      for (int t = 0; t < kMaxD / 32; ++t) {
+        const int j = lane + 32 * t;
+        rj[t] = j < k ? rv0[j] : 0.0f;
+        zj[t] = j < k ? zu[j] : 0.0f;
+      }
+      const double degv = A.deg[v];
+      const float keyv = rr == 0 ? A.key[v] : 0.0f;
+      const int64_t ib = in.off[v];
+      const int c = in.cnt[v];
+      float m = 0.0f;
 #pragma unroll
-        for (int t = 0; t < kMaxD / 32; ++t) {
-          const int j = lane + 32 * t;
-          rj[h][t] = (vv[h] >= 0 && j < k) ? rv[j] : 0.0f;
+      for (int t = 0; t < kMaxD / 32; ++t) m = fmaxf(m, fabsf(rj[t]));
+      m = warp_max(m);
+      const float key = (float)((double)m / fmax(degv, 1.0));
+      const bool push = rr == 0 ? keyv > thr : key > thr;
+      if (!push) {
+        if (lane == 0) A.key[v] = key;
+        continue;
+      }
+      // first 32 in-arcs issued alongside the read-and-zero of r[u]
+      int vv0 = -1;
+      float w0 = 1.0f;
+      if (lane < c) {
+        vv0 = in.ids[ib + lane];
+        if (in.wts) w0 = (float)in.wts[ib + lane];
+      }
+      float* rv = A.rb + (int64_t)v * d;
+#pragma unroll
+      for (int t = 0; t < kMaxD / 32; ++t) {
+        const int j = lane + 32 * t;
+        if (j < k) {
+          rj[t] = atomicExch(rv + j, 0.0f);
+          zu[j] = zj[t] + rj[t];
         }
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int v = vv[h];
-        if (v < 0) continue;
-        float m = 0.0f;
-#pragma unroll
-        for (int t = 0; t < kMaxD / 32; ++t) m = fmaxf(m, fabsf(rj[h][t]));
-        m = warp_max(m);
-        const double degv = A.deg[v];
-        const float key = (float)((double)m / fmax(degv, 1.0));
-        const bool push = first ? A.key[v] > thr : key > thr;
-        if (!push) {
-          if (lane == 0) A.key[v] = key;
-          continue;
-        }
-        float* du = A.delta + (int64_t)v * d;
-        float* zu = A.Zb + (int64_t)v * d;
-        float* rv = A.rb + (int64_t)v * d;
-#pragma unroll
-        for (int t = 0; t < kMaxD / 32; ++t) {
-          const int j = lane + 32 * t;
-          if (j < k) {
-            du[j] = rj[h][t];
-            zu[j] += rj[h][t];
-            rv[j] = 0.0f;
+      if (lane == 0) A.key[v] = 0.0f;
+      ++myF;
+      for (int p0 = 0; p0 < c; p0 += 32) {
+        const int p = p0 + lane;
+        int vv = -1;
+        float cf = 0.0f;
+        if (p < c) {
+          float w = w0;
+          vv = vv0;
+          if (p0 > 0) {
+            vv = in.ids[ib + p];
+            w = in.wts ? (float)in.wts[ib + p] : 1.0f;
+          }
+          cf = (float)(om * w / fmax(A.deg[vv], 1.0));
+          if (atomicExch(&A.mark[vv], R + 1) != R + 1) {
+            const int ow = (vv >> 5) % C;
+            const int pos = atomicAdd(cl.map_shared_rank(&S.lcnt3[nxt], ow), 1);
+            if (pos < PCAP)
+              *cl.map_shared_rank(&S.plist[nxt][pos], ow) = vv;
+            else
+              lists[nxt][(int64_t)ow * stride + pos] = vv;
           }
         }
-        if (lane == 0) {
-          A.key[v] = 0.0f;
-          Fl[warp * seg + myF] = v;
+        const int cnt = min(32, c - p0);
+        for (int s2 = 0; s2 < cnt; ++s2) {
+          const int tv = __shfl_sync(0xffffffffu, vv, s2);
+          const float cc = __shfl_sync(0xffffffffu, cf, s2);
+          float* rt = A.rb + (int64_t)tv * d;
+#pragma unroll
+          for (int t = 0; t < kMaxD / 32; ++t) {
+            const int j = lane + 32 * t;
+            if (j < k) atomicAdd(rt + j, cc * rj[t]);  // RED.ADD.F32
+          }
         }
-        ++myF;
       }
     }
-    first = false;
     if (lane == 0) s_cnt[warp] = myF;
     __syncthreads();
     int nF = 0;
@@ -1481,60 +1538,21 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     PROF_MARK(26);
     if (tid == 0)
       for (int r = 0; r < C; ++r) *cl.map_shared_rank(&S.found[rank][0], r) = nF;
-    cl.sync();  // all residuals of this round's frontier are read and zeroed
+    cl.sync();  // pushes, contributions and next lists of this round landed
     PROF_MARK(27);
     long long tot = 0;
     for (int r = 0; r < C; ++r) tot += S.found[r][0];
-    if (tot == 0) break;
     ++R;
+    if (tot == 0) {
+      if (tid == 0) S.lcnt3[cur] = 0;  // all counters zero for the next event
+      break;
+    }
     ++rounds;
     pushes += tot;
     if (pushes > 1000000000LL) {
       if (rank == 0 && tid == 0) A.ctl->err = 9;  // NonConvergence
       break;
     }
-    // P2: scatter (1-alpha) w / max(deg v,1) delta_u into r[v], v in in(u)
-    const DevCSR& in = A.directed ? A.in : A.out;
-    for (int q = warp; q < nF; q += NW) {
-      int sw = 0, qq = q;
-      while (qq >= s_cnt[sw]) qq -= s_cnt[sw++];
-      const int u = Fl[sw * seg + qq];
-      float du[kMaxD / 32];
-#pragma unroll
-      for (int t = 0; t < kMaxD / 32; ++t) {
-        const int j = lane + 32 * t;
-        du[t] = j < k ? A.delta[(int64_t)u * d + j] : 0.0f;
-      }
-      const int64_t ib = in.off[u];
-      const int c = in.cnt[u];
-      for (int p0 = 0; p0 < c; p0 += 32) {
-        const int p = p0 + lane;
-        int v = -1;
-        float cf = 0.0f;
-        if (p < c) {
-          v = in.ids[ib + p];
-          const float w = in.wts ? (float)in.wts[ib + p] : 1.0f;
-          cf = (float)(om * w / fmax(A.deg[v], 1.0));
-          A.mark[v] = R;
-        }
-        const int cnt = min(32, c - p0);
-        for (int s2 = 0; s2 < cnt; ++s2) {
-          const int vv = __shfl_sync(0xffffffffu, v, s2);
-          const float cc = __shfl_sync(0xffffffffu, cf, s2);
-          float* rv = A.rb + (int64_t)vv * d;
-#pragma unroll
-          for (int t = 0; t < kMaxD / 32; ++t) {
-            const int j = lane + 32 * t;
-            if (j < k) atomicAdd(rv + j, cc * du[t]);  // RED.ADD.F32
-          }
-        }
-      }
-    }
-    PROF_MARK(28);
-    cl.sync();  // contributions landed
-    PROF_MARK(29);
-    // next candidates: own rows marked this round
-    ncand = compact([&](int v) { return A.mark[v] == R; }, Ll);
     PROF_MARK(30);
   }
   if (rank == 0 && tid == 0) {
@@ -1557,8 +1575,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     S.k = A.ctl->k;
     S.pp[0] = A.ctl->pp[0];
     S.pp[1] = A.ctl->pp[1];
+    for (int i = 0; i < 3; ++i) S.lcnt3[i] = 0;  // fused-PPR counters
   }
   __syncthreads();
+  cl.sync();  // counters zeroed before any CTA can append to them
   for (int64_t e = A.e_begin; e < A.e_end; ++e) {
     if (*(volatile int*)&A.ctl->err) break;
     const EventDesc ev = A.ev[e];

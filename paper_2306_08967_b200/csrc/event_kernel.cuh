@@ -35,6 +35,7 @@ struct EventKernelArgs {
   int* stamp;
   int* mark;
   int* listF;
+  int* listG;   // third candidate-list buffer of the fused push (round mod 3)
   int* listL;
   const int64_t* touched;
   long long* pstats;

@@ -1,5 +1,6 @@
 """Dev profiling helper: per-event latency of the cfg2 stream with and
-without the PPR enhancer (alpha = 1 bypasses it), for kernel breakdowns."""
+without the PPR enhancer (alpha = 1 bypasses it), for kernel breakdowns.
+Phase counters need the library built with `make EXTRA=-DDAMF_PROF=1`."""
 import sys, os, time, json
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
