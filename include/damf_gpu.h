@@ -154,8 +154,12 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
                                  const double* px_host, const double* py_host,
                                  const double* sigma_host, damf_gpu** out);
 
-/* Engine(g, cfg) (engine.cpp:5-10): randomized t-SVD init on device.
- * Not yet implemented on the GPU: returns DAMF_E_UNSUPPORTED. */
+/* Engine(g, cfg) (engine.cpp:5-10): FactorState::init_from_graph
+ * (factor_state.cpp:84-102) — randomized t-SVD of the adjacency on the device
+ * (svd.cpp:47-96: l = d + 10, 4 power iterations, the reference's Gaussian
+ * stream for Omega; graphs with n <= 600 take the exact dense SVD), then
+ * the factor-based constructor. DAMF_E_ZERO_MATRIX for an empty graph,
+ * DAMF_E_UNSUPPORTED if the sketch is numerically rank-deficient. */
 int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out);
 
 void damf_gpu_destroy(damf_gpu* h);

@@ -16,6 +16,7 @@
 #include "event_kernel.cuh"
 #include "materialize.cuh"
 #include "ppr.cuh"
+#include "tsvd.cuh"
 
 using namespace dgpu;
 
@@ -466,11 +467,90 @@ void damf_gpu_destroy(damf_gpu* h) {
   delete h;
 }
 
+// Engine(g, cfg) (engine.cpp:5-10): FactorState::init_from_graph (device
+// randomized t-SVD, csrc/tsvd.cu) followed by the factor-based constructor.
 int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out) {
-  (void)g;
-  (void)cfg;
   *out = nullptr;
-  return DAMF_E_UNSUPPORTED;  // device randomized t-SVD init: SURVEY 8(f)#1
+  if (!g || !cfg || cfg->d < 1 || cfg->d > kMaxD) return DAMF_E_K_TOO_LARGE;
+  const int64_t n = g->n, arcs = g->arcs;
+  if (n <= 0 || arcs <= 0) return DAMF_E_ZERO_MATRIX;  // init_from_graph: graph has no edges
+  // host views of the CSR (inputs may be device memory)
+  std::vector<int64_t> off(n + 1);
+  std::vector<int32_t> ids(arcs);
+  std::vector<double> w(g->weights ? arcs : 0);
+  if (cudaMemcpy(off.data(), g->offsets, (n + 1) * 8, cudaMemcpyDefault) != cudaSuccess ||
+      cudaMemcpy(ids.data(), g->targets, arcs * 4, cudaMemcpyDefault) != cudaSuccess ||
+      (g->weights && cudaMemcpy(w.data(), g->weights, arcs * 8, cudaMemcpyDefault) != cudaSuccess))
+    return DAMF_E_CUDA;
+  // A^T as a CSR (the in-adjacency); symmetric graphs reuse A
+  std::vector<int64_t> toff;
+  std::vector<int32_t> tids;
+  std::vector<double> tw;
+  if (!cfg->undirected) {
+    toff.assign(n + 1, 0);
+    for (int64_t p = 0; p < arcs; ++p) toff[ids[p] + 1]++;
+    for (int64_t u = 0; u < n; ++u) toff[u + 1] += toff[u];
+    tids.resize(arcs);
+    if (g->weights) tw.resize(arcs);
+    std::vector<int64_t> fill(toff.begin(), toff.end() - 1);
+    for (int64_t u = 0; u < n; ++u)
+      for (int64_t p = off[u]; p < off[u + 1]; ++p) {
+        const int64_t at = fill[ids[p]]++;
+        tids[at] = (int32_t)u;
+        if (g->weights) tw[at] = w[p];
+      }
+  }
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return DAMF_E_CUDA;
+  std::vector<void*> tmp;
+  auto up = [&](const void* src, size_t bytes) -> void* {
+    void* p = nullptr;
+    if (!bytes) return nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    tmp.push_back(p);
+    cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, st);
+    return p;
+  };
+  TsvdGraph tg{};
+  tg.n = n;
+  tg.arcs = arcs;
+  tg.off = (const int64_t*)up(off.data(), (n + 1) * 8);
+  tg.ids = (const int32_t*)up(ids.data(), arcs * 4);
+  tg.wts = g->weights ? (const double*)up(w.data(), arcs * 8) : nullptr;
+  if (cfg->undirected) {
+    tg.toff = tg.off;
+    tg.tids = tg.ids;
+    tg.twts = tg.wts;
+  } else {
+    tg.toff = (const int64_t*)up(toff.data(), (n + 1) * 8);
+    tg.tids = (const int32_t*)up(tids.data(), arcs * 4);
+    tg.twts = g->weights ? (const double*)up(tw.data(), arcs * 8) : nullptr;
+  }
+  int status = 0;
+  TsvdResult res;
+  if (!tg.off || !tg.ids || !tg.toff || !tg.tids ||
+      tsvd_init(tg, (int)cfg->d, cfg->seed, st, nsm, &res) != cudaSuccess)
+    status = DAMF_E_CUDA;
+  else if (res.status)
+    status = res.status == 6 ? DAMF_E_ZERO_MATRIX : DAMF_E_UNSUPPORTED;
+  cudaStreamSynchronize(st);
+  for (void* p : tmp) cudaFree(p);
+  cudaStreamDestroy(st);
+  if (status) return status;
+  const int k = res.k;
+  std::vector<double> I((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) I[(size_t)i * k + i] = 1.0;
+  const float* xb = res.xb_dev ? res.xb_dev : res.xb_host.data();
+  const float* yb = res.yb_dev ? res.yb_dev : res.yb_host.data();
+  damf_csr hg{n, arcs, off.data(), ids.data(), g->weights ? w.data() : nullptr};
+  const int r = damf_gpu_create_from_factors(&hg, cfg, k, xb, yb, I.data(), I.data(),
+                                             res.sigma.data(), out);
+  if (res.xb_dev) cudaFree(res.xb_dev);
+  if (res.yb_dev) cudaFree(res.yb_dev);
+  return r;
 }
 
 int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int64_t k,

@@ -1,0 +1,528 @@
+// Device randomized truncated SVD of the adjacency: the reference's
+// FactorState::init_from_graph (factor_state.cpp:84-102) over
+// randomized_tsvd (svd.cpp:47-96), so Engine(g, cfg) starts on the GPU.
+//
+//   l = min_dim <= 600 ? min_dim : min(min_dim, d + 10)
+//   Y = A Omega, Q = qr(Y); 4 x { Q = qr(A^T Q); Q = qr(A Q) } (l < min_dim)
+//   B^T = A^T Q = Q2 R2;  R2^T = Uc S Vc^T;  U = Q Uc, V = Q2 Vc
+//   keep k = min(d, rank) columns above 1e-12 s_1;  X_b = U sqrt(S), Y_b = V sqrt(S)
+//
+// Omega is the reference's stream (mt19937_64 + Box-Muller, rng.hpp),
+// generated on the host, so the device init reproduces the reference's
+// subspace; everything else is fp64 on the device:
+//   spmm_gather_f64   y[u] = sum_{p in row u} w_p x[ids_p]   (warp per row)
+//   gram_f64          G = Y^T Y  (row tiles in shared memory, fp64 atomics)
+//   chol_f64          G = R^T R, R^-1 (one CTA)  -> CholeskyQR2
+//   tall_mm           Y <- Y M  (row tiles in shared memory; fp64 or fp32 out)
+//   jacobi_svd_f64    one-sided Jacobi (round-robin pairs, one CTA)
+// Graphs with min_dim <= 600 take the reference's exact path (l = min_dim,
+// no power iterations), which is the exact truncated SVD of A: a dense
+// one-sided Jacobi SVD of A directly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <random>
+#include <vector>
+
+#include "common.cuh"
+#include "tsvd.cuh"
+
+namespace dgpu {
+
+namespace {
+
+constexpr int TT = 256;
+
+__global__ void spmm_gather_f64(const int64_t* off, const int32_t* ids, const double* wts,
+                                int64_t n, const double* __restrict__ x, double* __restrict__ y,
+                                int l) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nw) {
+    const int64_t b = off[u], e = off[u + 1];
+    for (int c0 = 0; c0 < l; c0 += 128) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int64_t p0 = b; p0 < e; p0 += 32) {
+        const int64_t p = p0 + lane;
+        int v = 0;
+        double w = 0.0;
+        if (p < e) {
+          v = ids[p];
+          w = wts ? wts[p] : 1.0;
+        }
+        const int cnt = (int)(e - p0 < 32 ? e - p0 : 32);
+        for (int s = 0; s < cnt; ++s) {
+          const int vv = __shfl_sync(0xffffffffu, v, s);
+          const double ww = __shfl_sync(0xffffffffu, w, s);
+          const double* xr = x + (int64_t)vv * l;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int c = c0 + lane + 32 * t;
+            if (c < l) acc[t] = fma(ww, xr[c], acc[t]);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c = c0 + lane + 32 * t;
+        if (c < l) y[u * l + c] = acc[t];
+      }
+    }
+  }
+}
+
+// G[i0 + a][j0 + b] (a, b < GB; G zeroed) += sum_r Y[r][i0 + a] Y[r][j0 + b]:
+// one GB x GB block of the Gram matrix per launch, row tiles of Y staged in
+// shared memory, 16 entries per thread, fp64 atomics at the end.
+constexpr int GB = 64;
+__global__ void gram_block_f64(const double* __restrict__ Y, int64_t n, int l, double* G, int i0,
+                               int j0) {
+  extern __shared__ double sy[];  // RT x l
+  constexpr int RT = 16;
+  constexpr int PER = GB * GB / TT;
+  double acc[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) acc[q] = 0.0;
+  for (int64_t r0 = (int64_t)blockIdx.x * RT; r0 < n; r0 += (int64_t)gridDim.x * RT) {
+    const int rows = (int)(n - r0 < RT ? n - r0 : RT);
+    __syncthreads();
+    for (int x = threadIdx.x; x < RT * l; x += TT) sy[x] = x / l < rows ? Y[r0 * l + x] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * TT;
+      const int i = i0 + e / GB, j = j0 + e % GB;
+      if (i >= l || j >= l) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < RT; ++r) s = fma(sy[r * l + i], sy[r * l + j], s);
+      acc[q] += s;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = threadIdx.x + q * TT;
+    const int i = i0 + e / GB, j = j0 + e % GB;
+    if (i < l && j < l) atomicAdd(&G[i * l + j], acc[q]);
+  }
+}
+
+// G = R^T R (R upper, row-major l x l, written in place of R), Rinv = R^-1.
+// One CTA. fail = 1 when a pivot is not positive (rank-deficient sketch).
+__global__ void chol_f64(const double* G, int l, double* R, double* Rinv, int* fail) {
+  __shared__ double dj;
+  __shared__ int bad;
+  for (int x = threadIdx.x; x < l * l; x += blockDim.x) R[x] = 0.0;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  double gmax = 0.0;
+  for (int i = 0; i < l; ++i) gmax = fmax(gmax, G[i * l + i]);
+  for (int j = 0; j < l; ++j) {
+    if (threadIdx.x == 0) {
+      double s = G[j * l + j];
+      for (int i = 0; i < j; ++i) s -= R[i * l + j] * R[i * l + j];
+      if (!(s > 1e-28 * gmax)) {
+        bad = 1;
+        s = 1.0;
+      }
+      dj = sqrt(s);
+      R[j * l + j] = dj;
+    }
+    __syncthreads();
+    for (int c = j + 1 + threadIdx.x; c < l; c += blockDim.x) {
+      double s = G[j * l + c];
+      for (int i = 0; i < j; ++i) s -= R[i * l + j] * R[i * l + c];
+      R[j * l + c] = s / dj;
+    }
+    __syncthreads();
+  }
+  // R^-1 (upper): column c by back substitution, one thread per column
+  for (int c = threadIdx.x; c < l; c += blockDim.x) {
+    for (int i = l - 1; i >= 0; --i) {
+      if (i > c) {
+        Rinv[i * l + c] = 0.0;
+        continue;
+      }
+      double s = i == c ? 1.0 : 0.0;
+      for (int m = i + 1; m <= c; ++m) s -= R[i * l + m] * Rinv[m * l + c];
+      Rinv[i * l + c] = s / R[i * l + i];
+    }
+  }
+  if (threadIdx.x == 0 && bad) *fail = 1;
+}
+
+// out[r][c] = sum_m Y[r][m] M[m][c] for c < mc (M: l x mc row-major), row
+// tiles staged in shared memory (in place when out == Y and mc <= l).
+template <typename TO>
+__global__ void tall_mm(const double* Y, int64_t n, int l, const double* __restrict__ M, int mc,
+                        TO* out, int ldo) {
+  extern __shared__ double st[];  // 32 x l
+  constexpr int RT = 32;
+  for (int64_t r0 = (int64_t)blockIdx.x * RT; r0 < n; r0 += (int64_t)gridDim.x * RT) {
+    const int rows = (int)(n - r0 < RT ? n - r0 : RT);
+    __syncthreads();
+    for (int x = threadIdx.x; x < RT * l; x += TT) st[x] = x / l < rows ? Y[r0 * l + x] : 0.0;
+    __syncthreads();
+    for (int x = threadIdx.x; x < rows * mc; x += TT) {
+      const int r = x / mc, c = x % mc;
+      double s = 0.0;
+      for (int m = 0; m < l; ++m) s = fma(st[r * l + m], M[(int64_t)m * mc + c], s);
+      out[(r0 + r) * ldo + c] = (TO)s;
+    }
+  }
+}
+
+__global__ void scale_cols(double* M, int rows, int cols, const double* s) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < rows * cols; x += gridDim.x * blockDim.x)
+    M[x] *= s[x % cols];
+}
+
+__global__ void norm2_f64(const double* x, int64_t m, double* out) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s += x[i] * x[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+__global__ void dense_from_csr(const int64_t* off, const int32_t* ids, const double* wts, int n,
+                               double* A /* column-major n x n */) {
+  for (int u = blockIdx.x; u < n; u += gridDim.x)
+    for (int64_t p = off[u] + threadIdx.x; p < off[u + 1]; p += blockDim.x)
+      atomicAdd(&A[(int64_t)ids[p] * n + u], wts ? wts[p] : 1.0);  // A[u][v], column v
+}
+
+// One-sided Jacobi SVD of A (m x l, column-major): A V = U S. On exit the
+// columns of A hold U S (unsorted), V (l x l column-major) the right vectors.
+// Round-robin pairings; one warp per column pair.
+__global__ void jacobi_svd_f64(double* A, int m, int l, double* V, int* sweeps_out) {
+  __shared__ int perm[1024];
+  __shared__ double smax[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int L = (l + 1) & ~1;  // even count; index l is a dummy when l is odd
+  for (int x = threadIdx.x; x < l * l; x += blockDim.x) V[x] = (x / l == x % l) ? 1.0 : 0.0;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) perm[i] = i;
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < 40; ++sweep) {
+    double off = 0.0;
+    for (int step = 0; step < L - 1; ++step) {
+      for (int pr = warp; pr < L / 2; pr += nw) {
+        int i = perm[pr], j = perm[L - 1 - pr];
+        if (i >= l || j >= l) continue;
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+        double* ai = A + (int64_t)i * m;
+        double* aj = A + (int64_t)j * m;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = lane; r < m; r += 32) {
+          const double x = ai[r], y = aj[r];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+        off = fmax(off, fabs(ga) / sqrt(al * be));
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int r = lane; r < m; r += 32) {
+          const double x = ai[r], y = aj[r];
+          ai[r] = c * x - s * y;
+          aj[r] = s * x + c * y;
+        }
+        double* vi = V + (int64_t)i * l;
+        double* vj = V + (int64_t)j * l;
+        for (int r = lane; r < l; r += 32) {
+          const double x = vi[r], y = vj[r];
+          vi[r] = c * x - s * y;
+          vj[r] = s * x + c * y;
+        }
+      }
+      __syncthreads();
+      // rotate the tournament (position 0 fixed)
+      if (threadIdx.x == 0) {
+        const int last = perm[L - 1];
+        for (int q = L - 1; q > 1; --q) perm[q] = perm[q - 1];
+        perm[1] = last;
+      }
+      __syncthreads();
+    }
+    if (lane == 0) smax[warp] = off;
+    __syncthreads();
+    double mx = 0.0;
+    for (int w = 0; w < nw; ++w) mx = fmax(mx, smax[w]);
+    __syncthreads();
+    if (mx <= 1e-15) break;
+  }
+  if (threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+__global__ void col_norms(const double* A, int m, int l, double* s) {
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int c = warp; c < l; c += nw) {
+    double v = 0.0;
+    for (int r = lane; r < m; r += 32) v = fma(A[(int64_t)c * m + r], A[(int64_t)c * m + r], v);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s[c] = sqrt(v);
+  }
+}
+
+cudaError_t ck(cudaError_t e) { return e; }
+
+}  // namespace
+
+// reference rng.hpp: mt19937_64, rand_unit = (x >> 11) * 2^-53, Box-Muller
+// with u1 > 0 rejection, one cosine sample per pair of draws
+static void reference_gaussians(uint64_t seed, int64_t count, double* out) {
+  std::mt19937_64 rng(seed);
+  for (int64_t i = 0; i < count; ++i) {
+    double u1;
+    do {
+      u1 = (double)(rng() >> 11) * 0x1.0p-53;
+    } while (u1 <= 0.0);
+    const double u2 = (double)(rng() >> 11) * 0x1.0p-53;
+    out[i] = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+  }
+}
+
+#define TCK(x)                           \
+  do {                                   \
+    cudaError_t _e = (x);                \
+    if (_e != cudaSuccess) return _e;    \
+  } while (0)
+
+cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st, int nsm,
+                      TsvdResult* res) {
+  const int64_t n = g.n;
+  res->k = 0;
+  res->status = 0;
+  if (n <= 0 || g.arcs <= 0) {
+    res->status = 6;  // ZeroMatrix: init_from_graph: graph has no edges
+    return cudaSuccess;
+  }
+  const int64_t min_dim = n;
+  const int l = (int)(min_dim <= 600 ? min_dim : std::min<int64_t>(min_dim, d + 10));
+  std::vector<double*> tmp;
+  auto alloc = [&](double** p, size_t count) -> cudaError_t {
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(count, 1) * sizeof(double));
+    if (e == cudaSuccess) tmp.push_back(*p);
+    return e;
+  };
+  auto free_all = [&]() {
+    for (double* p : tmp) cudaFree(p);
+  };
+  int* dflag = nullptr;
+  TCK(cudaMalloc(&dflag, 2 * sizeof(int)));
+  cudaError_t err = cudaSuccess;
+  double *U = nullptr, *V = nullptr, *S = nullptr;  // device: U (n x k, row-major), V, sigma
+  int k = 0;
+  std::vector<double> hs;
+  do {
+    if (min_dim <= 600) {
+      // exact path: dense A, one-sided Jacobi: A V = U S
+      double *A = nullptr, *Vd = nullptr, *s = nullptr;
+      if ((err = alloc(&A, (size_t)n * n)) || (err = alloc(&Vd, (size_t)n * n)) ||
+          (err = alloc(&s, (size_t)n)))
+        break;
+      cudaMemsetAsync(A, 0, (size_t)n * n * 8, st);
+      dense_from_csr<<<(int)std::min<int64_t>(n, 4096), 128, 0, st>>>(g.off, g.ids, g.wts, (int)n, A);
+      jacobi_svd_f64<<<1, 512, 0, st>>>(A, (int)n, (int)n, Vd, dflag);
+      col_norms<<<32, 256, 0, st>>>(A, (int)n, (int)n, s);
+      if ((err = cudaGetLastError())) break;
+      // order by sigma on the host (n <= 600)
+      hs.resize(n);
+      std::vector<double> ha((size_t)n * n), hv((size_t)n * n);
+      cudaMemcpyAsync(hs.data(), s, n * 8, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(ha.data(), A, (size_t)n * n * 8, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(hv.data(), Vd, (size_t)n * n * 8, cudaMemcpyDeviceToHost, st);
+      if ((err = cudaStreamSynchronize(st))) break;
+      std::vector<int> ord(n);
+      for (int i = 0; i < n; ++i) ord[i] = i;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hs[a] > hs[b]; });
+      int rank = 0;
+      while (rank < n && hs[ord[rank]] > 0.0) ++rank;
+      k = std::min(d, rank);
+      const double floor_ = 1e-12 * (rank > 0 ? hs[ord[0]] : 0.0);
+      while (k > 0 && hs[ord[k - 1]] <= floor_) --k;
+      if (k == 0) {
+        res->status = 6;
+        break;
+      }
+      // X_b = U sqrt(S) = A_col / sigma * sqrt(sigma), Y_b = V sqrt(S); row-major n x k
+      std::vector<float> xb((size_t)n * k), yb((size_t)n * k);
+      res->sigma.assign(k, 0.0);
+      for (int c = 0; c < k; ++c) {
+        const int j = ord[c];
+        const double sg = hs[j], r = std::sqrt(sg);
+        res->sigma[c] = sg;
+        for (int64_t r0 = 0; r0 < n; ++r0) {
+          xb[r0 * k + c] = (float)(ha[(size_t)j * n + r0] / sg * r);
+          yb[r0 * k + c] = (float)(hv[(size_t)j * n + r0] * r);
+        }
+      }
+      res->xb_host.swap(xb);
+      res->yb_host.swap(yb);
+      res->k = k;
+      break;
+    }
+    // ---- randomized path (l < min_dim)
+    double *Y = nullptr, *Q = nullptr, *G = nullptr, *R = nullptr, *Ri = nullptr, *Racc = nullptr,
+           *Rt = nullptr, *nrm = nullptr;
+    if ((err = alloc(&Y, (size_t)n * l)) || (err = alloc(&Q, (size_t)n * l)) ||
+        (err = alloc(&G, (size_t)l * l)) || (err = alloc(&R, (size_t)l * l)) ||
+        (err = alloc(&Ri, (size_t)l * l)) || (err = alloc(&Racc, (size_t)l * l)) ||
+        (err = alloc(&Rt, (size_t)l * l)) || (err = alloc(&nrm, 1)))
+      break;
+    {
+      std::vector<double> om((size_t)n * l);
+      reference_gaussians(seed, (int64_t)n * l, om.data());
+      if ((err = cudaMemcpyAsync(Q, om.data(), (size_t)n * l * 8, cudaMemcpyHostToDevice, st))) break;
+      if ((err = cudaStreamSynchronize(st))) break;
+    }
+    const int gs = nsm * 8;
+    const size_t gram_smem = (size_t)16 * l * 8, mm_smem = (size_t)32 * l * 8;
+    cudaFuncSetAttribute(tall_mm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
+    cudaFuncSetAttribute(tall_mm<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
+    auto apply = [&](const double* x, double* y, bool transposed) {
+      const int64_t* o = transposed ? g.toff : g.off;
+      const int32_t* i = transposed ? g.tids : g.ids;
+      const double* w = transposed ? g.twts : g.wts;
+      spmm_gather_f64<<<gs, 256, 0, st>>>(o, i, w, n, x, y, l);
+    };
+    // CholeskyQR2 in place on Y (n x l); R of the factorisation into Rout
+    auto cholqr2 = [&](double* Ym, double* Rout) -> int {
+      int hf = 0;
+      for (int pass = 0; pass < 2; ++pass) {
+        cudaMemsetAsync(G, 0, (size_t)l * l * 8, st);
+        cudaMemsetAsync(dflag, 0, sizeof(int), st);
+        for (int i0 = 0; i0 < l; i0 += GB)
+          for (int j0 = 0; j0 < l; j0 += GB)
+            gram_block_f64<<<gs, TT, gram_smem, st>>>(Ym, n, l, G, i0, j0);
+        chol_f64<<<1, 256, 0, st>>>(G, l, pass == 0 ? Racc : R, Ri, dflag);
+        tall_mm<double><<<gs, TT, mm_smem, st>>>(Ym, n, l, Ri, l, Ym, l);
+        cudaMemcpyAsync(&hf, dflag, sizeof(int), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        if (hf) return 1;
+      }
+      if (Rout) {
+        // R = R_pass2 * R_pass1 (upper l x l), on the device via tall_mm
+        tall_mm<double><<<1, TT, mm_smem, st>>>(R, l, l, Racc, l, Rout, l);
+      }
+      return 0;
+    };
+    apply(Q, Y, false);  // Y = A Omega
+    cudaMemsetAsync(nrm, 0, 8, st);
+    norm2_f64<<<gs, 256, 0, st>>>(Y, (int64_t)n * l, nrm);
+    double hn = 0;
+    cudaMemcpyAsync(&hn, nrm, 8, cudaMemcpyDeviceToHost, st);
+    if ((err = cudaStreamSynchronize(st))) break;
+    if (hn == 0.0) {
+      res->status = 6;  // randomized_tsvd: all-zero matrix
+      break;
+    }
+    if (cholqr2(Y, nullptr)) {
+      res->status = 101;  // rank-deficient sketch: not supported on the device path
+      break;
+    }
+    bool bad = false;
+    for (int it = 0; it < 4 && !bad; ++it) {
+      apply(Y, Q, true);  // Q = A^T Y
+      if (cholqr2(Q, nullptr)) bad = true;
+      if (!bad) {
+        apply(Q, Y, false);  // Y = A Q
+        if (cholqr2(Y, nullptr)) bad = true;
+      }
+    }
+    if (bad) {
+      res->status = 101;
+      break;
+    }
+    // B^T = A^T Q -> Q2 R2 (Q2 in place in Q)
+    apply(Y, Q, true);
+    if (cholqr2(Q, Rt)) {
+      res->status = 101;
+      break;
+    }
+    // R2^T (l x l) column-major == R2 row-major: Jacobi on it directly
+    double *Vc = nullptr, *s = nullptr;
+    if ((err = alloc(&Vc, (size_t)l * l)) || (err = alloc(&s, (size_t)l))) break;
+    // column-major copy of R2^T: element (r, c) of R2^T = R2[c][r] -> stored at c*l + r,
+    // i.e. exactly R2's row-major layout
+    jacobi_svd_f64<<<1, 512, 0, st>>>(Rt, l, l, Vc, dflag);
+    col_norms<<<32, 256, 0, st>>>(Rt, l, l, s);
+    if ((err = cudaGetLastError())) break;
+    hs.resize(l);
+    std::vector<double> ha((size_t)l * l), hv((size_t)l * l);
+    cudaMemcpyAsync(hs.data(), s, l * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(ha.data(), Rt, (size_t)l * l * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hv.data(), Vc, (size_t)l * l * 8, cudaMemcpyDeviceToHost, st);
+    if ((err = cudaStreamSynchronize(st))) break;
+    std::vector<int> ord(l);
+    for (int i = 0; i < l; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hs[a] > hs[b]; });
+    int rank = 0;
+    while (rank < l && hs[ord[rank]] > 0.0) ++rank;
+    k = std::min(d, rank);
+    const double floor_ = 1e-12 * (rank > 0 ? hs[ord[0]] : 0.0);
+    while (k > 0 && hs[ord[k - 1]] <= floor_) --k;
+    if (k == 0) {
+      res->status = 6;
+      break;
+    }
+    // Uc (l x k) = left vectors of R2^T = columns of (A V)/s; Vc (l x k)
+    // X_b = Y Uc sqrt(S) (Y holds Q), Y_b = Q2 Vc sqrt(S) (Q holds Q2)
+    std::vector<double> fu((size_t)l * k), fv((size_t)l * k);
+    res->sigma.assign(k, 0.0);
+    for (int c = 0; c < k; ++c) {
+      const int j = ord[c];
+      const double sg = hs[j], r = std::sqrt(sg);
+      res->sigma[c] = sg;
+      for (int m = 0; m < l; ++m) {
+        fu[(size_t)m * k + c] = ha[(size_t)j * l + m] / sg * r;
+        fv[(size_t)m * k + c] = hv[(size_t)j * l + m] * r;
+      }
+    }
+    double *Fu = nullptr, *Fv = nullptr;
+    if ((err = alloc(&Fu, (size_t)l * k)) || (err = alloc(&Fv, (size_t)l * k))) break;
+    cudaMemcpyAsync(Fu, fu.data(), (size_t)l * k * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(Fv, fv.data(), (size_t)l * k * 8, cudaMemcpyHostToDevice, st);
+    float *xb = nullptr, *yb = nullptr;
+    if ((err = cudaMalloc(&xb, (size_t)n * k * 4))) break;
+    if ((err = cudaMalloc(&yb, (size_t)n * k * 4))) {
+      cudaFree(xb);
+      break;
+    }
+    tall_mm<float><<<gs, TT, mm_smem, st>>>(Y, n, l, Fu, k, xb, k);
+    tall_mm<float><<<gs, TT, mm_smem, st>>>(Q, n, l, Fv, k, yb, k);
+    if ((err = cudaStreamSynchronize(st))) {
+      cudaFree(xb);
+      cudaFree(yb);
+      break;
+    }
+    res->xb_dev = xb;
+    res->yb_dev = yb;
+    res->k = k;
+  } while (0);
+  (void)U;
+  (void)V;
+  (void)S;
+  free_all();
+  cudaFree(dflag);
+  return err;
+}
+
+}  // namespace dgpu

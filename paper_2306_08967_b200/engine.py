@@ -187,6 +187,28 @@ class Engine:
         self.d = d
         self.alpha = alpha
 
+    @classmethod
+    def from_graph(cls, n, offsets, targets, weights, d, alpha=0.3, eps=1e-5, undirected=False,
+                   rebase_cond=1e8, rebase_every=50000, seed=0, node_capacity=0, arc_capacity=0):
+        """Engine(g, cfg) (engine.cpp:5-10): factors from the device randomized
+        t-SVD of the snapshot (damf_gpu_create, FactorState::init_from_graph)."""
+        L = lib()
+        offsets = np.ascontiguousarray(offsets, np.int64)
+        targets = np.ascontiguousarray(targets, np.int32)
+        weights = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        csr = Csr(n, len(targets), _p(offsets, i64p), _p(targets, i32p), _p(weights, f64p))
+        cfg = Config(d, alpha, eps, seed, rebase_cond, rebase_every, int(undirected), 0,
+                     node_capacity, arc_capacity)
+        self = cls.__new__(cls)
+        self.h = C.c_void_p()
+        st = L.damf_gpu_create(C.byref(csr), C.byref(cfg), C.byref(self.h))
+        if st:
+            self.h = None
+            raise DamfError(st, "damf_gpu_create failed")
+        self.d = d
+        self.alpha = alpha
+        return self
+
     def close(self):
         if getattr(self, "h", None):
             lib().damf_gpu_destroy(self.h)

@@ -212,3 +212,28 @@ def test_rebase_fold_is_fp64_accurate(k):
     err = np.abs(got - truth).max(1) / np.maximum(np.abs(truth).max(1), 1e-30)
     print(f"k={k}: worst row rel err {err.max():.2e}")
     assert err.max() <= 5e-6
+
+
+@pytest.mark.parametrize("case", ["small", "cfg1"])
+def test_device_tsvd_init_matches_oracle(case):
+    # Engine(g, cfg) on the device vs the oracle's FactorState::init_from_graph
+    # (same seed, same Gaussian stream): sigma and the factor products agree.
+    if case == "small":
+        g = oracle.gen_random_graph(300, 1500, 21)          # min_dim <= 600: exact path
+        d, n = 16, 300
+    else:
+        w = W.cfg1()
+        eu, ev = w["init"]
+        n, d = w["n"], 32
+        g = oracle.Graph(n, np.concatenate([eu, ev]), np.concatenate([ev, eu]), None, True)
+    oe = oracle.OracleEngine(g, d=d, alpha=1.0, seed=5)
+    off, tgt, wts = g.csr()
+    e = ge.Engine.from_graph(n, off, tgt, None if np.all(wts == 1.0) else wts, d, alpha=1.0,
+                             undirected=g.undirected, seed=5)
+    so, sg = oe.get(oe.SIGMA), e.get(ge.SIGMA)
+    print(case, "k", len(so), len(sg), "sigma rel", sigma_rel(sg, so))
+    assert len(so) == len(sg)
+    assert sigma_rel(sg, so) <= 1e-6
+    wp = sampled_product_rel(e.get(ge.X), e.get(ge.Y), oe.get(oe.X), oe.get(oe.Y))
+    print(case, "product", wp)
+    assert wp <= 1e-4
