@@ -507,16 +507,22 @@ def bench_cfg3(args):
     su, sv = (hk >> 32).cpu().numpy(), (hk & 0xFFFFFFFF).cpu().numpy()
     edges = int(keys.numel())
     del keys, drop, hk, held
-    X, Y, s = W.tsvd_factors_device(n, off, tgt, d, seed=2)
-    gen_s = time.time() - t0
-    k = len(s)
-    eng = ge.Engine(n, off, tgt, None, d, k, X, Y, np.eye(k), np.eye(k), s, alpha=1.0,
-                    undirected=True, node_capacity=1024, arc_capacity=1 << 22)
-    del X, Y, off, tgt
+    off_h, tgt_h = off.cpu().numpy(), tgt.cpu().numpy()
+    del off, tgt
     torch.cuda.empty_cache()
+    gen_s = time.time() - t0
+    # Engine(g, cfg): the reference's init (randomized t-SVD, d + 10, 4 power
+    # iterations) on the device (damf_gpu_create)
+    t1 = time.time()
+    eng = ge.Engine.from_graph(n, off_h, tgt_h, None, d, alpha=1.0, undirected=True, seed=2,
+                               node_capacity=1024, arc_capacity=1 << 22)
+    init_s = time.time() - t1
+    del off_h, tgt_h
     ev = W.EventList.edges(ge.ADD_EDGE, su, sv)
     res = {"graph": f"R-MAT scale 22 ef 16 (n={n}, edges={edges}), d=128, alpha=1",
-           "setup_s": round(gen_s, 1)}
+           "setup_s": round(gen_s, 1),
+           "init_s": round(init_s, 1),
+           "init": "damf_gpu_create: device randomized t-SVD (l = d + 10, 4 power iterations; sketch from the device Philox stream at this size)"}
     a = 0
     for batch, m in ((1, args.cfg3_events // 4), (64, args.cfg3_events // 2),
                      (1024, args.cfg3_events)):

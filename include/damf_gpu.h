@@ -78,10 +78,18 @@ typedef struct damf_config {
   double rebase_cond;    /* rebase when cond(P_X) exceeds this (1e8)      */
   int64_t rebase_every;  /* rebase every this many events (50000)         */
   int32_t undirected;    /* DynamicGraph(n, undirected)                   */
-  int32_t flags;         /* reserved, 0                                   */
+  int32_t flags;         /* DAMF_CFG_* bits, 0 by default                 */
   int64_t node_capacity; /* rows to reserve beyond n for AddNode (0=auto) */
   int64_t arc_capacity;  /* arc slots to reserve beyond arcs (0=auto)     */
 } damf_config;
+
+/* damf_config.flags */
+enum {
+  DAMF_CFG_REFERENCE_OMEGA = 1 /* damf_gpu_create: always draw the sketch from the
+                                  reference's Gaussian stream (rng.hpp) on the host;
+                                  by default sketches above 2^26 values use a
+                                  device counter-based generator */
+};
 
 /* Out-adjacency in CSR form. Arrays may be host or device memory (detected
  * with cudaPointerGetAttributes; device arrays are consumed in place).

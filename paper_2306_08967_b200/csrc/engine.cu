@@ -532,7 +532,7 @@ int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out) {
   int status = 0;
   TsvdResult res;
   if (!tg.off || !tg.ids || !tg.toff || !tg.tids ||
-      tsvd_init(tg, (int)cfg->d, cfg->seed, st, nsm, &res) != cudaSuccess)
+      tsvd_init(tg, (int)cfg->d, cfg->seed, st, nsm, &res, (cfg->flags & DAMF_CFG_REFERENCE_OMEGA) != 0) != cudaSuccess)
     status = DAMF_E_CUDA;
   else if (res.status)
     status = res.status == 6 ? DAMF_E_ZERO_MATRIX : DAMF_E_UNSUPPORTED;

@@ -281,7 +281,32 @@ __global__ void col_norms(const double* A, int m, int l, double* s) {
   }
 }
 
-cudaError_t ck(cudaError_t e) { return e; }
+// Counter-based Gaussians for large sketches (Philox-4x32-10 + Box-Muller):
+// same distribution as the reference stream, not the same bits.
+__device__ __forceinline__ void philox(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t h0 = (uint32_t)(p0 >> 32), l0 = (uint32_t)p0, h1 = (uint32_t)(p1 >> 32),
+                   l1 = (uint32_t)p1;
+    c[0] = h1 ^ c[1] ^ k0;
+    c[1] = l1;
+    c[2] = h0 ^ c[3] ^ k1;
+    c[3] = l0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+__global__ void gaussian_fill(double* out, int64_t count, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c[4] = {(uint32_t)i, (uint32_t)(i >> 32), 0x5bd1e995u, 0u};
+    philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t a = ((uint64_t)c[0] << 32) | c[1], b = ((uint64_t)c[2] << 32) | c[3];
+    const double u1 = ((double)(a >> 11) + 0.5) * 0x1.0p-53, u2 = (double)(b >> 11) * 0x1.0p-53;
+    out[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
 
 }  // namespace
 
@@ -306,7 +331,10 @@ static void reference_gaussians(uint64_t seed, int64_t count, double* out) {
   } while (0)
 
 cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st, int nsm,
-                      TsvdResult* res) {
+                      TsvdResult* res, bool exact_stream) {
+  // sketches up to 2^26 Gaussians take the reference's stream (a few seconds on
+  // one host core); larger ones a device counter-based generator
+  constexpr int64_t kHostStreamMax = int64_t(1) << 26;
   const int64_t n = g.n;
   res->k = 0;
   res->status = 0;
@@ -387,11 +415,16 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
         (err = alloc(&Ri, (size_t)l * l)) || (err = alloc(&Racc, (size_t)l * l)) ||
         (err = alloc(&Rt, (size_t)l * l)) || (err = alloc(&nrm, 1)))
       break;
-    {
+    if (exact_stream || (int64_t)n * l <= kHostStreamMax) {
+      // the reference's own Gaussian stream (rng.hpp), sequential on the host
       std::vector<double> om((size_t)n * l);
       reference_gaussians(seed, (int64_t)n * l, om.data());
       if ((err = cudaMemcpyAsync(Q, om.data(), (size_t)n * l * 8, cudaMemcpyHostToDevice, st))) break;
       if ((err = cudaStreamSynchronize(st))) break;
+      res->omega = 0;
+    } else {
+      gaussian_fill<<<nsm * 16, 256, 0, st>>>(Q, (int64_t)n * l, seed);
+      res->omega = 1;
     }
     const int gs = nsm * 8;
     const size_t gram_smem = (size_t)16 * l * 8, mm_smem = (size_t)32 * l * 8;

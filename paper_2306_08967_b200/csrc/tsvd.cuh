@@ -21,6 +21,7 @@ struct TsvdGraph {
 struct TsvdResult {
   int k = 0;
   int status = 0;                  // 0 ok, else damf status (6 ZeroMatrix, 101 unsupported)
+  int omega = 0;                   // 0: reference Gaussian stream, 1: device Philox stream
   std::vector<double> sigma;       // k
   float* xb_dev = nullptr;         // n x k device (randomized path), caller frees
   float* yb_dev = nullptr;
@@ -29,6 +30,6 @@ struct TsvdResult {
 
 // FactorState::init_from_graph (factor_state.cpp:84-102) on the device.
 cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st, int nsm,
-                      TsvdResult* res);
+                      TsvdResult* res, bool exact_stream);
 
 }  // namespace dgpu
