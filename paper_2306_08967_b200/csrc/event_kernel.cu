@@ -60,8 +60,6 @@ constexpr int PLD = 132;           // private-matrix row stride (d <= 128 in sme
 #define DAMF_GEMM_KU 8
 #endif
 constexpr int PCAP = 2048;         // fused-PPR candidate list entries kept in shared memory
-constexpr int SCH = 16;            // rows per staged operand chunk
-constexpr int SLD = 136;           // staged row stride (doubles, 16-byte multiple, >= kMaxD/2 + 8)
 
 template <int C>
 struct Smem {
@@ -85,9 +83,6 @@ struct Smem {
   long long found[C][2];          // graph row-scan results
   int lcnt3[3];                   // fused PPR: rows in this CTA's candidate lists (round mod 3)
   int plist[3][PCAP];             // fused PPR: candidate lists (round mod 3); overflow in global
-  alignas(128) double stg[2][SCH * SLD];  // TMA-staged K-row chunks of a rows_gemm operand
-  alignas(8) unsigned long long stg_bar[2];
-  unsigned stg_n[2];              // completed waits per staging buffer (mbarrier parity)
   int K, nrot, need;
   int k, pp[2];
   int err;
@@ -324,145 +319,6 @@ DAMF_D bool gj_inverse_cta(const double* PT, double* Q, int k, int ld, double* p
     __syncthreads();
   }
   return true;
-}
-
-// Same product as rows_gemm, with the shared operand In staged through
-// shared memory by the bulk-copy engine: SCH-row chunks, double-buffered on
-// two mbarriers, one thread issues one cp.async.bulk per row (no register
-// cost), so the next chunk streams while the tensor cores consume this one.
-// rows_gemm pays one dependent L2 round trip per 32 K-values per warp; this
-// path pays ~one for the whole product. In rows must be 16-byte aligned
-// (ldi * 8 % 16 == 0) and J <= 2 * (SLD - 4).
-DAMF_D uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-template <int C>
-DAMF_D void stage_chunk(Smem<C>& S, int b, const double* In, int ldi, int r0, int rows, int Jc) {
-  const uint32_t bar = smem_addr(&S.stg_bar[b]);
-  const uint32_t bytes = (uint32_t)Jc * 8;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * rows)
-               : "memory");
-  for (int r = 0; r < rows; ++r)
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(&S.stg[b][r * SLD])),
-        "l"(In + (int64_t)(r0 + r) * ldi), "r"(bytes), "r"(bar)
-        : "memory");
-}
-
-template <int C>
-DAMF_D void stage_wait(Smem<C>& S, int b) {
-  const uint32_t bar = smem_addr(&S.stg_bar[b]);
-  const uint32_t par = S.stg_n[b] & 1u;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "W_STG:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W_STG;\n\t}" ::"r"(bar),
-      "r"(par)
-      : "memory");
-}
-
-template <int C>
-DAMF_D void rows_gemm_staged(Smem<C>& S, double* Out, int ldo, int o0, const double* Coef, int ldc,
-                             int nt, const double* __restrict__ In, int ldi, int M, int J,
-                             double* fro) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ar = lane >> 2, ac = lane & 3;
-  const int Jc = (J + 1) & ~1;  // 16-byte multiple
-  const int nch = (M + SCH - 1) / SCH;
-  const int ntiles = (J + 7) >> 3;
-  // operand rows written by other CTAs (generic proxy) before the caller's
-  // cluster barrier; order them before the async-proxy reads
-  __syncthreads();
-  if (tid == 0) {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    stage_chunk(S, 0, In, ldi, 0, min(SCH, M), Jc);
-    if (nch > 1) stage_chunk(S, 1, In, ldi, SCH, min(SCH, M - SCH), Jc);
-  }
-  double frob = 0.0;
-  // each warp owns n8 tiles tb = warp, warp + NW (<= 2 per warp at J <= 128,
-  // 3 at J <= 192, ...) and m8 tiles of the nt (<= 16) output rows
-  constexpr int TPM = 4;
-  double d0[TPM][2], d1[TPM][2];
-#pragma unroll
-  for (int p = 0; p < TPM; ++p) d0[p][0] = d0[p][1] = d1[p][0] = d1[p][1] = 0.0;
-  const int mt = (nt + 7) >> 3;
-  for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    stage_wait(S, b);
-    const double* buf = S.stg[b];
-    const int rows = min(SCH, M - c * SCH);
-#pragma unroll
-    for (int q = 0; q < SCH / 4; ++q) {
-      const int kk = 4 * q + ac;  // row within the chunk
-      const int m = c * SCH + kk;
-      double a[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = 8 * h + ar;
-        a[h] = (h < mt && r < nt && kk < rows) ? Coef[(int64_t)r * ldc + m] : 0.0;
-      }
-#pragma unroll
-      for (int p = 0; p < TPM; ++p) {
-        const int tb = warp + p * NW;
-        if (tb >= ntiles) break;
-        const int bc = (tb << 3) + ar;
-        const double bv = (kk < rows && bc < J) ? buf[kk * SLD + bc] : 0.0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (h < mt) dmma(d0[p][h], d1[p][h], a[h], bv);
-      }
-    }
-    __syncthreads();  // every warp is done with buffer b
-    if (tid == 0) {
-      S.stg_n[b] += 1;
-      if (c + 2 < nch) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        stage_chunk(S, b, In, ldi, (c + 2) * SCH, min(SCH, M - (c + 2) * SCH), Jc);
-      }
-    }
-    __syncthreads();  // stg_n visible before the next wait
-  }
-#pragma unroll
-  for (int p = 0; p < TPM; ++p) {
-    const int tb = warp + p * NW;
-    if (tb >= ntiles) break;
-    const int col = (tb << 3) + 2 * ac;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = 8 * h + ar;
-      if (h < mt && r < nt) {
-        if (col < J) {
-          Out[(int64_t)(o0 + r) * ldo + col] = d0[p][h];
-          frob += d0[p][h] * d0[p][h];
-        }
-        if (col + 1 < J) {
-          Out[(int64_t)(o0 + r) * ldo + col + 1] = d1[p][h];
-          frob += d1[p][h] * d1[p][h];
-        }
-      }
-    }
-  }
-  if (fro) *fro = block_sum(S, frob);
-  __syncthreads();
-}
-
-// rows_gemm over the staged path in chunks of 16 output rows.
-template <int C>
-DAMF_D void rows_gemm_s(Smem<C>& S, double* Out, int ldo, int o0, const double* Coef, int ldc,
-                        int nt, const double* __restrict__ In, int ldi, int M, int J, double* fro) {
-  if (J > SLD || J > 8 * NW * 4 || ((ldi * 8) & 15) || (reinterpret_cast<uintptr_t>(In) & 15)) {
-    rows_gemm<C>(S, Out, ldo, o0, Coef, ldc, nt, In, ldi, M, J, fro);
-    return;
-  }
-  double total = 0.0;
-  for (int c = 0; c < nt; c += 16) {
-    double f = 0.0;
-    rows_gemm_staged<C>(S, Out, ldo, o0 + c, Coef + (int64_t)c * ldc, ldc, min(16, nt - c), In, ldi,
-                        M, J, fro ? &f : nullptr);
-    total += f;
-  }
-  if (fro) *fro = total;
 }
 
 // ------------------------------------------------------------ secular solver
@@ -1723,11 +1579,6 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     S.pp[0] = A.ctl->pp[0];
     S.pp[1] = A.ctl->pp[1];
     for (int i = 0; i < 3; ++i) S.lcnt3[i] = 0;  // fused-PPR counters
-    for (int b = 0; b < 2; ++b) {
-      S.stg_n[b] = 0;
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&S.stg_bar[b])));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   cl.sync();  // counters zeroed before any CTA can append to them

@@ -287,31 +287,6 @@ def cfg4_F(d, seed):
     return q * rng.uniform(0.5, 2.0, size=d)[None, :]
 
 
-def tsvd_factors(n, offsets, targets, d, seed=0, oversample=10, power=4):
-    """Randomized truncated SVD of the adjacency (the reference's init,
-    svd.cpp:47-96, with l = d + oversample) computed with numpy/scipy on the
-    host: X_b = U sqrt(S), Y_b = V sqrt(S), P = I. Used to seed both the GPU
-    engine and the oracle with identical factors."""
-    import scipy.sparse as sp
-    src, dst = csr_arcs(offsets, targets)
-    A = sp.csr_matrix((np.ones(len(src)), (src, dst)), shape=(n, n))
-    rng = np.random.Generator(np.random.PCG64(seed))
-    l = min(n, d + oversample)
-    Y = A @ rng.standard_normal((n, l))
-    Q, _ = np.linalg.qr(Y)
-    for _ in range(power):
-        Q, _ = np.linalg.qr(A.T @ Q)
-        Q, _ = np.linalg.qr(A @ Q)
-    Bt = A.T @ Q
-    Q2, R2 = np.linalg.qr(Bt)
-    Uc, s, Vct = np.linalg.svd(R2.T)
-    k = min(d, int((s > 1e-12 * s[0]).sum()))
-    U = Q @ Uc[:, :k]
-    V = Q2 @ Vct.T[:, :k]
-    s = s[:k]
-    return U * np.sqrt(s), V * np.sqrt(s), s
-
-
 # ------------------------------------------------ device builders (cfg 3-5)
 def csr_from_keys_device(n, keys, drop=None):
     """Symmetric CSR (offsets int64, targets int32; rows sorted) as CUDA
@@ -384,32 +359,3 @@ def degree_proportional_inserts(keys, tgt, m, seed):
             if len(out_u) == m:
                 break
     return np.array(out_u, np.int64), np.array(out_v, np.int64)
-
-
-def tsvd_factors_device(n, off, tgt, d, seed=0, oversample=10, power=4):
-    """Randomized truncated SVD of the symmetric adjacency on the GPU
-    (torch / cuSPARSE; the reference's init rule, svd.cpp:47-96) used to set
-    up the cfg-3 state for the bench: X_b = U sqrt(S), Y_b = V sqrt(S)."""
-    import torch
-    A = torch.sparse_csr_tensor(off, tgt.long(), torch.ones(tgt.numel(), device="cuda"),
-                                size=(n, n))
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(seed)
-    l = min(n, d + oversample)
-
-    def orth(y):
-        q, _ = torch.linalg.qr(y)
-        return q
-
-    Q = orth(A @ torch.randn(n, l, generator=gen, device="cuda"))
-    for _ in range(power):
-        Q = orth(A @ Q)  # A symmetric: A^T Q == A Q
-        Q = orth(A @ Q)
-    Bt = A @ Q
-    Q2, R2 = torch.linalg.qr(Bt)
-    Uc, s, Vct = torch.linalg.svd(R2.T.double())
-    k = min(d, int((s > 1e-12 * s[0]).sum()))
-    sq = torch.sqrt(s[:k])
-    X = (Q.double() @ Uc[:, :k] * sq).float()
-    Y = (Q2.double() @ Vct.T[:, :k] * sq).float()
-    return X.contiguous(), Y.contiguous(), s[:k].cpu().numpy()

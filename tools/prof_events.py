@@ -12,9 +12,8 @@ alphas = [float(a) for a in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1
 d = bench.build_cfg2()
 w = d["w"]
 for alpha in alphas:
-    k = len(d["sig"])
-    e = ge.Engine(d["n"], d["off"], d["tgt"], None, w["d"], k, d["xb"], d["yb"], np.eye(k), np.eye(k),
-                  d["sig"], alpha=alpha, eps=w["eps"], undirected=True, node_capacity=4096)
+    e = ge.Engine.from_graph(d["n"], d["off"], d["tgt"], None, w["d"], alpha=alpha, eps=w["eps"],
+                             undirected=True, seed=0, node_capacity=4096)
     s = w["stream"]
     e.apply(s.slice(0, 50))
     t0 = time.perf_counter()

@@ -25,8 +25,8 @@ elif mode == "ppr":
     print(e.ppr_init())
 elif mode == "events":
     import bench
-    dd = bench.build_cfg2(); w = dd["w"]; k = len(dd["sig"])
-    e = ge.Engine(dd["n"], dd["off"], dd["tgt"], None, 128, k, dd["xb"], dd["yb"], np.eye(k), np.eye(k),
-                  dd["sig"], alpha=0.15, eps=1e-5, undirected=True, node_capacity=4096)
+    dd = bench.build_cfg2(); w = dd["w"]
+    e = ge.Engine.from_graph(dd["n"], dd["off"], dd["tgt"], None, 128, alpha=0.15, eps=1e-5,
+                             undirected=True, seed=0, node_capacity=4096)
     e.apply(w["stream"].slice(0, 50))
     print(e.apply(w["stream"].slice(50, 250)))
