@@ -35,6 +35,9 @@ namespace {
 
 constexpr int TT = 256;
 
+// y[u] = sum_p w_p x[ids_p]: warp per row, NV column values per lane (one
+// pass over the row for l <= 32 NV), 4 neighbour rows in flight.
+template <int NV>
 __global__ void spmm_gather_f64(const int64_t* off, const int32_t* ids, const double* wts,
                                 int64_t n, const double* __restrict__ x, double* __restrict__ y,
                                 int l) {
@@ -43,71 +46,86 @@ __global__ void spmm_gather_f64(const int64_t* off, const int32_t* ids, const do
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u = warp; u < n; u += nw) {
     const int64_t b = off[u], e = off[u + 1];
-    for (int c0 = 0; c0 < l; c0 += 128) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int64_t p0 = b; p0 < e; p0 += 32) {
-        const int64_t p = p0 + lane;
-        int v = 0;
-        double w = 0.0;
-        if (p < e) {
-          v = ids[p];
-          w = wts ? wts[p] : 1.0;
-        }
-        const int cnt = (int)(e - p0 < 32 ? e - p0 : 32);
-        for (int s = 0; s < cnt; ++s) {
-          const int vv = __shfl_sync(0xffffffffu, v, s);
-          const double ww = __shfl_sync(0xffffffffu, w, s);
+    double acc[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = 0.0;
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+      const int64_t p = p0 + lane;
+      int v = 0;
+      double w = 0.0;
+      if (p < e) {
+        v = ids[p];
+        w = wts ? wts[p] : 1.0;
+      }
+      const int cnt = (int)(e - p0 < 32 ? e - p0 : 32);
+      for (int s0 = 0; s0 < cnt; s0 += 4) {
+        double xv[4][NV];
+        double ww[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int src = s0 + h < cnt ? s0 + h : 0;
+          const int vv = __shfl_sync(0xffffffffu, v, src);
+          ww[h] = s0 + h < cnt ? __shfl_sync(0xffffffffu, w, src) : 0.0;
           const double* xr = x + (int64_t)vv * l;
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int c = c0 + lane + 32 * t;
-            if (c < l) acc[t] = fma(ww, xr[c], acc[t]);
+          for (int t = 0; t < NV; ++t) {
+            const int c = lane + 32 * t;
+            xv[h][t] = c < l ? xr[c] : 0.0;
           }
         }
-      }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int c = c0 + lane + 32 * t;
-        if (c < l) y[u * l + c] = acc[t];
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+          for (int t = 0; t < NV; ++t) acc[t] = fma(ww[h], xv[h][t], acc[t]);
       }
+    }
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      const int c = lane + 32 * t;
+      if (c < l) y[u * l + c] = acc[t];
     }
   }
 }
 
 // G[i0 + a][j0 + b] (a, b < GB; G zeroed) += sum_r Y[r][i0 + a] Y[r][j0 + b]:
 // one GB x GB block of the Gram matrix per launch, row tiles of Y staged in
-// shared memory, 16 entries per thread, fp64 atomics at the end.
+// shared memory, a 4 x 4 register block of G per thread, fp64 atomics at the
+// end.
 constexpr int GB = 64;
 __global__ void gram_block_f64(const double* __restrict__ Y, int64_t n, int l, double* G, int i0,
                                int j0) {
   extern __shared__ double sy[];  // RT x l
-  constexpr int RT = 16;
-  constexpr int PER = GB * GB / TT;
-  double acc[PER];
+  constexpr int RT = 32;
+  const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;
+  const int ib = i0 + 4 * ti, jb = j0 + 4 * tj;
+  double acc[4][4];
 #pragma unroll
-  for (int q = 0; q < PER; ++q) acc[q] = 0.0;
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
   for (int64_t r0 = (int64_t)blockIdx.x * RT; r0 < n; r0 += (int64_t)gridDim.x * RT) {
     const int rows = (int)(n - r0 < RT ? n - r0 : RT);
     __syncthreads();
     for (int x = threadIdx.x; x < RT * l; x += TT) sy[x] = x / l < rows ? Y[r0 * l + x] : 0.0;
     __syncthreads();
+    for (int r = 0; r < RT; ++r) {
+      double yi[4], yj[4];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = threadIdx.x + q * TT;
-      const int i = i0 + e / GB, j = j0 + e % GB;
-      if (i >= l || j >= l) continue;
-      double s = 0.0;
+      for (int a = 0; a < 4; ++a) {
+        yi[a] = ib + a < l ? sy[r * l + ib + a] : 0.0;
+        yj[a] = jb + a < l ? sy[r * l + jb + a] : 0.0;
+      }
 #pragma unroll
-      for (int r = 0; r < RT; ++r) s = fma(sy[r * l + i], sy[r * l + j], s);
-      acc[q] += s;
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(yi[a], yj[b], acc[a][b]);
     }
   }
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int e = threadIdx.x + q * TT;
-    const int i = i0 + e / GB, j = j0 + e % GB;
-    if (i < l && j < l) atomicAdd(&G[i * l + j], acc[q]);
-  }
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (ib + a < l && jb + b < l) atomicAdd(&G[(ib + a) * l + jb + b], acc[a][b]);
 }
 
 // G = R^T R (R upper, row-major l x l, written in place of R), Rinv = R^-1.
@@ -155,22 +173,44 @@ __global__ void chol_f64(const double* G, int l, double* R, double* Rinv, int* f
 }
 
 // out[r][c] = sum_m Y[r][m] M[m][c] for c < mc (M: l x mc row-major), row
-// tiles staged in shared memory (in place when out == Y and mc <= l).
+// tiles staged in shared memory (in place when out == Y and mc <= l); each
+// thread computes a 4 x 4 output block per pass.
 template <typename TO>
 __global__ void tall_mm(const double* Y, int64_t n, int l, const double* __restrict__ M, int mc,
                         TO* out, int ldo) {
-  extern __shared__ double st[];  // 32 x l
-  constexpr int RT = 32;
+  extern __shared__ double st[];  // 64 x l
+  constexpr int RT = 64;
+  const int cb = (mc + 3) / 4;      // 4-column groups
+  const int nblk = (RT / 4) * cb;   // 4x4 blocks per tile
   for (int64_t r0 = (int64_t)blockIdx.x * RT; r0 < n; r0 += (int64_t)gridDim.x * RT) {
     const int rows = (int)(n - r0 < RT ? n - r0 : RT);
     __syncthreads();
     for (int x = threadIdx.x; x < RT * l; x += TT) st[x] = x / l < rows ? Y[r0 * l + x] : 0.0;
     __syncthreads();
-    for (int x = threadIdx.x; x < rows * mc; x += TT) {
-      const int r = x / mc, c = x % mc;
-      double s = 0.0;
-      for (int m = 0; m < l; ++m) s = fma(st[r * l + m], M[(int64_t)m * mc + c], s);
-      out[(r0 + r) * ldo + c] = (TO)s;
+    for (int bidx = threadIdx.x; bidx < nblk; bidx += TT) {
+      const int rb = 4 * (bidx / cb), c0 = 4 * (bidx % cb);
+      if (rb >= rows) continue;
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int m = 0; m < l; ++m) {
+        double ya[4], mb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) ya[a] = st[(rb + a) * l + m];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) mb[b] = c0 + b < mc ? __ldg(M + (int64_t)m * mc + c0 + b) : 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(ya[a], mb[b], acc[a][b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (rb + a < rows && c0 + b < mc) out[(r0 + rb + a) * ldo + c0 + b] = (TO)acc[a][b];
     }
   }
 }
@@ -427,14 +467,18 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
       res->omega = 1;
     }
     const int gs = nsm * 8;
-    const size_t gram_smem = (size_t)16 * l * 8, mm_smem = (size_t)32 * l * 8;
+    const size_t gram_smem = (size_t)32 * l * 8, mm_smem = (size_t)64 * l * 8;
     cudaFuncSetAttribute(tall_mm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
+    cudaFuncSetAttribute(gram_block_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem);
     cudaFuncSetAttribute(tall_mm<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
     auto apply = [&](const double* x, double* y, bool transposed) {
       const int64_t* o = transposed ? g.toff : g.off;
       const int32_t* i = transposed ? g.tids : g.ids;
       const double* w = transposed ? g.twts : g.wts;
-      spmm_gather_f64<<<gs, 256, 0, st>>>(o, i, w, n, x, y, l);
+      if (l <= 160)
+        spmm_gather_f64<5><<<gs, 256, 0, st>>>(o, i, w, n, x, y, l);
+      else
+        spmm_gather_f64<9><<<gs, 256, 0, st>>>(o, i, w, n, x, y, l);
     };
     // CholeskyQR2 in place on Y (n x l); R of the factorisation into Rout
     auto cholqr2 = [&](double* Ym, double* Rout) -> int {
