@@ -6,7 +6,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -diag-suppress 177 $(EXTRA)
 PKG       := paper_2306_08967_b200
 CSRC      := $(PKG)/csrc
-CU        := $(CSRC)/event_kernel.cu $(CSRC)/materialize.cu $(CSRC)/materialize_tc.cu $(CSRC)/ppr.cu $(CSRC)/tsvd.cu $(CSRC)/engine.cu
+CU        := $(CSRC)/event_kernel.cu $(CSRC)/materialize.cu $(CSRC)/materialize_tc.cu $(CSRC)/ppr.cu $(CSRC)/tsvd.cu $(CSRC)/score.cu $(CSRC)/engine.cu
 OBJ       := $(patsubst $(CSRC)/%.cu,build/obj/%.o,$(CU))
 LIB       := $(PKG)/libdamf_gpu.so
 ORACLE    := oracle/build/libdamf_oracle.so

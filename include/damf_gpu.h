@@ -180,6 +180,21 @@ int damf_gpu_sync(damf_gpu* h);
 int damf_gpu_apply(damf_gpu* h, const damf_event_batch* batch, int32_t mode,
                    damf_apply_stats* stats);
 
+/* Batched scoring. flags: DAMF_SCORE_ENHANCED scores
+ * <Z[u], Y[v]> instead of <X[u], Y[v]> (Engine::score, engine.cpp:49-52);
+ * DAMF_SCORE_SYMMETRIC_MAX takes max(s(u,v), s(v,u)) as pair_score does for
+ * undirected graphs (eval.cpp:211-215). u, v, out: host arrays of m. */
+enum { DAMF_SCORE_ENHANCED = 1, DAMF_SCORE_SYMMETRIC_MAX = 2 };
+int damf_gpu_score_pairs(damf_gpu* h, const int64_t* u, const int64_t* v, int64_t m,
+                         int32_t flags, double* out);
+
+/* The K best pairs of (u[i], v[i]) by score descending, pair index ascending
+ * on ties (run_graph_reconstruction's heap order, eval.cpp:336-371): writes
+ * min(K, m) indices into idx_out (host or device) and their scores into
+ * score_out (may be NULL). */
+int damf_gpu_topk_pairs(damf_gpu* h, const int64_t* u, const int64_t* v, int64_t m,
+                        int32_t flags, int64_t K, int64_t* idx_out, double* score_out);
+
 /* FactorState(xb, yb, ...) row by row: copy m rows (m x k fp32, host or
  * device memory) into X_b (which = DAMF_XB) or Y_b (DAMF_YB) starting at
  * row0. Lets a caller build huge states (config 5: 34 GB per factor) in

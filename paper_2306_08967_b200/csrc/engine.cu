@@ -16,6 +16,7 @@
 #include "event_kernel.cuh"
 #include "materialize.cuh"
 #include "ppr.cuh"
+#include "score.cuh"
 #include "tsvd.cuh"
 
 using namespace dgpu;
@@ -1268,6 +1269,66 @@ int damf_gpu_query_rows(damf_gpu* h, int32_t which, const int64_t* ids, int64_t 
   cudaFree(dids);
   cudaFree(dout);
   return 0;
+}
+
+// pair_score over a batch (eval.cpp:211-215) and the top-K of a pair set
+// (eval.cpp:336-371). ids: host arrays. flags: DAMF_SCORE_*.
+namespace {
+int score_batch(damf_gpu* h, const int64_t* u, const int64_t* v, int64_t m, int32_t flags,
+                double** dscores) {
+  if (int r = sync_ctl(h)) return r;
+  for (int64_t q = 0; q < m; ++q)
+    if (u[q] < 0 || u[q] >= h->n || v[q] < 0 || v[q] >= h->n)
+      return fail(h, DAMF_E_UNKNOWN_NODE, "score: unknown node");
+  const int k = h->k;
+  float *A = nullptr, *B = nullptr;
+  int64_t *du = nullptr, *dv = nullptr;
+  CK(cudaMalloc(&A, (size_t)std::max<int64_t>(h->n, 1) * k * 4));
+  CK(cudaMalloc(&B, (size_t)std::max<int64_t>(h->n, 1) * k * 4));
+  CK(cudaMalloc(&du, std::max<int64_t>(m, 1) * 8));
+  CK(cudaMalloc(&dv, std::max<int64_t>(m, 1) * 8));
+  CK(cudaMalloc(dscores, std::max<int64_t>(m, 1) * 8));
+  int r = damf_gpu_materialize(h, (flags & DAMF_SCORE_ENHANCED) ? DAMF_Z : DAMF_X, A, 1);
+  if (!r) r = damf_gpu_materialize(h, DAMF_Y, B, 1);
+  if (!r) {
+    CK(cudaMemcpyAsync(du, u, m * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(dv, v, m * 8, cudaMemcpyHostToDevice, h->st));
+    CK(launch_pair_scores(A, B, k, du, dv, m, (flags & DAMF_SCORE_SYMMETRIC_MAX) ? 1 : 0, *dscores,
+                          h->st, h->nsm));
+    CK(cudaStreamSynchronize(h->st));
+    h->launches += 3;
+  }
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(du);
+  cudaFree(dv);
+  return r;
+}
+}  // namespace
+
+int damf_gpu_score_pairs(damf_gpu* h, const int64_t* u, const int64_t* v, int64_t m, int32_t flags,
+                         double* out) {
+  if (!h) return DAMF_E_SHAPE_MISMATCH;
+  if (m <= 0) return 0;
+  double* ds = nullptr;
+  int r = score_batch(h, u, v, m, flags, &ds);
+  if (!r) CK(cudaMemcpy(out, ds, m * 8, cudaMemcpyDeviceToHost));
+  if (ds) cudaFree(ds);
+  return r;
+}
+
+int damf_gpu_topk_pairs(damf_gpu* h, const int64_t* u, const int64_t* v, int64_t m, int32_t flags,
+                        int64_t K, int64_t* idx_out, double* score_out) {
+  if (!h) return DAMF_E_SHAPE_MISMATCH;
+  if (m <= 0 || K <= 0) return 0;
+  double* ds = nullptr;
+  int r = score_batch(h, u, v, m, flags, &ds);
+  if (!r) {
+    CK(topk_indices(ds, m, K, idx_out, score_out, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
+  if (ds) cudaFree(ds);
+  return r;
 }
 
 int damf_gpu_score(damf_gpu* h, int64_t u, int64_t v, int32_t enhanced, double* out) {

@@ -101,6 +101,9 @@ def lib():
         L.damf_gpu_event_latencies.restype = C.c_int64
         L.damf_gpu_query_rows.argtypes = [vp, C.c_int32, i64p, C.c_int64, f32p]
         L.damf_gpu_load_rows.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, vp]
+        L.damf_gpu_score_pairs.argtypes = [vp, i64p, i64p, C.c_int64, C.c_int32, f64p]
+        L.damf_gpu_topk_pairs.argtypes = [vp, i64p, i64p, C.c_int64, C.c_int32, C.c_int64, i64p,
+                                          f64p]
         L.damf_gpu_ppr_trace.argtypes = [vp, vp, C.c_int]
         L.damf_gpu_score.argtypes = [vp, C.c_int64, C.c_int64, C.c_int32, f64p]
         L.damf_gpu_materialize.argtypes = [vp, C.c_int32, vp, C.c_int32]
@@ -274,6 +277,29 @@ class Engine:
             m, ptr = keep.shape[0], keep.ctypes.data
         self._check(lib().damf_gpu_load_rows(self.h, which, row0, m, C.c_void_p(ptr)))
         del keep
+
+    def score_pairs(self, u, v, enhanced=True, symmetric_max=False):
+        """pair_score over a batch (eval.cpp:211-215), fp64 scores."""
+        u = np.ascontiguousarray(u, np.int64)
+        v = np.ascontiguousarray(v, np.int64)
+        out = np.zeros(len(u))
+        flags = (1 if enhanced else 0) | (2 if symmetric_max else 0)
+        self._check(lib().damf_gpu_score_pairs(self.h, _p(u, i64p), _p(v, i64p), len(u), flags,
+                                               _p(out, f64p)))
+        return out
+
+    def topk_pairs(self, u, v, K, enhanced=True, symmetric_max=False):
+        """Indices and scores of the K best pairs (score desc, index asc),
+        run_graph_reconstruction's order (eval.cpp:336-371)."""
+        u = np.ascontiguousarray(u, np.int64)
+        v = np.ascontiguousarray(v, np.int64)
+        kk = min(K, len(u))
+        idx = np.zeros(kk, np.int64)
+        sc = np.zeros(kk)
+        flags = (1 if enhanced else 0) | (2 if symmetric_max else 0)
+        self._check(lib().damf_gpu_topk_pairs(self.h, _p(u, i64p), _p(v, i64p), len(u), flags, K,
+                                              _p(idx, i64p), _p(sc, f64p)))
+        return idx, sc
 
     def query(self, which, ids):
         ids = np.ascontiguousarray(ids, np.int64)

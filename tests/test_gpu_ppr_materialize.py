@@ -163,3 +163,32 @@ def test_large_graph_per_event_push_keeps_defect_bound():
     assert worst <= 1e-4 * (1 + 1e-3)
     e.close()
     torch.cuda.empty_cache()
+
+
+def test_batched_scores_and_topk_match_oracle():
+    # pair_score (eval.cpp:211-215) over a batch and the reconstruction top-K
+    # order (eval.cpp:336-371) against the oracle's Engine::score
+    g = oracle.gen_random_graph(400, 2400, 31, undirected=True)
+    oe = oracle.OracleEngine(g, d=16, alpha=0.3, eps=1e-6, seed=31)
+    e = gpu_from_oracle(g, oe, d=16, alpha=0.3, eps=1e-6)
+    rng = np.random.default_rng(3)
+    u = rng.integers(0, g.n, 3000)
+    v = rng.integers(0, g.n, 3000)
+    for enh in (True, False):
+        s = e.score_pairs(u, v, enhanced=enh, symmetric_max=True)
+        ref = np.array([max(oe.score(int(a), int(b), enh), oe.score(int(b), int(a), enh))
+                        for a, b in zip(u, v)])
+        err = np.abs(s - ref).max() / np.abs(ref).max()
+        print("enhanced" if enh else "plain", "max rel score err", err)
+        assert err <= 1e-5
+    K = 100
+    idx, sc = e.topk_pairs(u, v, K, enhanced=True, symmetric_max=True)
+    s = e.score_pairs(u, v, enhanced=True, symmetric_max=True)
+    order = np.lexsort((np.arange(len(s)), -s))[:K]
+    assert np.array_equal(idx, order) and np.allclose(sc, s[order])
+    ref = np.array([max(oe.score(int(a), int(b), True), oe.score(int(b), int(a), True))
+                    for a, b in zip(u, v)])
+    ref_top = set(np.lexsort((np.arange(len(ref)), -ref))[:K].tolist())
+    overlap = len(ref_top & set(idx.tolist())) / K
+    print("top-K overlap with the oracle", overlap)
+    assert overlap >= 0.97
