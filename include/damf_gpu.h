@@ -195,6 +195,13 @@ int damf_gpu_score_pairs(damf_gpu* h, const int64_t* u, const int64_t* v, int64_
 int damf_gpu_topk_pairs(damf_gpu* h, const int64_t* u, const int64_t* v, int64_t m,
                         int32_t flags, int64_t K, int64_t* idx_out, double* score_out);
 
+/* State persistence in the reference's DAMF v1 binary format (io.cpp:182-264:
+ * save_state / load_state). Files are interchangeable with the reference.
+ * load: `sizing` (may be NULL) supplies node/arc headroom and flags; the
+ * RunConfig comes from the file. */
+int damf_gpu_save_state(damf_gpu* h, const char* path);
+int damf_gpu_load_state(const char* path, const damf_config* sizing, damf_gpu** out);
+
 /* FactorState(xb, yb, ...) row by row: copy m rows (m x k fp32, host or
  * device memory) into X_b (which = DAMF_XB) or Y_b (DAMF_YB) starting at
  * row0. Lets a caller build huge states (config 5: 34 GB per factor) in

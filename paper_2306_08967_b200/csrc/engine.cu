@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -554,6 +555,8 @@ int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out) {
   return r;
 }
 
+static thread_local bool t_skip_ppr_init = false;  // load_state supplies Z_b / r_b
+
 int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int64_t k,
                                  const float* xb, const float* yb, const double* px,
                                  const double* py, const double* sigma, damf_gpu** outp) {
@@ -820,7 +823,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   }
   CK(cudaStreamSynchronize(h->st));
   *outp = h;
-  if (!h->alpha1) {
+  if (!h->alpha1 && !t_skip_ppr_init) {
     damf_apply_stats s{};
     int r = damf_gpu_ppr_init(h, &s);
     if (r) {
@@ -1455,6 +1458,206 @@ int damf_gpu_get_graph(damf_gpu* h, int64_t* offsets, int32_t* targets, double* 
     pos += cnt[u];
   }
   if (offsets) offsets[n] = pos;
+  return 0;
+}
+
+// ---- state persistence: the reference's DAMF v1 binary (io.cpp:182-264) --
+// magic "DAMF", u32 version 1, RunConfig, u64 events_applied, i64
+// events_since_rebase, sigma (i64 n + f64), X_b, Y_b, P_X, P_Y, Z_b, r_b
+// (i64 rows, i64 cols, f64 column-major), then the out-adjacency (i64 n; per
+// node i64 count and (i64 v, f64 w) pairs). Files written here load in the
+// reference and vice versa (fp32 rows round-trip through fp64 exactly).
+}  // extern "C"
+namespace {
+template <typename T>
+void putv(std::FILE* f, T v) {
+  std::fwrite(&v, sizeof(T), 1, f);
+}
+template <typename T>
+bool getv(std::FILE* f, T* v) {
+  return std::fread(v, sizeof(T), 1, f) == 1;
+}
+void put_rows(std::FILE* f, const std::vector<float>& rm, int64_t n, int64_t k) {
+  putv<int64_t>(f, n);
+  putv<int64_t>(f, k);
+  std::vector<double> col((size_t)n);
+  for (int64_t j = 0; j < k; ++j) {
+    for (int64_t i = 0; i < n; ++i) col[i] = rm[(size_t)i * k + j];
+    std::fwrite(col.data(), 8, (size_t)n, f);
+  }
+}
+bool get_matrix(std::FILE* f, int64_t* r, int64_t* c, std::vector<double>* colmajor) {
+  if (!getv(f, r) || !getv(f, c) || *r < 0 || *c < 0) return false;
+  colmajor->resize((size_t)(*r * *c));
+  return (size_t)(*r * *c) == 0 ||
+         std::fread(colmajor->data(), 8, (size_t)(*r * *c), f) == (size_t)(*r * *c);
+}
+}  // namespace
+extern "C" {
+
+int damf_gpu_save_state(damf_gpu* h, const char* path) {
+  if (!h) return DAMF_E_SHAPE_MISMATCH;
+  if (int r = sync_ctl(h)) return r;
+  const int64_t n = h->n, k = h->k;
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(h, DAMF_E_IO, std::string("cannot write ") + path);
+  std::fwrite("DAMF", 1, 4, f);
+  putv<uint32_t>(f, 1);
+  putv<int64_t>(f, h->cfg.d);
+  putv<double>(f, h->cfg.alpha);
+  putv<double>(f, h->cfg.eps);
+  putv<uint64_t>(f, h->cfg.seed);
+  putv<double>(f, h->cfg.rebase_cond);
+  putv<int64_t>(f, h->cfg.rebase_every);
+  putv<uint8_t>(f, h->cfg.undirected ? 1 : 0);
+  putv<uint64_t>(f, h->events_applied);
+  putv<int64_t>(f, h->since_rebase);
+  std::vector<double> sig((size_t)k);
+  CK(cudaMemcpy(sig.data(), h->sigma, k * 8, cudaMemcpyDeviceToHost));
+  putv<int64_t>(f, k);
+  std::fwrite(sig.data(), 8, (size_t)k, f);
+  std::vector<float> rows((size_t)n * k);
+  for (int which : {DAMF_XB, DAMF_YB}) {
+    if (int r = damf_gpu_get_state(h, which, rows.data())) { std::fclose(f); return r; }
+    put_rows(f, rows, n, k);
+  }
+  std::vector<double> P((size_t)k * k), Pc((size_t)k * k);
+  for (int which : {DAMF_PX, DAMF_PY}) {
+    if (int r = damf_gpu_get_state(h, which, P.data())) { std::fclose(f); return r; }
+    for (int64_t i = 0; i < k; ++i)
+      for (int64_t j = 0; j < k; ++j) Pc[(size_t)j * k + i] = P[(size_t)i * k + j];
+    putv<int64_t>(f, k);
+    putv<int64_t>(f, k);
+    std::fwrite(Pc.data(), 8, Pc.size(), f);
+  }
+  if (h->alpha1) {  // enhancer.cpp:34-38: Z_b mirrors X_b, r_b = 0
+    if (int r = damf_gpu_get_state(h, DAMF_XB, rows.data())) { std::fclose(f); return r; }
+    put_rows(f, rows, n, k);
+    std::fill(rows.begin(), rows.end(), 0.0f);
+    put_rows(f, rows, n, k);
+  } else {
+    for (int which : {DAMF_ZB, DAMF_RB}) {
+      if (int r = damf_gpu_get_state(h, which, rows.data())) { std::fclose(f); return r; }
+      put_rows(f, rows, n, k);
+    }
+  }
+  // adjacency (insertion order of the device rows; weights 1.0 when unweighted)
+  std::vector<int64_t> off(n);
+  std::vector<int32_t> cnt(n);
+  CK(cudaMemcpy(off.data(), h->out.off, n * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cnt.data(), h->out.cnt, n * 4, cudaMemcpyDeviceToHost));
+  int64_t top = 0;
+  CK(cudaMemcpy(&top, h->out.pool_top, 8, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> ids((size_t)std::max<int64_t>(top, 1));
+  std::vector<double> w(h->out.wts ? (size_t)std::max<int64_t>(top, 1) : 0);
+  CK(cudaMemcpy(ids.data(), h->out.ids, top * 4, cudaMemcpyDeviceToHost));
+  if (h->out.wts) CK(cudaMemcpy(w.data(), h->out.wts, top * 8, cudaMemcpyDeviceToHost));
+  putv<int64_t>(f, n);
+  for (int64_t u = 0; u < n; ++u) {
+    putv<int64_t>(f, cnt[u]);
+    for (int32_t p = 0; p < cnt[u]; ++p) {
+      putv<int64_t>(f, ids[off[u] + p]);
+      putv<double>(f, h->out.wts ? w[off[u] + p] : 1.0);
+    }
+  }
+  const bool ok = std::ferror(f) == 0;
+  if (std::fclose(f) != 0 || !ok) return fail(h, DAMF_E_IO, std::string("write failed: ") + path);
+  return 0;
+}
+
+int damf_gpu_load_state(const char* path, const damf_config* sizing, damf_gpu** out) {
+  *out = nullptr;
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return DAMF_E_IO;
+  auto bad = [&](int code) {
+    std::fclose(f);
+    return code;
+  };
+  char magic[4];
+  uint32_t version = 0;
+  if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "DAMF", 4) != 0) return bad(DAMF_E_PARSE);
+  if (!getv(f, &version) || version != 1) return bad(DAMF_E_PARSE);
+  damf_config cfg{};
+  uint8_t und = 0;
+  uint64_t applied = 0;
+  int64_t since = 0;
+  if (!getv(f, &cfg.d) || !getv(f, &cfg.alpha) || !getv(f, &cfg.eps) || !getv(f, &cfg.seed) ||
+      !getv(f, &cfg.rebase_cond) || !getv(f, &cfg.rebase_every) || !getv(f, &und) ||
+      !getv(f, &applied) || !getv(f, &since))
+    return bad(DAMF_E_PARSE);
+  cfg.undirected = und ? 1 : 0;
+  if (sizing) {
+    cfg.node_capacity = sizing->node_capacity;
+    cfg.arc_capacity = sizing->arc_capacity;
+    cfg.flags = sizing->flags;
+  }
+  int64_t k = 0;
+  if (!getv(f, &k) || k < 1 || k > cfg.d) return bad(DAMF_E_PARSE);
+  std::vector<double> sig((size_t)k);
+  if (std::fread(sig.data(), 8, (size_t)k, f) != (size_t)k) return bad(DAMF_E_PARSE);
+  int64_t r = 0, c = 0;
+  std::vector<double> xb, yb, px, py, zb, rb;
+  if (!get_matrix(f, &r, &c, &xb) || c != k) return bad(DAMF_E_PARSE);
+  const int64_t n = r;
+  if (!get_matrix(f, &r, &c, &yb) || r != n || c != k) return bad(DAMF_E_PARSE);
+  if (!get_matrix(f, &r, &c, &px) || r != k || c != k) return bad(DAMF_E_PARSE);
+  if (!get_matrix(f, &r, &c, &py) || r != k || c != k) return bad(DAMF_E_PARSE);
+  if (!get_matrix(f, &r, &c, &zb) || r != n || c != k) return bad(DAMF_E_PARSE);
+  if (!get_matrix(f, &r, &c, &rb) || r != n || c != k) return bad(DAMF_E_PARSE);
+  int64_t gn = 0;
+  if (!getv(f, &gn) || gn != n) return bad(DAMF_E_PARSE);
+  std::vector<int64_t> off((size_t)n + 1, 0);
+  std::vector<int32_t> tgt;
+  std::vector<double> wts;
+  bool weighted = false;
+  for (int64_t u = 0; u < n; ++u) {
+    int64_t cnt = 0;
+    if (!getv(f, &cnt) || cnt < 0) return bad(DAMF_E_PARSE);
+    for (int64_t i = 0; i < cnt; ++i) {
+      int64_t v = 0;
+      double w = 0;
+      if (!getv(f, &v) || !getv(f, &w) || v < 0 || v >= n) return bad(DAMF_E_PARSE);
+      tgt.push_back((int32_t)v);
+      wts.push_back(w);
+      weighted = weighted || w != 1.0;
+    }
+    off[u + 1] = (int64_t)tgt.size();
+  }
+  std::fclose(f);
+  // fp64 column-major -> fp32 row-major (X_b, Y_b); P row-major
+  auto rows32 = [&](const std::vector<double>& cm) {
+    std::vector<float> o((size_t)n * k);
+    for (int64_t j = 0; j < k; ++j)
+      for (int64_t i = 0; i < n; ++i) o[(size_t)i * k + j] = (float)cm[(size_t)j * n + i];
+    return o;
+  };
+  auto rowmajor = [&](const std::vector<double>& cm) {
+    std::vector<double> o((size_t)k * k);
+    for (int64_t i = 0; i < k; ++i)
+      for (int64_t j = 0; j < k; ++j) o[(size_t)i * k + j] = cm[(size_t)j * k + i];
+    return o;
+  };
+  const std::vector<float> x32 = rows32(xb), y32 = rows32(yb);
+  const std::vector<double> pxr = rowmajor(px), pyr = rowmajor(py);
+  damf_csr g{n, (int64_t)tgt.size(), off.data(), tgt.data(), weighted ? wts.data() : nullptr};
+  t_skip_ppr_init = true;
+  const int st = damf_gpu_create_from_factors(&g, &cfg, k, x32.data(), y32.data(), pxr.data(),
+                                              pyr.data(), sig.data(), out);
+  t_skip_ppr_init = false;
+  if (st) return st;
+  damf_gpu* h = *out;
+  h->events_applied = applied;
+  h->since_rebase = since;
+  if (!h->alpha1) {
+    // Engine(g, fs, es, ...) resumes the saved enhancer (engine.hpp:32-34)
+    const std::vector<float> z32 = rows32(zb), r32 = rows32(rb);
+    CK(cudaMemcpy2D(h->Zb, (size_t)h->d * 4, z32.data(), (size_t)k * 4, (size_t)k * 4, n,
+                    cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(h->rb, (size_t)h->d * 4, r32.data(), (size_t)k * 4, (size_t)k * 4, n,
+                    cudaMemcpyHostToDevice));
+    CK(launch_ppr_keys(ppr_args(h), h->nsm, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
   return 0;
 }
 

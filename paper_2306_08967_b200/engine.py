@@ -102,6 +102,8 @@ def lib():
         L.damf_gpu_query_rows.argtypes = [vp, C.c_int32, i64p, C.c_int64, f32p]
         L.damf_gpu_load_rows.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, vp]
         L.damf_gpu_score_pairs.argtypes = [vp, i64p, i64p, C.c_int64, C.c_int32, f64p]
+        L.damf_gpu_save_state.argtypes = [vp, C.c_char_p]
+        L.damf_gpu_load_state.argtypes = [C.c_char_p, C.POINTER(Config), C.POINTER(vp)]
         L.damf_gpu_topk_pairs.argtypes = [vp, i64p, i64p, C.c_int64, C.c_int32, C.c_int64, i64p,
                                           f64p]
         L.damf_gpu_ppr_trace.argtypes = [vp, vp, C.c_int]
@@ -210,6 +212,26 @@ class Engine:
             raise DamfError(st, "damf_gpu_create failed")
         self.d = d
         self.alpha = alpha
+        return self
+
+    def save_state(self, path):
+        """save_state (io.cpp:182-222): the reference's DAMF v1 binary."""
+        self._check(lib().damf_gpu_save_state(self.h, str(path).encode()))
+
+    @classmethod
+    def load_state(cls, path, node_capacity=0, arc_capacity=0):
+        """load_state (io.cpp:224-264): resume from a DAMF v1 file (ours or the
+        reference's)."""
+        L = lib()
+        sizing = Config(0, 0.0, 0.0, 0, 0.0, 0, 0, 0, node_capacity, arc_capacity)
+        self = cls.__new__(cls)
+        self.h = C.c_void_p()
+        st = L.damf_gpu_load_state(str(path).encode(), C.byref(sizing), C.byref(self.h))
+        if st:
+            self.h = None
+            raise DamfError(st, f"damf_gpu_load_state({path}) failed")
+        dg = self.diag()
+        self.d = dg["d"]
         return self
 
     def close(self):

@@ -1,0 +1,120 @@
+"""State persistence in the reference's DAMF v1 format (io.cpp:182-264).
+
+The format is parsed / written here independently from the library (the
+layout of save_state: magic, version, RunConfig, counters, sigma, X_b, Y_b,
+P_X, P_Y, Z_b, r_b column-major fp64, then the adjacency), so a file the
+device writes is readable as the reference's, and a file laid out like the
+reference's (built from the oracle's fp64 state) resumes on the device."""
+import os
+import struct
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import gpu_from_oracle, product, rel_frob, sigma_rel
+from paper_2306_08967_b200 import engine as ge
+from paper_2306_08967_b200.workloads import EventList
+
+pytestmark = pytest.mark.gpu
+
+
+def read_damf(path):
+    b = open(path, "rb").read()
+    pos = 0
+
+    def take(fmt):
+        nonlocal pos
+        v = struct.unpack_from(fmt, b, pos)
+        pos += struct.calcsize(fmt)
+        return v
+
+    assert b[:4] == b"DAMF"
+    pos = 4
+    (ver,) = take("<I")
+    d, alpha, eps, seed, rc, re_, und, applied, since = take("<qddQdqBQq")
+    (k,) = take("<q")
+    sig = np.array(take(f"<{k}d"))
+
+    def mat():
+        r, c = take("<qq")
+        return np.array(take(f"<{r * c}d")).reshape(c, r).T
+
+    xb, yb, px, py, zb, rb = (mat() for _ in range(6))
+    (n,) = take("<q")
+    adj = []
+    for _ in range(n):
+        (c,) = take("<q")
+        adj.append([take("<qd") for _ in range(c)])
+    assert pos == len(b)
+    return dict(ver=ver, d=d, alpha=alpha, eps=eps, undirected=und, applied=applied, since=since,
+                sigma=sig, xb=xb, yb=yb, px=px, py=py, zb=zb, rb=rb, adj=adj)
+
+
+def write_damf(path, st):
+    with open(path, "wb") as f:
+        f.write(b"DAMF")
+        f.write(struct.pack("<I", 1))
+        f.write(struct.pack("<qddQdqBQq", st["d"], st["alpha"], st["eps"], 0, 1e8, 50000,
+                            st["undirected"], st["applied"], st["since"]))
+        f.write(struct.pack("<q", len(st["sigma"])) + np.asarray(st["sigma"], "<f8").tobytes())
+        for m in (st["xb"], st["yb"], st["px"], st["py"], st["zb"], st["rb"]):
+            m = np.asarray(m, np.float64)
+            f.write(struct.pack("<qq", *m.shape) + np.asfortranarray(m).tobytes(order="F"))
+        f.write(struct.pack("<q", len(st["adj"])))
+        for row in st["adj"]:
+            f.write(struct.pack("<q", len(row)))
+            for v, w in row:
+                f.write(struct.pack("<qd", v, w))
+
+
+def test_save_is_reference_layout_and_round_trips(tmp_path):
+    g, ev = oracle.gen_mixed_stream(200, 150, 600, 120, 77)
+    oe = oracle.OracleEngine(g, d=12, alpha=0.25, eps=1e-6, seed=77)
+    e = gpu_from_oracle(g, oe, d=12, alpha=0.25, eps=1e-6)
+    e.apply(ev.slice(0, 60))
+    path = str(tmp_path / "state.damf")
+    e.save_state(path)
+    st = read_damf(path)
+    assert st["ver"] == 1 and st["d"] == 12 and st["applied"] == 60
+    assert np.array_equal(st["xb"], e.get(ge.XB).astype(np.float64))
+    assert np.array_equal(st["px"], e.get(ge.PX))
+    assert np.array_equal(st["zb"], e.get(ge.ZB).astype(np.float64))
+    off, ids, _ = e.graph_sets()
+    for u in range(e.n):
+        assert sorted(v for v, _ in st["adj"][u]) == sorted(ids[off[u]:off[u + 1]].tolist())
+    # resume and continue: same results as the engine that never stopped
+    e2 = ge.Engine.load_state(path)
+    assert e2.diag()["events_applied"] == 60
+    assert np.array_equal(e2.get(ge.Z), e.get(ge.Z))
+    e.apply(ev.slice(60, 120))
+    e2.apply(ev.slice(60, 120))
+    wp = rel_frob(product(e2.get(ge.X), e2.get(ge.Y)), product(e.get(ge.X), e.get(ge.Y)))
+    print("resumed vs uninterrupted product", wp)
+    assert wp <= 1e-6 and sigma_rel(e2.get(ge.SIGMA), e.get(ge.SIGMA)) <= 1e-9
+
+
+def test_reference_layout_file_resumes_on_device(tmp_path):
+    # a file laid out like the reference's save_state, from the oracle's fp64
+    # state, resumes on the device and answers the same queries
+    g, ev = oracle.gen_mixed_stream(150, 120, 500, 60, 91)
+    oe = oracle.OracleEngine(g, d=10, alpha=0.3, eps=1e-7, seed=91)
+    oe.apply(ev.slice(0, 40))
+    n = oe.dims()[0]
+    off, ids, _ = oe.graph_sets()
+    st = dict(d=10, alpha=0.3, eps=1e-7, undirected=0, applied=40, since=40,
+              sigma=oe.get(oe.SIGMA), xb=oe.get(oe.XB), yb=oe.get(oe.YB), px=oe.get(oe.PX),
+              py=oe.get(oe.PY), zb=oe.get(oe.ZB), rb=oe.get(oe.RB),
+              adj=[[(int(v), 1.0) for v in ids[off[u]:off[u + 1]]] for u in range(n)])
+    path = str(tmp_path / "ref.damf")
+    write_damf(path, st)
+    e = ge.Engine.load_state(path, node_capacity=64)
+    assert e.n == n and e.k == len(st["sigma"])
+    zr = rel_frob(e.get(ge.Z).astype(np.float64), oe.get(oe.Z))
+    print("loaded Z vs oracle", zr)
+    assert zr <= 1e-6
+    e.apply(ev.slice(40, 60))
+    oe.apply(ev.slice(40, 60))
+    wp = rel_frob(product(e.get(ge.X), e.get(ge.Y)), product(oe.get(oe.X), oe.get(oe.Y)))
+    print("after 20 more events: product vs oracle", wp)
+    assert wp <= 1e-5
