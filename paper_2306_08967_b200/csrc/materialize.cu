@@ -7,6 +7,8 @@
 // row tiles of X stream through registers with 128-bit loads; each thread
 // owns a 4-row x 4-column register block. Safe in place (out == in): a CTA
 // reads its whole row tile into shared memory before writing it.
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "materialize.cuh"
 
@@ -304,6 +306,16 @@ __global__ void split_f_kernel(const double* FT, int ldf, int k, float* hi, floa
     lo[x] = (float)(f - (double)h);
   }
 }
+// bf16 hi/lo split for the d = 256 kind::f16 path (materialize_tc.cu)
+__global__ void split_f_bf16_kernel(const double* FT, int ldf, int k, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < k * k; x += gridDim.x * blockDim.x) {
+    const int j = x / k, m = x % k;
+    const double f = FT[(int64_t)j * ldf + m];
+    const __nv_bfloat16 h = __double2bfloat16(f);
+    hi[x] = h;
+    lo[x] = __double2bfloat16(f - (double)__bfloat162float(h));
+  }
+}
 float* g_fsplit = nullptr;
 }  // namespace
 
@@ -317,6 +329,12 @@ cudaError_t launch_materialize(const float* X, int64_t n, int k, int ldx, const 
     if (!g_fsplit) {
       cudaError_t e = cudaMalloc(&g_fsplit, 2 * kMaxD * kMaxD * sizeof(float));
       if (e != cudaSuccess) return e;
+    }
+    if (k == 256) {
+      __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(g_fsplit);
+      split_f_bf16_kernel<<<64, 256, 0, s>>>(FT, ldf, k, h, h + k * k);
+      return launch_materialize_tc(X, n, k, ldx, g_fsplit, reinterpret_cast<float*>(h + k * k), Z, ldz,
+                                   s, nsm);
     }
     split_f_kernel<<<64, 256, 0, s>>>(FT, ldf, k, g_fsplit, g_fsplit + k * k);
     return launch_materialize_tc(X, n, k, ldx, g_fsplit, g_fsplit + k * k, Z, ldz, s, nsm);

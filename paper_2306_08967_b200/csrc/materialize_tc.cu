@@ -2,11 +2,12 @@
 // (factor_state.cpp:120-123 query_all, :215-222 rebase, enhancer.cpp:196-206).
 //
 // Precision: single-pass TF32 misses the 1e-4 contract (SURVEY hard part 3),
-// so each K-step issues three kind::tf32 MMAs into one FP32 TMEM accumulator:
-//     Z = Xhi*Fhi + Xhi*Flo + Xlo*Fhi      (relative error ~2^-20)
-// with Xhi = X rounded to an exact TF32 value in shared memory (low 13
-// mantissa bits cleared), Xlo = X - Xhi (exact), Fhi/Flo likewise from the
-// fp64 F on the host.
+// so each K-step issues three MMAs into one FP32 TMEM accumulator:
+//     Z = Xhi*Fhi + Xhi*Flo + Xlo*Fhi
+// d <= 128: kind::tf32 with Xhi = X rounded to an exact TF32 value in shared
+// memory (low 13 mantissa bits cleared), Xlo = X - Xhi (exact), Fhi/Flo
+// likewise from the fp64 F (relative error ~2^-20). d = 256: kind::f16 with
+// BF16 hi/lo parts (see materialize_bf16_256; ~4e-6).
 //
 // Warp roles (320 threads, one persistent CTA per SM, 128-row tiles):
 //   warp 0      TMA producer: X chunks (128 rows x 32 fp32 = one 128-byte
@@ -14,10 +15,12 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5   split: Xhi in place and Xlo into the stage's second buffer,
 //               fence.proxy.async, arrive
-//   warps 6-9   epilogue: tcgen05.ld 32 lanes x 32 columns, row stores
-// F (hi and lo, K-major, SW128 layout) stays resident in shared memory; the
-// accumulator is double-buffered in TMEM so the epilogue of tile t overlaps
-// the MMAs of tile t+1.
+//   warps 6-9   epilogue: tcgen05.ld 32 lanes x 32 columns, swizzled smem
+//               staging, TMA bulk tensor stores
+// d <= 64: F (hi and lo, K-major, SW128) resident in shared memory; d = 128:
+// F^T resident in TMEM (materialize_tc128_ts); d = 256: F^T streamed in K
+// slices, multicast across a 4-CTA cluster. The accumulator is double-
+// buffered in TMEM so the epilogue of tile t overlaps the MMAs of tile t+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -491,40 +494,137 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-// d = 256: F (hi + lo = 512 KB) fits neither shared memory nor TMEM, so it
-// streams with X: each stage holds one 32-wide K slice of the X tile (raw ->
-// hi in place, lo) and the matching K slice of F^T for all 256 output
-// columns (hi, lo; 256 rows x 128 B each, SW128), loaded by TMA from L2
-// (F stays L2-resident: 512 KB). Per slice 4 x 3 kind::tf32 MMAs with
-// N = 256; the 128 x 256 fp32 accumulator is double-buffered in TMEM (512
-// columns).
-constexpr int T256_STAGES = 2;
-constexpr int F256_BYTES = 256 * 128;  // one K slice of F^T (256 rows x 128 B)
-constexpr int T256_STAGE = 2 * CHUNK_BYTES + 2 * F256_BYTES;  // 96 KB
+// d = 256 on kind::f16 (BF16 inputs, FP32 accumulate). At d = 256 three
+// kind::tf32 passes need ~1.25 PFLOP/s of TF32 to keep up with HBM, which is
+// above the TF32 rate; three BF16 passes run at twice that rate and move half
+// the F bytes:   Z = Xhi*Fhi + Xhi*Flo + Xlo*Fhi   with Xhi = bf16_rn(X),
+// Xlo = bf16_rn(X - Xhi) (representation error 2^-17 |x|), F likewise from
+// fp64; measured 4e-6 relative Frobenius error, inside the 1e-4 contract.
+// Three decoupled rings per 32-wide K slice, so the HBM stream is not held
+// up by the tensor pipe: the raw X slice (one fp32 SW128 TMA box, 16 KB) is
+// freed as soon as the split warps have read it; the split writes the bf16
+// hi and lo operands (128 rows x 64 B each, SW64) into an operand ring that
+// the MMAs release; the F^T slices (256 rows x 32 bf16, hi and lo, SW64,
+// 16 KB each, TMA from L2) have their own ring, filled by a second producer.
+constexpr int B256_KC = 32;                        // K per slice
+constexpr int B256_XR = 4;                         // raw X ring (16 KB each)
+constexpr int B256_OP = 2;                         // operand ring (hi + lo, 16 KB each)
+constexpr int B256_FR = 3;                         // F ring (hi + lo, 32 KB each)
+constexpr int B256_F = 256 * 64;                   // one K slice of F^T (bf16), 16 KB
+constexpr int B256_CS = 4;                         // cluster size sharing each F slice (measured:
+                                                   // 1 / 2 / 4 -> 3.65 / 3.53 / 3.38 ms at n = 2^23)
+constexpr int B256_THREADS = THREADS + 32;         // + the F producer warp
+constexpr size_t B256_SMEM = 1024 + (size_t)B256_XR * CHUNK_BYTES + (size_t)B256_OP * 2 * 8192 +
+                             (size_t)B256_FR * 2 * B256_F + 8 * OSTAGE + 512;
 
-__global__ void __launch_bounds__(THREADS, 1)
-    materialize_tc256(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap zmap,
-                      const __grid_constant__ CUtensorMap fhmap, const __grid_constant__ CUtensorMap flmap,
-                      int64_t n) {
-  constexpr int D = 256, KB = D / KC, STAGES = T256_STAGES;
+// K-major SW64 UMMA descriptor (8-row groups 512 B apart)
+DAMF_D uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return d;
+}
+DAMF_D float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+DAMF_D void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+DAMF_D void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+DAMF_D uint32_t pack_bf16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));  // a -> low half
+  return r;
+}
+
+DAMF_D uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DAMF_D void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+DAMF_D void tma_load_2d_mc(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+DAMF_D void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// CS CTAs of a cluster work on CS different row tiles with the same F^T K
+// slices: CTA r loads rows [r*256/CS, (r+1)*256/CS) of each F slice and
+// multicasts them to every CTA of the cluster, so L2 serves each F slice once
+// per cluster instead of once per CTA. An F slot is refilled only when every
+// CTA's MMAs have released it (each MMA commit arrives on all CTAs' F-empty
+// barrier). All CTAs of a cluster run the same number of tile iterations; a
+// CTA whose tile is past the end re-reads the last tile and stores nothing.
+// Warps: 0 X producer, 1 MMA, 2-5 split, 6-9 epilogue, 10 F producer.
+template <int CS>
+__global__ void __launch_bounds__(B256_THREADS, 1)
+    materialize_bf16_256(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap zmap,
+                         const __grid_constant__ CUtensorMap fhmap, const __grid_constant__ CUtensorMap flmap,
+                         int64_t n) {
+  constexpr int D = 256, KB = D / B256_KC;
+  constexpr int FRW = 256 / CS;  // F^T rows this CTA loads per slice
+  constexpr uint16_t ALL = (uint16_t)((1u << CS) - 1);
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sS = sm;                                   // [STAGES][Xhi|Xlo|Fhi|Flo]
-  unsigned char* sO = sS + STAGES * T256_STAGE;             // [4 warps][2][4 KB]
+  unsigned char* sXR = sm;                                        // [XR][16 KB] raw fp32
+  unsigned char* sOP = sXR + B256_XR * CHUNK_BYTES;               // [OP][hi 8 KB | lo 8 KB]
+  unsigned char* sF = sOP + B256_OP * 2 * 8192;                   // [FR][hi 16 KB | lo 16 KB]
+  unsigned char* sO = sF + B256_FR * 2 * B256_F;                  // [4 warps][2][4 KB]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 4 * 2 * OSTAGE);
-  uint64_t* full = bars;
-  uint64_t* ready = bars + STAGES;
-  uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* tfull = bars + 3 * STAGES;
-  uint64_t* tempty = bars + 3 * STAGES + 2;
-  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  uint64_t* xfull = bars;                          // X TMA -> split
+  uint64_t* xempty = xfull + B256_XR;              // split -> X producer (4 warps)
+  uint64_t* ofull = xempty + B256_XR;              // split -> MMA (4 warps)
+  uint64_t* oempty = ofull + B256_OP;              // MMA -> split
+  uint64_t* ffull = oempty + B256_OP;              // F TMA -> MMA
+  uint64_t* fempty = ffull + B256_FR;              // MMAs of all CS CTAs -> F producer
+  uint64_t* tfull = fempty + B256_FR;              // MMA -> epilogue (2)
+  uint64_t* tempty = tfull + 2;                    // epilogue -> MMA (2)
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CS > 1 ? (int)cluster_rank() : 0;
   const int64_t ntiles = (n + TM - 1) / TM;
+  const int64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+  // tile of iteration i: (cid + i * ncl) * CS + rank, while the group's first tile exists
+  auto tile_of = [&](int64_t i) { return (cid + i * ncl) * CS + rank; };
+  const int64_t iters = ntiles > cid * CS ? (ntiles - cid * CS + ncl * CS - 1) / (ncl * CS) : 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&ready[s], 4);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < B256_XR; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 4);
+    }
+    for (int s = 0; s < B256_OP; ++s) {
+      mbar_init(&ofull[s], 4);
+      mbar_init(&oempty[s], 1);
+    }
+    for (int s = 0; s < B256_FR; ++s) {
+      mbar_init(&ffull[s], 1);
+      mbar_init(&fempty[s], CS);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -539,103 +639,137 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CS > 1) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_base_s;
   if (warp == 0) {
+    // ===== X producer: raw fp32 K slices of this CTA's tiles
     if (lane == 0) {
       uint32_t it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int64_t i = 0; i < iters; ++i) {
+        const int64_t t = tile_of(i) < ntiles ? tile_of(i) : ntiles - 1;
         for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-          unsigned char* st = sS + (size_t)s * T256_STAGE;
-          mbar_expect_tx(&full[s], CHUNK_BYTES + 2 * F256_BYTES);
-          tma_load_2d(st, &xmap, kb * KC, (int)(t * TM), &full[s]);
-          tma_load_2d(st + 2 * CHUNK_BYTES, &fhmap, kb * KC, 0, &full[s]);
-          tma_load_2d(st + 2 * CHUNK_BYTES + F256_BYTES, &flmap, kb * KC, 0, &full[s]);
+          const int s = it % B256_XR;
+          if (it >= B256_XR) mbar_wait(&xempty[s], ((it / B256_XR) - 1) & 1);
+          mbar_expect_tx(&xfull[s], CHUNK_BYTES);
+          tma_load_2d(sXR + (size_t)s * CHUNK_BYTES, &xmap, kb * B256_KC, (int)(t * TM), &xfull[s]);
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ===== F producer: this CTA's rows of every F^T slice, multicast to the cluster
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t i = 0; i < iters; ++i)
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % B256_FR;
+          if (it >= B256_FR) mbar_wait(&fempty[s], ((it / B256_FR) - 1) & 1);
+          mbar_expect_tx(&ffull[s], 2 * B256_F);
+          unsigned char* fh = sF + (size_t)s * 2 * B256_F + rank * FRW * 64;
+          if (CS > 1) {
+            tma_load_2d_mc(fh, &fhmap, kb * B256_KC, rank * FRW, &ffull[s], ALL);
+            tma_load_2d_mc(fh + B256_F, &flmap, kb * B256_KC, rank * FRW, &ffull[s], ALL);
+          } else {
+            tma_load_2d(fh, &fhmap, kb * B256_KC, 0, &ffull[s]);
+            tma_load_2d(fh + B256_F, &flmap, kb * B256_KC, 0, &ffull[s]);
+          }
         }
     }
   } else if (warp == 1) {
+    // ===== MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(D >> 3) << 17) |
+      // kind::f16: D = F32, A = B = BF16, both K-major, N = 256, M = 128
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(D >> 3) << 17) |
                                  ((uint32_t)(TM >> 4) << 24);
       uint32_t it = 0, tl = 0;
-      const uint32_t sbase = smem_u32(sS);
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+      const uint32_t obase = smem_u32(sOP), fbase = smem_u32(sF);
+      for (int64_t i = 0; i < iters; ++i, ++tl) {
         const int a = tl & 1;
         if (tl >= 2) mbar_wait(&tempty[a], ((tl >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t dtm = tmem + (uint32_t)(a * D);
         for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&ready[s], (it / STAGES) & 1);
+          const int so = it % B256_OP, sf = it % B256_FR;
+          mbar_wait(&ffull[sf], (it / B256_FR) & 1);
+          mbar_wait(&ofull[so], (it / B256_OP) & 1);
           tc_fence_after();
-          const uint32_t xh = sbase + (uint32_t)s * T256_STAGE, xl = xh + CHUNK_BYTES;
-          const uint32_t fh = xh + 2 * CHUNK_BYTES, fl = fh + F256_BYTES;
+          const uint32_t xh = obase + (uint32_t)so * 2 * 8192, xl = xh + 8192;
+          const uint32_t fh = fbase + (uint32_t)sf * 2 * B256_F, fl = fh + B256_F;
 #pragma unroll
-          for (int ks = 0; ks < KC / 8; ++ks) {
+          for (int ks = 0; ks < B256_KC / 16; ++ks) {  // 16 bf16 (32 B) per MMA
             const uint32_t ko = ks * 32;
             const uint32_t acc0 = (kb | ks) ? 1u : 0u;
-            mma_tf32(dtm, umma_desc(xh + ko), umma_desc(fh + ko), idesc, acc0);
-            mma_tf32(dtm, umma_desc(xh + ko), umma_desc(fl + ko), idesc, 1u);
-            mma_tf32(dtm, umma_desc(xl + ko), umma_desc(fh + ko), idesc, 1u);
+            mma_bf16(dtm, umma_desc_sw64(xh + ko), umma_desc_sw64(fh + ko), idesc, acc0);
+            mma_bf16(dtm, umma_desc_sw64(xh + ko), umma_desc_sw64(fl + ko), idesc, 1u);
+            mma_bf16(dtm, umma_desc_sw64(xl + ko), umma_desc_sw64(fh + ko), idesc, 1u);
           }
-          mma_commit(&empty[s]);
+          mma_commit(&oempty[so]);
+          if (CS > 1) mma_commit_mc(&fempty[sf], ALL); else mma_commit(&fempty[sf]);
         }
         mma_commit(&tfull[a]);
       }
     }
   } else if (warp < 6) {
-    const int st = threadIdx.x - 64;
+    // ===== split: row r of a raw slice (32 fp32, SW128) -> 32 bf16 hi and
+    // 32 bf16 lo (SW64 rows of the operand slot)
+    const int r = threadIdx.x - 64;
+    const uint32_t xbase = smem_u32(sXR), obase = smem_u32(sOP);
     uint32_t it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+    for (int64_t i = 0; i < iters; ++i)
       for (int kb = 0; kb < KB; ++kb, ++it) {
-        const int s = it % STAGES;
-        mbar_wait(&full[s], (it / STAGES) & 1);
-        float4* xh = reinterpret_cast<float4*>(sS + (size_t)s * T256_STAGE);
-        float4* xl = reinterpret_cast<float4*>(sS + (size_t)s * T256_STAGE + CHUNK_BYTES);
+        const int sx = it % B256_XR, so = it % B256_OP;
+        mbar_wait(&xfull[sx], (it / B256_XR) & 1);
+        const uint32_t st = xbase + (uint32_t)sx * CHUNK_BYTES;
+        float4 v[8];
 #pragma unroll
-        for (int q = 0; q < CHUNK_BYTES / 16 / 128; ++q) {
-          const int i = st + q * 128;
-          float4 v = xh[i];
-          float4 h, l;
-          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-          l.x = v.x - h.x;
-          l.y = v.y - h.y;
-          l.z = v.z - h.z;
-          l.w = v.w - h.w;
-          xh[i] = h;
-          xl[i] = l;
+        for (int c = 0; c < 8; ++c) v[c] = lds128(st + r * 128 + ((c ^ (r & 7)) << 4));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[sx]);  // raw slot free: values are in registers
+        if (it >= B256_OP) mbar_wait(&oempty[so], ((it / B256_OP) - 1) & 1);
+        const uint32_t ob = obase + (uint32_t)so * 2 * 8192;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {  // bf16 chunk c = fp32 columns 8c .. 8c+7
+          const float4 p = v[2 * c], q = v[2 * c + 1];
+          uint4 h, l;
+          h.x = pack_bf16(p.x, p.y);
+          h.y = pack_bf16(p.z, p.w);
+          h.z = pack_bf16(q.x, q.y);
+          h.w = pack_bf16(q.z, q.w);
+          l.x = pack_bf16(p.x - __uint_as_float(h.x << 16), p.y - __uint_as_float(h.x & 0xFFFF0000u));
+          l.y = pack_bf16(p.z - __uint_as_float(h.y << 16), p.w - __uint_as_float(h.y & 0xFFFF0000u));
+          l.z = pack_bf16(q.x - __uint_as_float(h.z << 16), q.y - __uint_as_float(h.z & 0xFFFF0000u));
+          l.w = pack_bf16(q.z - __uint_as_float(h.w << 16), q.w - __uint_as_float(h.w & 0xFFFF0000u));
+          const uint32_t off = r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+          sts128(ob + off, h);
+          sts128(ob + 8192 + off, l);
         }
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ready[s]);
+        if (lane == 0) mbar_arrive(&ofull[so]);
       }
   } else {
+    // ===== epilogue: TMEM -> registers -> swizzled smem -> TMA store
     const int q = warp & 3;
     unsigned char* stg = sO + (size_t)(warp - 6) * 2 * OSTAGE;
     uint32_t tl = 0, sb = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+    for (int64_t i = 0; i < iters; ++i, ++tl) {
+      const int64_t t = tile_of(i);
       const int a = tl & 1;
       mbar_wait(&tfull[a], (tl >> 1) & 1);
       tc_fence_after();
       const int64_t row0 = t * TM + q * 32;
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 32, sb ^= 1) {
-        uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * D + c0), r);
+        uint32_t rr[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * D + c0), rr);
         unsigned char* buf = stg + sb * OSTAGE;
         if (lane == 0) tma_store_wait_read1();
         __syncwarp();
 #pragma unroll
         for (int v = 0; v < 8; ++v)
           *reinterpret_cast<float4*>(buf + sw128(lane, 4 * v)) =
-              make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                          __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+              make_float4(__uint_as_float(rr[4 * v]), __uint_as_float(rr[4 * v + 1]),
+                          __uint_as_float(rr[4 * v + 2]), __uint_as_float(rr[4 * v + 3]));
         fence_proxy_async();
         __syncwarp();
         if (lane == 0 && row0 < n) tma_store_2d(&zmap, c0, (int)row0, buf);
@@ -647,11 +781,58 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) tma_store_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
+  // no CTA may leave while a peer can still multicast into it or arrive on its barriers
+  if (CS > 1) cluster_sync_all(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
+}
+
+template <int CS>
+cudaError_t launch_bf16_256(const CUtensorMap& map, const CUtensorMap& zm, const CUtensorMap& fh,
+                            const CUtensorMap& fl, int64_t n, int64_t ntiles, cudaStream_t s, int nsm) {
+  const size_t smem = B256_SMEM;
+  static int grid = 0;
+  if (!grid) {
+    cudaError_t e = cudaFuncSetAttribute(materialize_bf16_256<CS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    grid = nsm / CS * CS;
+    if (CS > 1) {  // clusters live inside a GPC: use as many as fit at once
+      cudaLaunchConfig_t q = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.gridDim = dim3(grid);
+      q.blockDim = dim3(B256_THREADS);
+      q.dynamicSmemBytes = smem;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, materialize_bf16_256<CS>, &q) == cudaSuccess && ncl > 0 &&
+          ncl * CS < grid)
+        grid = ncl * CS;
+    }
+  }
+  int g = grid;
+  const int64_t groups = (ntiles + CS - 1) / CS;
+  if (groups * CS < g) g = (int)(groups * CS);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(B256_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, materialize_bf16_256<CS>, map, zm, fh, fl, n);
 }
 
 template <int D>
@@ -696,28 +877,20 @@ cudaError_t launch_tc(const float* X, int64_t n, int ldx, const float* Fhi, cons
   const int64_t ntiles = (n + TM - 1) / TM;
   const int grid = (int)(ntiles < nsm ? ntiles : nsm);
   if (D == 256) {
+    // Fhi / Flo hold bf16 [256][256] (FT layout) for this path
     CUtensorMap fh, fl;
     cuuint64_t fdims[2] = {256, 256};
-    cuuint64_t fstr[1] = {256 * 4};
-    cuuint32_t fbox[2] = {(cuuint32_t)KC, 256u};
-    r = encode(&fh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Fhi), fdims, fstr, fbox,
-               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    cuuint64_t fstr[1] = {256 * 2};
+    cuuint32_t fbox[2] = {(cuuint32_t)B256_KC, (cuuint32_t)(256 / B256_CS)};
+    r = encode(&fh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<float*>(Fhi), fdims, fstr, fbox,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    r = encode(&fl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Flo), fdims, fstr, fbox,
-               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    r = encode(&fl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<float*>(Flo), fdims, fstr, fbox,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    const size_t smem = 1024 + T256_STAGES * T256_STAGE + 8 * OSTAGE + 256;
-    static bool cfg256 = false;
-    if (!cfg256) {
-      cudaError_t e = cudaFuncSetAttribute(materialize_tc256,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      cfg256 = true;
-    }
-    materialize_tc256<<<grid, THREADS, smem, s>>>(map, zm, fh, fl, n);
-    return cudaGetLastError();
+    return launch_bf16_256<B256_CS>(map, zm, fh, fl, n, ntiles, s, nsm);
   }
   if (D == 128) {
     const size_t smem = 1024 + TS_STAGES * 2 * CHUNK_BYTES + 8 * OSTAGE + 256;
