@@ -1456,32 +1456,51 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     __syncthreads();
     if (tid == 0) S.lcnt3[old] = 0;  // next filled in round rr + 1 (after this round's barrier)
     int myF = 0;
-    for (int q = warp; q < mycnt; q += NW) {
-      const int v = (rr > 0 && q < PCAP) ? S.plist[cur][q] : lists[cur][(int64_t)rank * stride + q];
-      // independent loads of the candidate, issued together
+    // Candidates are evaluated four per warp at a time (8-lane groups, one
+    // row each: the loads of four rows are in flight together); most are
+    // below threshold and only get their key stored. The whole warp then
+    // pushes the group's rows that are over it, one after another.
+    for (int q0 = warp * 4; q0 < mycnt; q0 += NW * 4) {
+      const int grp = lane >> 3, gl = lane & 7;
+      const int qg = q0 + grp;
+      int vg = -1;
+      bool pg = false;
+      if (qg < mycnt)
+        vg = (rr > 0 && qg < PCAP) ? S.plist[cur][qg] : lists[cur][(int64_t)rank * stride + qg];
+      if (rr == 0) {
+        pg = vg >= 0 && A.key[vg] > thr;
+      } else {
+        float mg = 0.0f;
+        if (vg >= 0) {
+          const float* rg = A.rb + (int64_t)vg * d;
+#pragma unroll
+          for (int t = 0; t < kMaxD / 8; ++t) {
+            const int j = gl + 8 * t;
+            if (j < k) mg = fmaxf(mg, fabsf(rg[j]));
+          }
+        }
+        mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, 1));
+        mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, 2));
+        mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, 4));
+        if (vg >= 0) {
+          const float keyg = (float)((double)mg / fmax(A.deg[vg], 1.0));
+          pg = keyg > thr;
+          if (!pg && gl == 0) A.key[vg] = keyg;
+        }
+      }
+      const unsigned pmask = __ballot_sync(0xffffffffu, pg && gl == 0);
+      for (unsigned pm = pmask; pm; pm &= pm - 1) {
+      const int v = __shfl_sync(0xffffffffu, vg, __ffs(pm) - 1);
       const float* rv0 = A.rb + (int64_t)v * d;
       float* zu = A.Zb + (int64_t)v * d;
       float rj[kMaxD / 32], zj[kMaxD / 32];
 #pragma unroll
       for (int t = 0; t < kMaxD / 32; ++t) {
         const int j = lane + 32 * t;
-        rj[t] = j < k ? rv0[j] : 0.0f;
         zj[t] = j < k ? zu[j] : 0.0f;
       }
-      const double degv = A.deg[v];
-      const float keyv = rr == 0 ? A.key[v] : 0.0f;
       const int64_t ib = in.off[v];
       const int c = in.cnt[v];
-      float m = 0.0f;
-#pragma unroll
-      for (int t = 0; t < kMaxD / 32; ++t) m = fmaxf(m, fabsf(rj[t]));
-      m = warp_max(m);
-      const float key = (float)((double)m / fmax(degv, 1.0));
-      const bool push = rr == 0 ? keyv > thr : key > thr;
-      if (!push) {
-        if (lane == 0) A.key[v] = key;
-        continue;
-      }
       // first 32 in-arcs issued alongside the read-and-zero of r[u]
       int vv0 = -1;
       float w0 = 1.0f;
@@ -1533,6 +1552,7 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
           }
         }
       }
+    }
     }
     if (lane == 0) s_cnt[warp] = myF;
     __syncthreads();

@@ -600,6 +600,7 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
   using CL = Cols<PER, VEC>;
   cg::grid_group g = cg::this_grid();
   __shared__ int s_id[PW][32];
+  __shared__ int s_pair[PW][32];
   __shared__ float s_w[PW][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int grp = lane / G, gl = lane & (G - 1);
@@ -607,6 +608,7 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
   const unsigned lt = (1u << lane) - 1u;
   const int gw = blockIdx.x * PW + wib, nw = gridDim.x * PW;
   int* sid = s_id[wib];
+  int* spair = s_pair[wib];
   float* sw = s_w[wib];
   unsigned long long* wq = A.wq;
   unsigned long long* sc = wq + WQ_SC;
@@ -615,6 +617,47 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
   const float thr = (float)(A.alpha_eps / *A.smax);
   const double om = 1.0 - A.alpha;
   const DevCSR& inC = A.directed ? A.in : A.out;
+  // Isolated edges (u - v, both of degree 1, undirected): their residual
+  // bounces between the two rows, shrinking by (1-alpha)^2 per two pushes,
+  // which on R-MAT graphs (many such components) keeps ~50 extra rounds
+  // alive with a few hundred rows each. A pushed paired row instead takes
+  // the pair to its fixed point in one step: with c_uv = (1-alpha) w / deg v
+  // (what pushing u adds to r[v]) the infinite alternating sequence pushes
+  //   S_u = (r_u + c_vu r_v) / (1 - c_uv c_vu),  S_v = (r_v + c_uv r_u) / (...)
+  // out of u and v; Z[u] += S_u, Z[v] += S_v, r[u] = r[v] = 0 (zero residual,
+  // inside the defect bound enhancer.cpp:98-157 asks for). Both rows of a
+  // pair may be closed concurrently in one round: the residuals are taken
+  // with atomicExch and the Z updates are atomic, so each part is counted once.
+  auto pair_of = [&](int u) -> int {
+    if (A.directed || inC.cnt[u] != 1) return -1;
+    const int v = inC.ids[inC.off[u]];
+    if (v == u || inC.cnt[v] != 1 || inC.ids[inC.off[v]] != u) return -1;
+    return v;
+  };
+  auto close_pair = [&](int u, int v) {
+    const double wu = inC.wts ? inC.wts[inC.off[u]] : 1.0;
+    const double wv = inC.wts ? inC.wts[inC.off[v]] : 1.0;
+    const float cuv = (float)(om * wu / fmax(A.deg[v], 1.0));
+    const float cvu = (float)(om * wv / fmax(A.deg[u], 1.0));
+    const float inv = (float)(1.0 / (1.0 - (double)cuv * (double)cvu));
+    float* ru = A.rb + (int64_t)u * d;
+    float* rv = A.rb + (int64_t)v * d;
+    float* zu = A.Zb + (int64_t)u * d;
+    float* zv = A.Zb + (int64_t)v * d;
+#pragma unroll
+    for (int e = 0; e < CL::NE; ++e) {
+      const int j = CL::col(gl, e);
+      if (j < k) {
+        const float a = atomicExch(ru + j, 0.0f), b = atomicExch(rv + j, 0.0f);
+        atomicAdd(zu + j, (a + cvu * b) * inv);
+        atomicAdd(zv + j, (b + cuv * a) * inv);
+      }
+    }
+    if (gl == 0) {
+      A.key[u] = 0.0f;
+      A.key[v] = 0.0f;
+    }
+  };
   const bool resume = A.split && A.pst->phase == 1;
   int R = resume ? A.pst->R : (int)A.stats[2];  // device-resident round stamp base (monotonic)
   if (blockIdx.x == 0)
@@ -730,11 +773,19 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
           if (!pm) continue;
           const int np = __popc(pm);
           mine += np;
-          if (push) sid[__popc(pm & lt)] = v;
-          myS += add_items(v, push);
+          const int pv = push ? pair_of(v) : -1;
+          if (push) {
+            sid[__popc(pm & lt)] = v;
+            spair[__popc(pm & lt)] = pv;
+          }
+          myS += add_items(v, push && pv < 0);
           __syncwarp();
           for (int j = grp; j < np; j += NG) {
-            const int u = sid[j];
+            const int u = sid[j], pu = spair[j];
+            if (pu >= 0) {
+              close_pair(u, pu);
+              continue;
+            }
             float x[CL::NE];
             CL::load(A.rb + (int64_t)u * d, gl, k, x);
             push_row(u, x);
@@ -751,6 +802,7 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
           const int q = base + grp;
           const int v = q < start + cnt ? candL[q] : -1;
           bool push = false;
+          int pv = -1;
           float x[CL::NE];
           if (v >= 0) {
             CL::load(A.rb + (int64_t)v * d, gl, k, x);
@@ -762,12 +814,17 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
             for (int o = G / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(gm, m, o, G));
             const float key = (float)((double)m / fmax(A.deg[v], 1.0));
             push = key > thr;
-            if (push) push_row(v, x);
-            else if (gl == 0) A.key[v] = key;
+            if (push) {
+              pv = pair_of(v);
+              if (pv >= 0) close_pair(v, pv);
+              else push_row(v, x);
+            } else if (gl == 0) {
+              A.key[v] = key;
+            }
           }
           const unsigned pm = __ballot_sync(0xffffffffu, push && gl == 0);
           mine += __popc(pm);
-          myS += add_items(v, push && gl == 0);
+          myS += add_items(v, push && gl == 0 && pv < 0);
         }
       }
     }

@@ -86,7 +86,8 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"{LIB_PATH} is not built (run `make` or __graft_entry__.build())")
-        L = C.CDLL(LIB_PATH)
+        # DAMF_GPU_LIB: load another build of the same library (A/B timing of kernel variants)
+        L = C.CDLL(os.environ.get("DAMF_GPU_LIB", LIB_PATH))
         vp = C.c_void_p
         L.damf_gpu_last_error.restype = C.c_char_p
         L.damf_gpu_last_error.argtypes = [vp]

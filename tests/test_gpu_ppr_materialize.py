@@ -192,3 +192,63 @@ def test_batched_scores_and_topk_match_oracle():
     overlap = len(ref_top & set(idx.tolist())) / K
     print("top-K overlap with the oracle", overlap)
     assert overlap >= 0.97
+
+
+def test_whole_gpu_push_closes_isolated_edges():
+    # The whole-GPU push (init_propagate, ppr.cu) takes a pushed row of an
+    # isolated edge (both ends of degree 1) to the pair's fixed point in one
+    # step. Graph: 400 isolated edges plus a random component; checked
+    # against the exact solve of Z = alpha X + (1-alpha) D^-1 A Z and the
+    # reference's defect bound (eval.cpp:591-610) after init_propagate and
+    # after a push that follows structural churn on pair rows.
+    from paper_2306_08967_b200 import workloads as W
+    rng = np.random.default_rng(21)
+    npair, nr = 400, 1200
+    n = 2 * npair + nr
+    pu = np.arange(0, 2 * npair, 2)
+    eu = [pu, 2 * npair + rng.integers(0, nr, 5 * nr)]
+    ev = [pu + 1, 2 * npair + rng.integers(0, nr, 5 * nr)]
+    u, v = np.concatenate(eu), np.concatenate(ev)
+    keep = u != v
+    key = np.unique(np.minimum(u[keep], v[keep]) * n + np.maximum(u[keep], v[keep]))
+    off, tgt = W.undirected_csr(n, key // n, key % n)
+    d, alpha, eps = 8, 0.15, 1e-6
+    x = (rng.standard_normal((n, d)) / np.sqrt(d)).astype(np.float32)
+    e = ge.Engine(n, off, tgt, None, d, d, x, x, np.eye(d), np.eye(d), np.ones(d), alpha=alpha,
+                  eps=eps, undirected=True, node_capacity=64)
+    st = e.ppr_init()
+
+    def check(e):
+        offs, ids, deg = e.graph_sets()
+        xx = e.get(ge.X).astype(np.float64)
+        z = e.get(ge.Z).astype(np.float64)
+        dfc = dense_defect(e.n, offs, ids, deg, xx, z, alpha)
+        op = np.eye(e.n)
+        for a in range(e.n):
+            if deg[a] > 0:
+                for b in ids[offs[a]:offs[a + 1]]:
+                    op[a, b] -= (1 - alpha) / deg[a]
+        zs = np.linalg.solve(op, alpha * xx)
+        # pair rows: one closed-form step, so they sit at the fixed point
+        pr = np.arange(2 * npair)
+        solo = [a for a in pr if deg[a] == 1 and deg[ids[offs[a]]] == 1]
+        perr = np.abs(z[solo] - zs[solo]).max() / np.abs(zs[solo]).max()
+        return dfc, perr, len(solo)
+
+    dfc, perr, ns = check(e)
+    print("init", st, "defect", dfc, "pair err", perr, ns)
+    assert ns >= 2 * npair - 10
+    assert dfc <= eps * (1 + 1e-6) + 2e-7
+    assert perr <= 1e-5
+    # churn: attach some pair rows to the big component, detach others, push
+    evs = []
+    for t in range(20):
+        a = int(pu[t])
+        evs.append(EventList.edges(ge.ADD_EDGE, [a], [2 * npair + int(rng.integers(nr))]))
+    for ev_ in evs:
+        e.apply(ev_, mode=ge.APPLY_GRAPH_AND_PPR_ONLY | ge.APPLY_DEFER_PUSH)
+    st2 = e.ppr_push()
+    dfc, perr, ns = check(e)
+    print("push", st2, "defect", dfc, "pair err", perr, ns)
+    assert dfc <= eps * (1 + 1e-6) + 2e-7
+    assert perr <= 1e-5

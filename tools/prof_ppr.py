@@ -43,5 +43,10 @@ for a, b in zip(us.tolist(), vs.tolist()):
     seen.add((a, b)); seen.add((b, a)); eu.append(a); ev.append(b)
     if len(eu) == 1000: break
 e.apply(W.EventList.edges(ge.ADD_EDGE, eu, ev), mode=ge.APPLY_GRAPH_AND_PPR_ONLY | ge.APPLY_DEFER_PUSH)
-run("push", e.ppr_push)
+if os.environ.get("PROF_PUSH_ONLY"):  # ncu --profile-from-start off: capture only this push
+    torch.cuda.synchronize(); torch.cuda.profiler.start()
+    run("push", e.ppr_push)
+    torch.cuda.synchronize(); torch.cuda.profiler.stop()
+else:
+    run("push", e.ppr_push)
 e.close()
