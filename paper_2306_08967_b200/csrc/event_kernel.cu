@@ -60,6 +60,7 @@ constexpr int PLD = 132;           // private-matrix row stride (d <= 128 in sme
 #define DAMF_GEMM_KU 8
 #endif
 constexpr int PCAP = 2048;         // fused-PPR candidate list entries kept in shared memory
+constexpr int GBUF_D = 4224;       // staging slot: 32 rows x 132 doubles (33 KB)
 
 template <int C>
 struct Smem {
@@ -86,7 +87,14 @@ struct Smem {
   int K, nrot, need;
   int k, pp[2];
   int err;
+  // GEMM operand staging: chunks of the streamed matrix (rows x ld doubles,
+  // one bulk copy each) in a two-slot ring, completion on gbar[slot]
+  alignas(128) double gbuf[2][GBUF_D];
+  unsigned long long gbar[2];
+  unsigned gq[2];                 // completed phases per slot
+  long long gprof[3];             // DAMF_PROF: staged-GEMM wait / DMMA / barrier cycles
 };
+static_assert(sizeof(Smem<16>) <= 232448, "event kernel shared memory above the 227 KB opt-in limit");
 
 // ----------------------------------------------------------------- reductions
 template <int C>
@@ -136,7 +144,7 @@ DAMF_D void own_range(int k, int n, int C, int rank, int& lo, int& hi) {
 // Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane>>2][lane&3],
 // b = B[lane&3][lane>>2], d{0,1} = D[lane>>2][2*(lane&3) + {0,1}].
 DAMF_D void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -225,6 +233,183 @@ DAMF_D void rows_gemm(Smem<C>& S, double* Out, int ldo, int o0, const double* Co
     total += f;
   }
   if (fro) *fro = total;
+}
+
+// Several row GEMMs with the same shapes, Out_j[o0 + r][:] = Coef_j[r][:] In_j,
+// with In_j streamed through shared memory instead of per-lane L2 loads:
+// thread 0 bulk-copies chunks of CR rows (contiguous, rows x ldi doubles) of
+// In_0, In_1, ... into a two-slot ring (cp.async.bulk + mbarrier), so the
+// copy of the next chunk -- also across GEMMs -- overlaps the DMMAs of this
+// one and each GEMM pays one L2 latency instead of one per K-chunk per warp.
+// nt <= 8 * MT rows, J <= 64 * TPW columns (8 warps x TPW 8-column tiles).
+struct GemmJob {
+  double* Out;
+  const double* Coef;
+  const double* In;
+  double* fro;
+};
+DAMF_D unsigned ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DAMF_D void mbar_wait_parity(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "GW_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra GW_WAIT;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+template <int C>
+DAMF_D void stage_chunk(Smem<C>& S, int slot, const double* src, unsigned bytes) {
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&S.gbar[slot]);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(S.gbuf[slot])),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+template <int C, int MT, int TPW>
+__device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0, int ldc, int nt,
+                             int ldi, int M, int J) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int ntiles = (J + 7) >> 3;
+  const int CR = min((GBUF_D / ldi) & ~3, (M + 3) & ~3);  // rows per chunk (multiple of 4)
+  const int nch = (M + CR - 1) / CR;
+  const int T = nj * nch;
+  const unsigned q0 = S.gq[0], q1 = S.gq[1];
+#if DAMF_PROF
+  const long long _gs = clock64();
+#endif
+  auto issue = [&](int t) {
+    const int j = t / nch, c = t % nch;
+    const int rows = min(CR, M - c * CR);
+    stage_chunk<C>(S, t & 1, jobs[j].In + (int64_t)c * CR * ldi, (unsigned)(rows * ldi * 8));
+  };
+  if (threadIdx.x == 0) {
+    // In was written through the generic proxy (other CTAs, before a cluster
+    // barrier): order it before the bulk copies. Once per call -- the fence
+    // waits for this thread's outstanding stores, so not once per chunk.
+    asm volatile("fence.proxy.async;" ::: "memory");
+    issue(0);
+    if (T > 1) issue(1);
+  }
+  int bc[TPW];
+  bool bok[TPW];
+#pragma unroll
+  for (int p = 0; p < TPW; ++p) {
+    const int tb = warp + NW * p;  // this warp's 8-column tiles
+    bc[p] = (tb << 3) + (lane >> 2);
+    bok[p] = tb < ntiles && bc[p] < J;
+  }
+  // two accumulator sets (even / odd k-steps): 2 * TPW * MT independent DMMA chains per warp
+  double d0[2][TPW][MT], d1[2][TPW][MT];
+  double frob = 0.0;
+  for (int t = 0; t < T; ++t) {
+    const int j = t / nch, c = t % nch;
+    if (c == 0) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int p = 0; p < TPW; ++p)
+#pragma unroll
+          for (int h = 0; h < MT; ++h) d0[u][p][h] = d1[u][p][h] = 0.0;
+      frob = 0.0;
+    }
+    const int slot = t & 1;
+#if DAMF_PROF
+    long long _g0 = clock64();
+#endif
+    mbar_wait_parity(&S.gbar[slot], ((slot ? q1 : q0) + (t >> 1)) & 1);
+#if DAMF_PROF
+    long long _g1 = clock64();
+    if (threadIdx.x == 0 && ctarank() == 0) S.gprof[0] += _g1 - _g0;
+#endif
+    const double* sb = S.gbuf[slot];
+    const double* Coef = jobs[j].Coef;
+    const int m0 = c * CR, rows = min(CR, M - m0);
+    for (int mm = 0; mm < rows; mm += 16) {
+      // operands of four k-steps loaded before their DMMAs
+      double a[4][MT], b[4][TPW];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int mr = mm + 4 * u + ac;
+        const bool mok = mr < rows;
+#pragma unroll
+        for (int h = 0; h < MT; ++h) {
+          const int r = 8 * h + ar;
+          a[u][h] = (r < nt && mok) ? Coef[(int64_t)r * ldc + m0 + mr] : 0.0;
+        }
+#pragma unroll
+        for (int p = 0; p < TPW; ++p) b[u][p] = (bok[p] && mok) ? sb[mr * ldi + bc[p]] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int p = 0; p < TPW; ++p)
+#pragma unroll
+          for (int h = 0; h < MT; ++h) dmma(d0[u & 1][p][h], d1[u & 1][p][h], a[u][h], b[u][p]);
+    }
+#if DAMF_PROF
+    long long _g2 = clock64();
+    if (threadIdx.x == 0 && ctarank() == 0) S.gprof[1] += _g2 - _g1;
+#endif
+    __syncthreads();  // every warp is done with this slot
+
+    if (threadIdx.x == 0 && t + 2 < T) issue(t + 2);
+    if (c == nch - 1) {
+      double* Out = jobs[j].Out;
+#pragma unroll
+      for (int p = 0; p < TPW; ++p) {
+        const int tb = warp + NW * p;
+        const int col = (tb << 3) + 2 * ac;
+#pragma unroll
+        for (int h = 0; h < MT; ++h) {
+          const int r = 8 * h + ar;
+          const double v0 = d0[0][p][h] + d0[1][p][h], v1 = d1[0][p][h] + d1[1][p][h];
+          if (r < nt && tb < ntiles) {
+            if (col < J) {
+              Out[(int64_t)(o0 + r) * ldo + col] = v0;
+              frob += v0 * v0;
+            }
+            if (col + 1 < J) {
+              Out[(int64_t)(o0 + r) * ldo + col + 1] = v1;
+              frob += v1 * v1;
+            }
+          }
+        }
+      }
+      if (jobs[j].fro) *jobs[j].fro = block_sum(S, frob);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.gq[0] = q0 + (unsigned)((T + 1) >> 1);
+    S.gq[1] = q1 + (unsigned)(T >> 1);
+  }
+  __syncthreads();
+#if DAMF_PROF
+  if (threadIdx.x == 0 && ctarank() == 0) S.gprof[2] += clock64() - _gs;
+#endif
+}
+
+// Dispatch: the staged form when the shapes fit it, else one rows_gemm each.
+template <int C>
+DAMF_D void rows_gemms(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0, int ldc, int nt,
+                       int ldi, int M, int J) {
+  if (nt <= 8 && J <= 128)
+    rows_gemm_staged<C, 1, 2>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
+  else if (nt <= 16 && J <= 128)
+    rows_gemm_staged<C, 2, 2>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
+  else if (nt <= 16 && J <= 256)
+    rows_gemm_staged<C, 2, 4>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
+  else
+    for (int j = 0; j < nj; ++j)
+      rows_gemm<C>(S, jobs[j].Out, ldo, o0, jobs[j].Coef, ldc, nt, jobs[j].In, ldi, M, J, jobs[j].fro);
 }
 
 // ---------------------------------------------- exact inverse (one CTA)
@@ -888,7 +1073,10 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     eig_rank1<C>(S, cl, S.lamA, S.zz, lm, n, olo, ohi, PB[0], pld, olo, S.lamB, A.ctl->prof);
     PROF_MARK(4);
     // E columns t (rows of E^T, private): E^T[t] = sum_e Q2^T[t][e] Q1^T[e]
-    rows_gemm<C>(S, PB[1], pld, 0, PB[0], pld, ohi - olo, A.ws_Q1T, ld, n, n, nullptr);
+    {
+      const GemmJob job = {PB[1], PB[0], A.ws_Q1T, nullptr};
+      rows_gemms<C>(S, &job, 1, pld, 0, pld, ohi - olo, ld, n, n);
+    }
   } else {
     for (int x = tid; x < (ohi - olo) * n; x += NT) {
       const int t = olo + x / n, i = x % n;
@@ -1089,12 +1277,14 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     // ---- the four GEMMs on the FP64 tensor cores (owned rows t) -------------
     const int nt = kohi - olo;
     double fro[4] = {0.0, 0.0, 0.0, 0.0};
-    rows_gemm<C>(S, PTA_n, ld, olo, prow(0, olo), pld, nt, PTA, ld, k, k, &fro[0]);
-    rows_gemm<C>(S, PTB_n, ld, olo, prow(3, olo), pld, nt, PTB, ld, k, k, &fro[2]);
-    if (!exact) {
-      rows_gemm<C>(S, QA_n, ld, olo, prow(fbuf, olo), pld, nt, QA, ld, k, k, &fro[1]);
-      rows_gemm<C>(S, QB_n, ld, olo, prow(gbuf, olo), pld, nt, QB, ld, k, k, &fro[3]);
-    } else {
+    {
+      const GemmJob jobs[4] = {{PTA_n, prow(0, olo), PTA, &fro[0]},
+                               {PTB_n, prow(3, olo), PTB, &fro[2]},
+                               {QA_n, prow(fbuf, olo), QA, &fro[1]},
+                               {QB_n, prow(gbuf, olo), QB, &fro[3]}};
+      rows_gemms<C>(S, jobs, exact ? 2 : 4, ld, olo, pld, nt, ld, k, k);
+    }
+    if (exact) {
       // exact inverses of the new projections (rank 0: side A, rank 1: side B),
       // then the row fixes y = x_cur P_new^-1 with x_cur = ex / ey / new row
       cl.sync();  // new P^T rows visible
@@ -1599,6 +1789,13 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     S.pp[0] = A.ctl->pp[0];
     S.pp[1] = A.ctl->pp[1];
     for (int i = 0; i < 3; ++i) S.lcnt3[i] = 0;  // fused-PPR counters
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&S.gbar[i])));
+      S.gq[i] = 0;
+    }
+    for (int i = 0; i < 3; ++i) S.gprof[i] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   cl.sync();  // counters zeroed before any CTA can append to them
@@ -1724,6 +1921,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
       break;
     }
   }
+#if DAMF_PROF
+  if (rank == 0 && threadIdx.x == 0)
+    for (int i = 0; i < 3; ++i) A.ctl->prof[28 + i] += (unsigned long long)S.gprof[i];
+#endif
 }
 
 // ------------------------------------------------------------------ launch

@@ -35,6 +35,8 @@ for alpha in alphas:
     out["eig_us_per_event"] = {nm: round(pc[16 + i] / 1.965e3 / (nev + 50), 2) for i, nm in enumerate(en)}
     pn = ["ppr.absorb", "ppr.smax", "ppr.cand0", "ppr.P1", "ppr.B1", "ppr.P2", "ppr.B2", "ppr.compact"]
     out["ppr_us_per_event"] = {nm: round(pc[23 + i] / 1.965e3 / (nev + 50), 2) for i, nm in enumerate(pn)}
+    out["staged_gemm_us_per_event"] = {nm: round(pc[28 + i] / 1.965e3 / (nev + 50), 2)
+                                       for i, nm in enumerate(["wait", "dmma", "whole_call"])}
     out["root_iters_mean"] = float(pc[13] / max(pc[14], 1))
     out["root_iters_max"] = int(pc[15])
     print(json.dumps(out))
