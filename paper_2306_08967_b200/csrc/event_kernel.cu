@@ -60,7 +60,7 @@ constexpr int PLD = 132;           // private-matrix row stride (d <= 128 in sme
 #define DAMF_GEMM_KU 8
 #endif
 constexpr int PCAP = 2048;         // fused-PPR candidate list entries kept in shared memory
-constexpr int GBUF_D = 4224;       // staging slot: 32 rows x 132 doubles (33 KB)
+constexpr int GBUF_D = 4224;       // GEMM staging slot: 32 rows x 132 doubles (33 KB)
 
 template <int C>
 struct Smem {
@@ -83,14 +83,17 @@ struct Smem {
   double bred[NW];
   long long found[C][2];          // graph row-scan results
   int lcnt3[3];                   // fused PPR: rows in this CTA's candidate lists (round mod 3)
-  int plist[3][PCAP];             // fused PPR: candidate lists (round mod 3); overflow in global
+  // The fused-PPR candidate lists live only inside an event's push and the
+  // GEMM staging ring only inside the factor update: one region serves both
+  // (keeps the carve-out small enough to leave L1 for the push's row reads)
+  union alignas(16) {
+    int plist[3][PCAP];           // fused PPR: candidate lists (round mod 3); overflow in global
+    double gbuf[2][GBUF_D];       // GEMM operand staging: two slots of chunk rows x ld doubles
+  };
   int K, nrot, need;
   int k, pp[2];
   int err;
-  // GEMM operand staging: chunks of the streamed matrix (rows x ld doubles,
-  // one bulk copy each) in a two-slot ring, completion on gbar[slot]
-  alignas(128) double gbuf[2][GBUF_D];
-  unsigned long long gbar[2];
+  unsigned long long gbar[2];     // GEMM staging: bulk-copy completion per slot
   unsigned gq[2];                 // completed phases per slot
   long long gprof[3];             // DAMF_PROF: staged-GEMM wait / DMMA / barrier cycles
 };
@@ -537,6 +540,28 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
   }
   const double dorg = kd[o];
   double tau = 0.5 * (lo + hi);
+  if (j < K - 1) {
+    // initial guess as in LAPACK dlaed4: the two nearest poles exact, the
+    // other terms frozen at the midpoint (C), i.e. the root of
+    // C + z_j^2/(d_j - l) + z_{j+1}^2/(d_{j+1} - l) = 0 (a quadratic); keeps
+    // the slow roots (tiny z, root hugging a pole) from starting at the midpoint
+    const double del = kd[j + 1] - kd[j], mid = 0.5 * del;
+    double sm = 0;  // sum at the midpoint over all terms (recomputed, cheap)
+    for (int i = gl; i < K; i += 16) sm += kz2[i] / ((kd[i] - kd[j]) - mid);
+    sm = gsum(sm, gm);
+    const double C = 1.0 / rho + sm + kz2[j] / mid - kz2[j + 1] / mid;
+    double g;
+    if (o == j) {
+      const double Aq = C * del + kz2[j] + kz2[j + 1], Bq = kz2[j] * del;
+      const double sq = sqrt(fabs(Aq * Aq - 4.0 * Bq * C));
+      g = Aq > 0.0 ? 2.0 * Bq / (Aq + sq) : (Aq - sq) / (2.0 * C);
+    } else {
+      const double Aq = C * del - kz2[j] - kz2[j + 1], Bq = kz2[j + 1] * del;
+      const double sq = sqrt(fabs(Aq * Aq + 4.0 * Bq * C));
+      g = Aq < 0.0 ? 2.0 * Bq / (Aq - sq) : -(Aq + sq) / (2.0 * C);
+    }
+    if (g > lo && g < hi) tau = g;
+  }
   int it = 0;
   for (; it < 120; ++it) {
     double psi = 0, phi = 0, dpsi = 0, dphi = 0, aerr = 0;
@@ -1074,8 +1099,20 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     PROF_MARK(4);
     // E columns t (rows of E^T, private): E^T[t] = sum_e Q2^T[t][e] Q1^T[e]
     {
+      // columns [0, n & ~7) on the tensor cores (full 8-column tiles: no
+      // third tile group per warp for the one column of the (k+1)-th
+      // direction); the last n % 8 columns by warp dot products
+      const int jm = n & ~7, nt = ohi - olo;
       const GemmJob job = {PB[1], PB[0], A.ws_Q1T, nullptr};
-      rows_gemms<C>(S, &job, 1, pld, 0, pld, ohi - olo, ld, n, n);
+      rows_gemms<C>(S, &job, 1, pld, 0, pld, nt, ld, n, jm);
+      for (int x = warp; x < nt * (n - jm); x += NW) {
+        const int r = x / (n - jm), j = jm + x % (n - jm);
+        double acc = 0.0;
+        for (int e = lane; e < n; e += 32) acc += PB[0][(int64_t)r * pld + e] * A.ws_Q1T[(int64_t)e * ld + j];
+        acc = warp_sum(acc);
+        if (lane == 0) PB[1][(int64_t)r * pld + j] = acc;
+      }
+      __syncthreads();
     }
   } else {
     for (int x = tid; x < (ohi - olo) * n; x += NT) {
@@ -1646,51 +1683,32 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     __syncthreads();
     if (tid == 0) S.lcnt3[old] = 0;  // next filled in round rr + 1 (after this round's barrier)
     int myF = 0;
-    // Candidates are evaluated four per warp at a time (8-lane groups, one
-    // row each: the loads of four rows are in flight together); most are
-    // below threshold and only get their key stored. The whole warp then
-    // pushes the group's rows that are over it, one after another.
-    for (int q0 = warp * 4; q0 < mycnt; q0 += NW * 4) {
-      const int grp = lane >> 3, gl = lane & 7;
-      const int qg = q0 + grp;
-      int vg = -1;
-      bool pg = false;
-      if (qg < mycnt)
-        vg = (rr > 0 && qg < PCAP) ? S.plist[cur][qg] : lists[cur][(int64_t)rank * stride + qg];
-      if (rr == 0) {
-        pg = vg >= 0 && A.key[vg] > thr;
-      } else {
-        float mg = 0.0f;
-        if (vg >= 0) {
-          const float* rg = A.rb + (int64_t)vg * d;
-#pragma unroll
-          for (int t = 0; t < kMaxD / 8; ++t) {
-            const int j = gl + 8 * t;
-            if (j < k) mg = fmaxf(mg, fabsf(rg[j]));
-          }
-        }
-        mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, 1));
-        mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, 2));
-        mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, 4));
-        if (vg >= 0) {
-          const float keyg = (float)((double)mg / fmax(A.deg[vg], 1.0));
-          pg = keyg > thr;
-          if (!pg && gl == 0) A.key[vg] = keyg;
-        }
-      }
-      const unsigned pmask = __ballot_sync(0xffffffffu, pg && gl == 0);
-      for (unsigned pm = pmask; pm; pm &= pm - 1) {
-      const int v = __shfl_sync(0xffffffffu, vg, __ffs(pm) - 1);
+    for (int q = warp; q < mycnt; q += NW) {
+      const int v = (rr > 0 && q < PCAP) ? S.plist[cur][q] : lists[cur][(int64_t)rank * stride + q];
+      // independent loads of the candidate, issued together
       const float* rv0 = A.rb + (int64_t)v * d;
       float* zu = A.Zb + (int64_t)v * d;
       float rj[kMaxD / 32], zj[kMaxD / 32];
 #pragma unroll
       for (int t = 0; t < kMaxD / 32; ++t) {
         const int j = lane + 32 * t;
+        rj[t] = j < k ? rv0[j] : 0.0f;
         zj[t] = j < k ? zu[j] : 0.0f;
       }
+      const double degv = A.deg[v];
+      const float keyv = rr == 0 ? A.key[v] : 0.0f;
       const int64_t ib = in.off[v];
       const int c = in.cnt[v];
+      float m = 0.0f;
+#pragma unroll
+      for (int t = 0; t < kMaxD / 32; ++t) m = fmaxf(m, fabsf(rj[t]));
+      m = warp_max(m);
+      const float key = (float)((double)m / fmax(degv, 1.0));
+      const bool push = rr == 0 ? keyv > thr : key > thr;
+      if (!push) {
+        if (lane == 0) A.key[v] = key;
+        continue;
+      }
       // first 32 in-arcs issued alongside the read-and-zero of r[u]
       int vv0 = -1;
       float w0 = 1.0f;
@@ -1743,7 +1761,6 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
         }
       }
     }
-    }
     if (lane == 0) s_cnt[warp] = myF;
     __syncthreads();
     int nF = 0;
@@ -1778,7 +1795,10 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
 }
 
 // ------------------------------------------------------------------ kernel
-template <int C>
+// FUSED: the per-event PPR push runs in the cluster after each event's
+// factor update (alpha < 1 on graphs up to 1 M rows); the factor-only
+// instantiation (alpha = 1, or the whole-GPU push afterwards) has no push code.
+template <int C, bool FUSED>
 __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<C>& S = *reinterpret_cast<Smem<C>*>(smem_raw);
@@ -1908,7 +1928,7 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
         rank1_step<C>(A, S, cl, st);
       }
     }
-    if (A.fused_ppr) {
+    if (FUSED) {
       cl.sync();  // factor / graph writes visible to the enhancer
       ppr_event<C>(A, S, cl, ev);
     }
@@ -1928,16 +1948,16 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
 }
 
 // ------------------------------------------------------------------ launch
-template <int C>
-static cudaError_t launch_c(const EventKernelArgs& a, cudaStream_t s) {
+template <int C, bool FUSED>
+static cudaError_t launch_cf(const EventKernelArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(Smem<C>);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(damf_event_kernel<C>,
+    cudaError_t e = cudaFuncSetAttribute(damf_event_kernel<C, FUSED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (C > 8) {
-      e = cudaFuncSetAttribute(damf_event_kernel<C>,
+      e = cudaFuncSetAttribute(damf_event_kernel<C, FUSED>,
                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
@@ -1955,7 +1975,11 @@ static cudaError_t launch_c(const EventKernelArgs& a, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, damf_event_kernel<C>, a);
+  return cudaLaunchKernelEx(&cfg, damf_event_kernel<C, FUSED>, a);
+}
+template <int C>
+static cudaError_t launch_c(const EventKernelArgs& a, cudaStream_t s) {
+  return a.fused_ppr ? launch_cf<C, true>(a, s) : launch_cf<C, false>(a, s);
 }
 
 int event_cluster_size() {
@@ -1964,9 +1988,9 @@ int event_cluster_size() {
   // Prefer 16 CTAs (non-portable) when the device can co-schedule it.
   int c16 = 0;
   {
-    cudaFuncSetAttribute(damf_event_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(damf_event_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(Smem<16>));
-    cudaFuncSetAttribute(damf_event_kernel<16>,
+    cudaFuncSetAttribute(damf_event_kernel<16, true>,
                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16, 1, 1);
@@ -1979,7 +2003,7 @@ int event_cluster_size() {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&c16, damf_event_kernel<16>, &cfg) != cudaSuccess) c16 = 0;
+    if (cudaOccupancyMaxActiveClusters(&c16, damf_event_kernel<16, true>, &cfg) != cudaSuccess) c16 = 0;
     cudaGetLastError();
   }
   chosen = c16 > 0 ? 16 : 8;
