@@ -340,6 +340,8 @@ def bench_materialize(args, hbm, peak_kind):
             except Exception:
                 bf16 = 2250.0
             tf = 3 * 2.0 * n * d * d / (t * 1e-3) / 1e12
+            res["d256"]["traffic"] = ncu_traffic("r1_mat256_raw.csv", "materialize_bf16_256")
+            res["d256"]["traffic_source"] = "profiles/r1_mat256_raw.csv (ncu --set full, same shape)"
             res["d256"]["tensor_side"] = {"passes": "3 x bf16 (hi*hi + hi*lo + lo*hi)",
                                           "achieved_bf16_TFLOPs": round(tf, 1),
                                           "peak_bf16_TFLOPs": round(bf16, 1), "frac": round(tf / bf16, 4)}
