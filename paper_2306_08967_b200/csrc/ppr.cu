@@ -66,6 +66,9 @@ DAMF_D float row_key(const float* r, int k, double deg) {
 
 constexpr int HEAVY = PPR_HEAVY;
 constexpr int CH = PPR_CH;
+#ifndef DAMF_PROF
+#define DAMF_PROF 0  // phase timers (tools/prof_ppr.py builds with make EXTRA=-DDAMF_PROF=1)
+#endif
 #ifndef PPR_G
 #define PPR_G 16
 #endif
@@ -703,11 +706,13 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
   int rounds = resume ? A.pst->rounds : 0;
   int cur = resume ? A.pst->cur : 0;  // items[cur]: rows touched by this round's scatter
   bool split_exit = false;
-  // per-phase wall time (block 0 thread 0, %globaltimer ns) -> ctl->prof[24..28]
+  // per-phase wall time (block 0 thread 0, %globaltimer ns) -> ctl->prof[24..28],
+  // only in DAMF_PROF builds: the global read-modify-write would otherwise sit
+  // on block 0's path into every phase
   const bool tl = blockIdx.x == 0 && threadIdx.x == 0;
-  unsigned long long tp = tl ? globaltimer() : 0;
+  unsigned long long tp = (DAMF_PROF && tl) ? globaltimer() : 0;
   auto tmark = [&](int slot) {
-    if (tl) {
+    if (DAMF_PROF && tl) {
       const unsigned long long t = globaltimer();
       A.ctl->prof[slot] += t - tp;
       tp = t;

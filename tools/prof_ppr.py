@@ -1,5 +1,6 @@
 """Dev driver: per-phase wall time of the whole-GPU PPR push (ctl->prof[24..28])
-for init_propagate and a push after 1,000 structure-only insertions."""
+for init_propagate and a push after 1,000 structure-only insertions.
+Phase timers need the library built with `make EXTRA=-DDAMF_PROF=1`."""
 import sys, os, math, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
