@@ -806,7 +806,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
       CK(dalloc(h, &h->pst, (size_t)1));
       CK(cudaMemsetAsync(h->pst, 0, sizeof(PprState), h->st));
       CK(cudaMallocHost(&h->h_pst, sizeof(PprState)));
-      CK(dalloc(h, &h->mitems, 2 * ((size_t)ncap + (size_t)(h->out.pool_size / 512) + 4096)));
+      CK(dalloc(h, &h->mitems, 2 * ((size_t)ncap + (size_t)(h->out.pool_size / PPR_MCH) + 4096)));
       CK(dalloc(h, &h->hdone, nh));
       CK(cudaMemsetAsync(h->hdone, 0, nh * 4, h->st));
       CK(dalloc(h, &h->items0, (size_t)ncap + chunks + 4096));

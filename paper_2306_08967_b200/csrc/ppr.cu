@@ -577,7 +577,7 @@ DAMF_D void dense_pull(const PprArgs& A, unsigned long long* wq, int R, int nchu
     }
 }
 
-constexpr int MCH = 512;  // in-arcs per scatter item
+constexpr int MCH = PPR_MCH;  // in-arcs per scatter item (ppr.cuh)
 
 // One cooperative kernel runs every round of the push with grid barriers.
 // Each round:
@@ -718,7 +718,9 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
       tp = t;
     }
   };
+  unsigned long long tr0 = 0;  // DAMF_PROF: round start (block 0 thread 0)
   for (;;) {
+    if (DAMF_PROF && tl) tr0 = globaltimer();
     ++R;
     const int par = R & 1;
     unsigned long long* pushc = &sc[(SC_PUSH + R % 3) * QS];
@@ -757,10 +759,24 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(&sc[(SC_MITEMS + par) * QS], (unsigned long long)all);
       base = __shfl_sync(0xffffffffu, base, 0);
-      const unsigned long long pos = base + tot - nit;
-      for (int i = 0; i < nit; ++i) {
-        A.mitems[2 * (pos + i)] = u;
-        A.mitems[2 * (pos + i) + 1] = i;
+      // the whole warp writes the items (a hub's in-list is thousands of
+      // items: one lane alone would hold its round up); item idx belongs to
+      // the last lane whose exclusive offset is <= idx
+      const int excl = tot - nit;
+      for (int b = 0; b < all; b += 32) {
+        const int idx = b + lane;
+        int l = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int e = __shfl_sync(0xffffffffu, excl, (l + step) & 31);
+          if (l + step < 32 && e <= idx) l += step;
+        }
+        const int uo = __shfl_sync(0xffffffffu, u, l);
+        const int eo = __shfl_sync(0xffffffffu, excl, l);
+        if (idx < all) {
+          A.mitems[2 * (base + idx)] = uo;
+          A.mitems[2 * (base + idx) + 1] = idx - eo;
+        }
       }
       return c;
     };
@@ -867,6 +883,9 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
       t[1] = dense;
       t[2] = S;
       t[3] = nmi;
+      // DAMF_PROF builds: push-phase ns in the high half of t[3], round ns
+      // in t[1] >> 1 (added at the end of the round)
+      if (DAMF_PROF) t[3] |= (long long)((globaltimer() - tr0) << 32);
     }
     if (dense && A.split) {
       // hand the round to the lean pull kernel (more warps per SM than this
@@ -898,6 +917,18 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
           const int u = A.mitems[2 * it], ci = A.mitems[2 * it + 1];
           const int64_t ib = inC.off[u];
           const int beg = ci * MCH, end = min(beg + MCH, inC.cnt[u]);
+          // Random-row reductions that miss L2 run at ~80 GB/s (each one waits
+          // for its line from DRAM inside the atomic unit): first pull this
+          // item's target rows into L2 with bulk prefetches (all in flight at
+          // once), then reduce into L2-resident lines.
+          for (int p0 = beg; p0 < end; p0 += 32) {
+            const int p = p0 + lane;
+            if (p < end) {
+              const float* row = A.rb + (int64_t)inC.ids[ib + p] * d;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((unsigned)(k * 4 + 15) & ~15u)
+                           : "memory");
+            }
+          }
           float x[CL::NE];
           CL::load(A.delta + (int64_t)u * d, gl, k, x);
           if (lane == 0) c_arcs += end - beg;
@@ -911,7 +942,9 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
               const double w = inC.wts ? inC.wts[ib + p] : 1.0;
               coef = (float)(om * w / fmax(A.deg[v], 1.0));
             }
-            const bool t = ok && atomicExch(&A.mark[v], R) != R;
+            // first toucher appends v; a plain L2 read first keeps the many
+            // pushers of a hub's neighbours off the same returning atomic
+            const bool t = ok && __ldcg(&A.mark[v]) != R && atomicExch(&A.mark[v], R) != R;
             const unsigned tm = __ballot_sync(0xffffffffu, t);
             if (tm) {
               unsigned long long b0 = 0;
@@ -952,6 +985,8 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
     }
     g.sync();
     tmark(dense ? 26 : 27);
+    if (DAMF_PROF && tl && A.trace && rounds <= 1024)
+      A.trace[4 * (rounds - 1) + 1] |= (long long)((globaltimer() - tr0) << 1);
     const int ntouched = dense ? 0 : (int)*(volatile unsigned long long*)&sc[(SC_ITEMS + par) * QS];
     if (blockIdx.x == 0) {
       if (threadIdx.x < NQ) {

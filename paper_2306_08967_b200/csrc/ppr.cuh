@@ -5,6 +5,11 @@ namespace dgpu {
 
 constexpr int PPR_HEAVY = 256;  // rows with more out-arcs are pulled in chunks
 constexpr int PPR_CH = 256;     // arcs per chunk
+// In-arcs per scatter item. Short items spread a pushed row's in-list over
+// many warps: a warp issues its reductions back to back, so one 512-arc item
+// kept a warp busy for ~0.2 ms and set the length of its round (R-MAT scale
+// 23, push after 1,000 inserts: 3.4 ms at 512, 1.8 at 64, 1.4 at 32/16/8).
+constexpr int PPR_MCH = 32;
 
 // Cross-launch state of a push split into cooperative rounds + standalone
 // dense-pull launches (damf_gpu_ppr_init / _push).

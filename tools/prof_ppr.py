@@ -30,7 +30,9 @@ def run(label, fn):
     tr = np.zeros(4 * 1024, np.int64)
     r = ge.lib().damf_gpu_ppr_trace(e.h, tr.ctypes.data_as(C.c_void_p), 1024)
     tr = tr[:4 * max(r, 0)].reshape(-1, 4)
-    print("   rounds (nF, dense, items, heavy):", ";".join(f"{a},{b},{c},{d_}" for a, b, c, d_ in tr.tolist()))
+    print("   rounds (nF, dense, items, scatter items[, push us, round us]):")
+    print("   " + ";".join(f"{a},{b & 1},{c},{d_ & 0xffffffff}" + (f",{(d_ >> 32) / 1e3:.1f},{(b >> 1) / 1e3:.1f}" if (b >> 1) else "")
+                         for a, b, c, d_ in tr.tolist()))
     for s, nm in names.items():
         print(f"   {nm:14s} {(int(p1[s]) - int(p0[s]))/1e6:9.3f} ms")
 run("init", e.ppr_init)
