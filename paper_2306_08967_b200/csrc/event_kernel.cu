@@ -275,9 +275,12 @@ DAMF_D void stage_chunk(Smem<C>& S, int slot, const double* src, unsigned bytes)
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
-template <int C, int MT, int TPW>
-__device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0, int ldc, int nt,
-                             int ldi, int M, int J) {
+// KF > 0: shapes fixed at compile time (M = J = KF, ldi = ldc = KF + 4, the
+// k = 128 update GEMMs), so the chunk loops unroll without predicates.
+template <int C, int MT, int TPW, int KF>
+__device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0,
+                                              int ldc_, int nt, int ldi_, int M_, int J_) {
+  const int ldc = KF ? KF + 4 : ldc_, ldi = KF ? KF + 4 : ldi_, M = KF ? KF : M_, J = KF ? KF : J_;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ar = lane >> 2, ac = lane & 3;
   const int ntiles = (J + 7) >> 3;
@@ -334,7 +337,7 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
 #endif
     const double* sb = S.gbuf[slot];
     const double* Coef = jobs[j].Coef;
-    const int m0 = c * CR, rows = min(CR, M - m0);
+    const int m0 = c * CR, rows = (KF && KF % CR == 0) ? CR : min(CR, M - m0);
     for (int mm = 0; mm < rows; mm += 16) {
       // operands of four k-steps loaded before their DMMAs
       double a[4][MT], b[4][TPW];
@@ -404,12 +407,14 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
 template <int C>
 DAMF_D void rows_gemms(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0, int ldc, int nt,
                        int ldi, int M, int J) {
-  if (nt <= 8 && J <= 128)
-    rows_gemm_staged<C, 1, 2>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
+  if (nt <= 8 && M == 128 && J == 128 && ldi == 132 && ldc == 132)
+    rows_gemm_staged<C, 1, 2, 128>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
+  else if (nt <= 8 && J <= 128)
+    rows_gemm_staged<C, 1, 2, 0>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
   else if (nt <= 16 && J <= 128)
-    rows_gemm_staged<C, 2, 2>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
+    rows_gemm_staged<C, 2, 2, 0>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
   else if (nt <= 16 && J <= 256)
-    rows_gemm_staged<C, 2, 4>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
+    rows_gemm_staged<C, 2, 4, 0>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
   else
     for (int j = 0; j < nj; ++j)
       rows_gemm<C>(S, jobs[j].Out, ldo, o0, jobs[j].Coef, ldc, nt, jobs[j].In, ldi, M, J, jobs[j].fro);
