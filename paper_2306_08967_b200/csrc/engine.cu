@@ -202,6 +202,10 @@ struct damf_gpu {
   int nsm = 148;
   DevCtl* ctl = nullptr;
   DevCtl* h_ctl = nullptr;  // pinned
+  // h_ctl / h_pstats mirror the device exactly: set by sync_ctl, cleared by
+  // every entry point that may enqueue device work (apply skips its
+  // pre-launch round trip when the mirror is fresh)
+  bool ctl_fresh = false;
   float *Xb = nullptr, *Yb = nullptr, *Zb = nullptr, *rb = nullptr, *delta = nullptr,
         *key = nullptr;
   int *stamp = nullptr, *mark = nullptr, *listF = nullptr, *listL = nullptr, *blk = nullptr;
@@ -403,6 +407,7 @@ int sync_ctl(damf_gpu* h) {
   CK(cudaStreamSynchronize(h->st));
   h->k = h->h_ctl->k;
   h->round_base = (int)h->h_pstats[2];
+  h->ctl_fresh = true;
   return 0;
 }
 
@@ -445,6 +450,7 @@ const char* damf_gpu_version(void) { return "damf_gpu sm_100a (cluster update, S
 const char* damf_gpu_last_error(const damf_gpu* h) { return h ? h->err.c_str() : "null handle"; }
 
 int damf_gpu_sync(damf_gpu* h) {
+  if (h) h->ctl_fresh = false;
   CK(cudaStreamSynchronize(h->st));
   return 0;
 }
@@ -836,6 +842,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
 }
 
 int damf_gpu_ppr_init(damf_gpu* h, damf_apply_stats* stats) {
+  if (h) h->ctl_fresh = false;
   if (h->alpha1) return 0;
   if (int r = sync_ctl(h)) return r;
   PprArgs a = ppr_args(h);
@@ -853,6 +860,7 @@ int damf_gpu_ppr_init(damf_gpu* h, damf_apply_stats* stats) {
 }
 
 int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
+  if (h) h->ctl_fresh = false;
   if (h->alpha1) return 0;
   if (int r = sync_ctl(h)) return r;
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
@@ -867,6 +875,7 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
 }
 
 int damf_gpu_rebase(damf_gpu* h) {
+  if (h) h->ctl_fresh = false;
   if (int r = sync_ctl(h)) return r;
   const int k = h->k, d = h->d, ld = h->ld;
   // folds use fp64 accumulation: P may be ill-conditioned here (cond up to
@@ -1103,7 +1112,8 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     CK(cudaMalloc(&h->t_begin, h->t_cap * 8));
     CK(cudaMalloc(&h->t_end, h->t_cap * 8));
   }
-  if (int r = sync_ctl(h)) return r;
+  if (!h->ctl_fresh)
+    if (int r = sync_ctl(h)) return r;
   const long long rank1_0 = h->h_ctl->rank1, folds0 = h->h_ctl->folds;
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
   EventKernelArgs ea = event_args(h);
@@ -1123,6 +1133,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     // when only absorption is requested; otherwise one cooperative push
     // kernel per event over the whole GPU.
     const bool fused = ppr && (h->n_cap <= (1 << 20) || (mode & DAMF_APPLY_DEFER_PUSH));
+    h->ctl_fresh = false;
     if (!ppr || fused) {
       ea.e_begin = i;
       ea.e_end = j;
@@ -1165,7 +1176,8 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     }
     i = done;
   }
-  if (int r = sync_ctl(h)) return r;
+  if (!h->ctl_fresh)
+    if (int r = sync_ctl(h)) return r;
   int status = 0;
   if (h->h_ctl->err) {
     const int64_t fe = h->h_ctl->err_event;
@@ -1226,6 +1238,7 @@ int64_t damf_gpu_event_latencies(damf_gpu* h, double* out, int64_t max) {
 }
 
 int damf_gpu_load_rows(damf_gpu* h, int32_t which, int64_t row0, int64_t m, const float* src) {
+  if (h) h->ctl_fresh = false;
   if (!h) return DAMF_E_SHAPE_MISMATCH;
   if (which != DAMF_XB && which != DAMF_YB)
     return fail(h, DAMF_E_SHAPE_MISMATCH, "load_rows: which must be DAMF_XB or DAMF_YB");
@@ -1360,6 +1373,7 @@ int damf_gpu_score(damf_gpu* h, int64_t u, int64_t v, int32_t enhanced, double* 
 }
 
 int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_device) {
+  if (h) h->ctl_fresh = false;
   if (int r = sync_ctl(h)) return r;
   const float* base = which == DAMF_Y ? h->Yb : which == DAMF_Z ? h->Zb : h->Xb;
   const double* PT = live_PT(h, which == DAMF_Y ? 1 : 0);
