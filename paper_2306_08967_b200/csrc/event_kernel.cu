@@ -142,6 +142,25 @@ DAMF_D void own_range(int k, int n, int C, int rank, int& lo, int& hi) {
   if (rank == C - 1) hi = n;
 }
 
+template <int C>
+DAMF_D long long block_max_ll(Smem<C>& S, long long v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = x > v ? x : v;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) S.bred[threadIdx.x >> 5] = __longlong_as_double(v);
+  __syncthreads();
+  long long m = -1;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const long long x = __double_as_longlong(S.bred[w]);
+    m = x > m ? x : m;
+  }
+  __syncthreads();
+  return m;
+}
+
 // ------------------------------------------------------------- row GEMM
 // FP64 tensor-core MMA (DMMA): D[8x8] += A[8x4] (row) * B[4x8] (col).
 // Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane>>2][lane&3],
@@ -888,6 +907,14 @@ DAMF_D long long find_arc(Smem<C>& S, cg::cluster_group& cl, const DevCSR& g, in
   const int rank = (int)cl.block_rank();
   const long long cnt = g.cnt[u];
   const int64_t base = g.off[u];
+  if (cnt <= 4 * NT) {
+    // short row: every CTA scans all of it (same answer everywhere), no
+    // cluster barrier
+    long long pos = -1;
+    for (long long p = threadIdx.x; p < cnt; p += NT)
+      if (g.ids[base + p] == (int32_t)v) pos = p;
+    return block_max_ll<C>(S, pos);
+  }
   const long long per = (cnt + C - 1) / C;
   const long long lo = min(cnt, (long long)rank * per), hi = min(cnt, lo + per);
   long long pos = -1;
