@@ -1717,6 +1717,11 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     int myF = 0;
     for (int q = warp; q < mycnt; q += NW) {
       const int v = (rr > 0 && q < PCAP) ? S.plist[cur][q] : lists[cur][(int64_t)rank * stride + q];
+      // key[v] is an upper bound of |r_v|_inf / max(deg v, 1) (see the
+      // scatter below); read it before r, fenced, so every scatter increment
+      // it includes is also in the r read
+      const float K0 = __ldcg(&A.key[v]);
+      __threadfence();
       // independent loads of the candidate, issued together
       const float* rv0 = A.rb + (int64_t)v * d;
       float* zu = A.Zb + (int64_t)v * d;
@@ -1728,7 +1733,6 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
         zj[t] = j < k ? zu[j] : 0.0f;
       }
       const double degv = A.deg[v];
-      const float keyv = rr == 0 ? A.key[v] : 0.0f;
       const int64_t ib = in.off[v];
       const int c = in.cnt[v];
       float m = 0.0f;
@@ -1736,9 +1740,10 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
       for (int t = 0; t < kMaxD / 32; ++t) m = fmaxf(m, fabsf(rj[t]));
       m = warp_max(m);
       const float key = (float)((double)m / fmax(degv, 1.0));
-      const bool push = rr == 0 ? keyv > thr : key > thr;
+      const bool push = key > thr;
       if (!push) {
-        if (lane == 0) A.key[v] = key;
+        // exact key of the state read, plus whatever was added since K0
+        if (lane == 0) atomicAdd(&A.key[v], key - K0);
         continue;
       }
       // first 32 in-arcs issued alongside the read-and-zero of r[u]
@@ -1757,12 +1762,18 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
           zu[j] = zj[t] + rj[t];
         }
       }
-      if (lane == 0) A.key[v] = 0.0f;
+      // r_v now holds only what arrived after the exchange: drop the part K0
+      // bounded, keep later increments
+      if (lane == 0) atomicAdd(&A.key[v], -K0);
       ++myF;
+      float dmax = 0.0f;  // |delta|_inf of this push
+#pragma unroll
+      for (int t = 0; t < kMaxD / 32; ++t) dmax = fmaxf(dmax, fabsf(rj[t]));
+      dmax = warp_max(dmax);
       for (int p0 = 0; p0 < c; p0 += 32) {
         const int p = p0 + lane;
         int vv = -1;
-        float cf = 0.0f;
+        float cf = 0.0f, inc = 0.0f;
         if (p < c) {
           float w = w0;
           vv = vv0;
@@ -1770,15 +1781,10 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
             vv = in.ids[ib + p];
             w = in.wts ? (float)in.wts[ib + p] : 1.0f;
           }
-          cf = (float)(om * w / fmax(A.deg[vv], 1.0));
-          if (atomicExch(&A.mark[vv], R + 1) != R + 1) {
-            const int ow = (vv >> 5) % C;
-            const int pos = atomicAdd(cl.map_shared_rank(&S.lcnt3[nxt], ow), 1);
-            if (pos < PCAP)
-              *cl.map_shared_rank(&S.plist[nxt][pos], ow) = vv;
-            else
-              lists[nxt][(int64_t)ow * stride + pos] = vv;
-          }
+          const double dg = fmax(A.deg[vv], 1.0);
+          cf = (float)(om * w / dg);
+          // bound of the key increase of vv (1e-4 slack for fp32 rounding)
+          inc = (float)(fabs(om * w) / (dg * dg) * (double)dmax * (1.0 + 1e-4));
         }
         const int cnt = min(32, c - p0);
         for (int s2 = 0; s2 < cnt; ++s2) {
@@ -1789,6 +1795,21 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
           for (int t = 0; t < kMaxD / 32; ++t) {
             const int j = lane + 32 * t;
             if (j < k) atomicAdd(rt + j, cc * rj[t]);  // RED.ADD.F32
+          }
+        }
+        // Candidates for the next round are only the targets whose key bound
+        // crosses the threshold (a target under it cannot be over it); the
+        // contributions are ordered before the bound update.
+        __threadfence();
+        if (p < c) {
+          const float kb = atomicAdd(&A.key[vv], inc) + inc;
+          if (kb > thr && atomicExch(&A.mark[vv], R + 1) != R + 1) {
+            const int ow = (vv >> 5) % C;
+            const int pos = atomicAdd(cl.map_shared_rank(&S.lcnt3[nxt], ow), 1);
+            if (pos < PCAP)
+              *cl.map_shared_rank(&S.plist[nxt][pos], ow) = vv;
+            else
+              lists[nxt][(int64_t)ow * stride + pos] = vv;
           }
         }
       }
