@@ -206,6 +206,14 @@ struct damf_gpu {
   // every entry point that may enqueue device work (apply skips its
   // pre-launch round trip when the mirror is fresh)
   bool ctl_fresh = false;
+  // Rows whose residual changed since the last completed push (absorbed
+  // structure-only events with a deferred push). While pend_valid, every
+  // other row's key is at most the threshold (nothing else changed r, deg or
+  // s_max), so damf_gpu_ppr_push can start from these rows instead of
+  // checking every key.
+  std::vector<int32_t> pend;
+  bool pend_valid = false;
+  int32_t* pend_d = nullptr;
   float *Xb = nullptr, *Yb = nullptr, *Zb = nullptr, *rb = nullptr, *delta = nullptr,
         *key = nullptr;
   int *stamp = nullptr, *mark = nullptr, *listF = nullptr, *listL = nullptr, *blk = nullptr;
@@ -419,12 +427,17 @@ double* live_Q(damf_gpu* h, int side) { return h->Q[side][h->h_ctl->pp[side]]; }
 // split = 1 (whole-graph calls): dense pull rounds run as a standalone
 // kernel with more warps per SM; the cooperative kernel exits before such a
 // round and is relaunched after it (one small host read per dense round).
-int run_push(damf_gpu* h, int grid, unsigned long long* t_end, int split = 0) {
+int run_push(damf_gpu* h, int grid, unsigned long long* t_end, int split = 0,
+             const int32_t* cand = nullptr, int ncand = -1) {
   h->launches += 2;
   CK(launch_smax(h->PT[0][0], h->PT[0][1], h->ctl, h->ld, h->smax, h->st));
   PprArgs a = ppr_args(h);
   a.t_end = t_end;
   a.split = split;
+  if (cand) {
+    a.cand = const_cast<int32_t*>(cand);
+    a.ncand = ncand;
+  }
   const int gmax = ppr_push_max_grid(h->nsm, h->d);
   for (;;) {
     CK(launch_ppr_push(a, std::min(grid, gmax), h->st));
@@ -796,6 +809,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
     CK(dalloc(h, &h->listF, (size_t)ncap + 16 * 32 * 2 + 4096));
     CK(dalloc(h, &h->listG, (size_t)ncap + 16 * 32 * 2 + 4096));
     CK(dalloc(h, &h->listL, (size_t)ncap + 16 * 32 * 2 + 4096));
+    CK(dalloc(h, &h->pend_d, (size_t)ncap / 16 + 16));  // damf_gpu_ppr_push's starting rows
     CK(dalloc(h, &h->blk, (size_t)4096));
     CK(dalloc(h, &h->blk64, (size_t)4096));
     {
@@ -849,9 +863,12 @@ int damf_gpu_ppr_init(damf_gpu* h, damf_apply_stats* stats) {
   CK(launch_ppr_init(a, h->nsm, h->st));
   CK(launch_ppr_keys(a, h->nsm, h->st));
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
+  h->pend.clear();
+  h->pend_valid = false;
   if (int r = run_push(h, 1 << 20, nullptr, 1)) return r;
   if (int r = sync_ctl(h)) return r;
   if (h->h_ctl->err) return fail(h, h->h_ctl->err, "push_to_tolerance: push budget exceeded");
+  h->pend_valid = true;
   if (stats) {
     stats->pushes = h->h_pstats[0] - p0;
     stats->push_rounds = h->h_pstats[1] - r0;
@@ -864,9 +881,22 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
   if (h->alpha1) return 0;
   if (int r = sync_ctl(h)) return r;
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
-  if (int r = run_push(h, 1 << 20, nullptr, 1)) return r;
+  const int32_t* cand = nullptr;
+  int ncand = -1;
+  if (h->pend_valid && h->pend_d && (int64_t)h->pend.size() * 16 < h->n) {
+    std::sort(h->pend.begin(), h->pend.end());
+    h->pend.erase(std::unique(h->pend.begin(), h->pend.end()), h->pend.end());
+    if (!h->pend.empty())
+      CK(cudaMemcpyAsync(h->pend_d, h->pend.data(), h->pend.size() * 4, cudaMemcpyHostToDevice, h->st));
+    cand = h->pend_d;
+    ncand = (int)h->pend.size();
+  }
+  h->pend.clear();
+  h->pend_valid = false;
+  if (int r = run_push(h, 1 << 20, nullptr, 1, cand, ncand)) return r;
   if (int r = sync_ctl(h)) return r;
   if (h->h_ctl->err) return fail(h, h->h_ctl->err, "push_to_tolerance: push budget exceeded");
+  h->pend_valid = true;
   if (stats) {
     stats->pushes = h->h_pstats[0] - p0;
     stats->push_rounds = h->h_pstats[1] - r0;
@@ -876,6 +906,7 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
 
 int damf_gpu_rebase(damf_gpu* h) {
   if (h) h->ctl_fresh = false;
+  if (h) h->pend_valid = false;  // r <- r T and re-keyed: keys may exceed the threshold
   if (int r = sync_ctl(h)) return r;
   const int k = h->k, d = h->d, ld = h->ld;
   // folds use fp64 accumulation: P may be ill-conditioned here (cond up to
@@ -1220,6 +1251,20 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     }
     h->lat_us.resize(m);
     for (int64_t e = 0; e < m; ++e) h->lat_us[e] = (double)(te[e] - tb[e]) * 1e-3;
+  }
+  if (!h->alpha1) {
+    if (!(mode & DAMF_APPLY_DEFER_PUSH)) {
+      // every event was pushed to tolerance (fused or whole-GPU)
+      h->pend.clear();
+      h->pend_valid = status == 0;
+    } else if (!(mode & DAMF_APPLY_GRAPH_AND_PPR_ONLY)) {
+      h->pend_valid = false;  // factor updates moved s_max: every key must be re-checked
+    } else if (h->pend_valid) {
+      for (int64_t e = 0; e < s.applied; ++e) {
+        const EventDesc& ed = h->ev.h[e];
+        for (int64_t t = 0; t < ed.touched_cnt; ++t) h->pend.push_back((int32_t)h->touched.h[ed.touched_off + t]);
+      }
+    }
   }
   s.rank1_updates = h->h_ctl->rank1 - rank1_0;
   s.eager_folds = h->h_ctl->folds - folds0;
