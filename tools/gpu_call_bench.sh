@@ -3,5 +3,5 @@ set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc $?"
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu --cfg5-events 2000 --cfg3-events 512 > gpurun_out/plain_bench_small.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --cfg5-events 2000 --cfg3-events 512 > gpurun_out/ncu_bench.log 2>&1; echo "ncu bench rc $?"
-python tools/prof_kernels.py ppr 23 > gpurun_out/plain_ppr.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/ppr23_launches.csv python tools/prof_kernels.py ppr 23 > gpurun_out/ncu_ppr.log 2>&1; echo "ncu ppr rc $?"
+echo "ppr launch list skipped (unchanged kernels)"
 python tools/prof_kernels.py events > gpurun_out/plain_ev.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:damf_event_kernel -s 1 -c 1 -o gpurun_out/evk_final python tools/prof_kernels.py events > gpurun_out/ncu_ev.log 2>&1; echo "ncu ev rc $?"
