@@ -1435,7 +1435,7 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
   const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
   if (h->h_ctl->cond_est <= kPreciseCond) {
     CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
-  } else if (nd >= 0 && nd <= kDirtyCap) {
+  } else if (nd >= 0 && nd <= kDirtyCap && h->k <= 128) {  // in-place fp64 rows: k <= 128
     const int k = h->k;
     CK(launch_materialize(base, h->n, k, h->d, PT, h->ld, k, out, k, h->st, h->nsm));
     if (nd > 0) {

@@ -129,3 +129,30 @@ def test_error_kinds_and_partial_application():
     with pytest.raises(ge.DamfError) as ex:
         e.apply(EventList.edges(ge.ADD_EDGE, [0], [10_000]))
     assert ex.value.kind == "UnknownNode"
+
+
+@pytest.mark.parametrize("d,alpha", [(192, 1.0), (256, 0.3)])
+def test_wide_rank_stream_matches_oracle(d, alpha):
+    # k > 128: the wide DMMA folds and the k > 128 query path (no in-place
+    # fp64 patch of dirty rows), against the oracle (update_engine.cpp:144-204)
+    from helpers import gpu_from_oracle, sampled_product_rel, sigma_rel
+    from paper_2306_08967_b200.workloads import EventList
+    g = oracle.gen_random_graph(600, 6000, 3, undirected=True)
+    oe = oracle.OracleEngine(g, d=d, alpha=alpha, eps=1e-5, seed=3)
+    e = gpu_from_oracle(g, oe, d=d, alpha=alpha, eps=1e-5)
+    rng = np.random.default_rng(1)
+    off, tgt, _ = g.csr()
+    pairs = []
+    while len(pairs) < 20:
+        a, b = (int(x) for x in rng.integers(0, g.n, 2))
+        if a != b and not np.any(tgt[off[a]:off[a + 1]] == b) and (a, b) not in pairs and (b, a) not in pairs:
+            pairs.append((a, b))
+    ev = oracle.Events.edges(1, [p[0] for p in pairs], [p[1] for p in pairs])
+    st = e.apply(EventList(*(getattr(ev, f) for f in ("kind", "u", "v", "w", "in_off", "in_ids", "in_w",
+                                                      "out_off", "out_ids", "out_w"))))
+    oe.apply(ev)
+    assert st["applied"] == len(pairs)
+    prel = sampled_product_rel(e.get(ge.X), e.get(ge.Y), oe.get(oe.X), oe.get(oe.Y))
+    srel = sigma_rel(e.get(ge.SIGMA), oe.get(oe.SIGMA))
+    print(d, alpha, "product", prel, "sigma", srel)
+    assert prel <= 1e-4 and srel <= 1e-6
