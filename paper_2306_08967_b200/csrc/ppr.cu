@@ -921,7 +921,8 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
           // for its line from DRAM inside the atomic unit): first pull this
           // item's target rows into L2 with bulk prefetches (all in flight at
           // once), then reduce into L2-resident lines.
-          for (int p0 = beg; p0 < end; p0 += 32) {
+          // (bulk prefetches need 16-byte aligned rows: d % 4 == 0)
+          for (int p0 = beg; (d & 3) == 0 && p0 < end; p0 += 32) {
             const int p = p0 + lane;
             if (p < end) {
               const float* row = A.rb + (int64_t)inC.ids[ib + p] * d;

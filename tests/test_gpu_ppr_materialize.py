@@ -252,3 +252,23 @@ def test_whole_gpu_push_closes_isolated_edges():
     print("push", st2, "defect", dfc, "pair err", perr, ns)
     assert dfc <= eps * (1 + 1e-6) + 2e-7
     assert perr <= 1e-5
+
+
+@pytest.mark.parametrize("d", [5, 13])
+def test_odd_rank_enhanced_stream(d):
+    # rows of d % 4 != 0 floats are not 16-byte aligned: the whole-GPU push's
+    # vector / bulk paths must stand aside (init_propagate, then a mixed
+    # directed stream with the fused push), checked against the oracle and
+    # the defect bound (eval.cpp:591-610)
+    from helpers import sampled_product_rel, sigma_rel
+    g, ev = oracle.gen_mixed_stream(260, 180, 1000, 120, 17 + d)
+    oe = oracle.OracleEngine(g, d=d, alpha=0.3, eps=1e-6, seed=d)
+    e = gpu_from_oracle(g, oe, d=d, alpha=0.3, eps=1e-6, node_capacity=128)
+    st = e.apply(EventList(*(getattr(ev, f) for f in ("kind", "u", "v", "w", "in_off", "in_ids", "in_w",
+                                                      "out_off", "out_ids", "out_w"))))
+    oe.apply(ev)
+    assert st["applied"] == len(ev)
+    assert sampled_product_rel(e.get(ge.X), e.get(ge.Y), oe.get(oe.X), oe.get(oe.Y)) <= 1e-4
+    assert sigma_rel(e.get(ge.SIGMA), oe.get(oe.SIGMA)) <= 1e-6
+    off, ids, deg = e.graph_sets()
+    assert dense_defect(e.n, off, ids, deg, e.get(ge.X), e.get(ge.Z), 0.3) <= 1e-6 * (1 + 1e-6) + 2e-7
