@@ -458,7 +458,9 @@ int run_push(damf_gpu* h, int grid, unsigned long long* t_end, int split = 0,
 
 extern "C" {
 
-const char* damf_gpu_version(void) { return "damf_gpu sm_100a (cluster update, SIMT materialise, pull PPR)"; }
+const char* damf_gpu_version(void) {
+  return "damf_gpu sm_100a (cluster event update on FP64 tensor cores, tcgen05 materialise, fused + whole-GPU PPR push)";
+}
 
 const char* damf_gpu_last_error(const damf_gpu* h) { return h ? h->err.c_str() : "null handle"; }
 
