@@ -1167,7 +1167,28 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     // kernel per event over the whole GPU.
     const bool fused = ppr && (h->n_cap <= (1 << 20) || (mode & DAMF_APPLY_DEFER_PUSH));
     h->ctl_fresh = false;
-    if (!ppr || fused) {
+    // Split mode (16-CTA clusters): per event a factor-only kernel, then the
+    // push as its own kernel -- 76 registers and 16 warps per CTA instead of
+    // sharing the factor kernel's 255-register, 8-warp budget (cfg-2 mean
+    // event 300 -> 283 us, same-box A/B). The in-kernel fused push remains
+    // for 8-CTA clusters.
+    const bool split = fused && event_cluster_size() == 16;
+    // no stop recorded yet for this launch group (the kernels stop at an
+    // event that requests a rebase and skip everything after it)
+    h->h_ctl->stop_event = -1;
+    CK(cudaMemcpyAsync(&h->ctl->stop_event, &h->h_ctl->stop_event, sizeof(long long),
+                       cudaMemcpyHostToDevice, h->st));
+    if (split) {
+      // one-event factor kernel, then the push kernel for that event
+      ea.fused_ppr = 0;
+      for (int64_t e = i; e < j; ++e) {
+        ea.e_begin = e;
+        ea.e_end = e + 1;
+        CK(launch_event_kernel(ea, h->st));
+        CK(launch_ppr_kernel(ea, h->st));
+        h->launches += 2;
+      }
+    } else if (!ppr || fused) {
       ea.e_begin = i;
       ea.e_end = j;
       ea.fused_ppr = fused ? 1 : 0;

@@ -1537,16 +1537,17 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
 // semantics, see ppr.cu). CTA c owns the row chunk [c*n/C, (c+1)*n/C): its
 // frontier / affected lists never leave the CTA, so each round needs only
 // two cluster barriers (after the pushes, after the pulls + count).
-template <int C>
-DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& cl,
+template <int C, class SMT, int PNT>
+DAMF_D void ppr_event(const EventKernelArgs& A, SMT& S, cg::cluster_group& cl,
                       const EventDesc& ev) {
+  constexpr int PNW = PNT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cl.block_rank();
   const int k = S.k, d = A.d;
   const double alpha = A.alpha, om = 1.0 - alpha;
   long long _pt = clock64();
   // ---- absorb_structure_delta for the touched rows (warp per row)
-  for (int q = rank * NW + warp; q < ev.touched_cnt; q += C * NW) {
+  for (int q = rank * PNW + warp; q < ev.touched_cnt; q += C * PNW) {
     const int64_t u = A.touched[ev.touched_off + q];
     float acc[kMaxD / 32];
 #pragma unroll
@@ -1585,12 +1586,12 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     int lo, hi;
     block_range(k, C, rank, lo, hi);
     double c1 = 0;
-    for (int j = lo + warp; j < hi; j += NW) {
+    for (int j = lo + warp; j < hi; j += PNW) {
       double s = 0;
       for (int i = lane; i < k; i += 32) s += fabs(PT[(int64_t)j * A.ld + i]);
       c1 = fmax(c1, warp_sum(s));
     }
-    for (int i = tid; i < k; i += NT) {
+    for (int i = tid; i < k; i += PNT) {
       double s = 0;
       for (int j = lo; j < hi; ++j) s += fabs(PT[(int64_t)j * A.ld + i]);
       S.partL[0][i] = s;
@@ -1599,14 +1600,14 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     __syncthreads();
     if (tid == 0) {
       double m = 0;
-      for (int w = 0; w < NW; ++w) m = fmax(m, S.bred[w]);
+      for (int w = 0; w < PNW; ++w) m = fmax(m, S.bred[w]);
       S.partS[2] = m;
     }
   }
   cl.sync();
   double col1 = 0, rowinf = 0;
   for (int r = 0; r < C; ++r) col1 = fmax(col1, *cl.map_shared_rank(&S.partS[2], r));
-  for (int i = tid; i < k; i += NT) {
+  for (int i = tid; i < k; i += PNT) {
     double s = 0;
     for (int r = 0; r < C; ++r) s += *cl.map_shared_rank(&S.partL[0][i], r);
     rowinf = fmax(rowinf, s);
@@ -1618,7 +1619,7 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     if (lane == 0) S.bred[warp] = m;
     __syncthreads();
     m = 0;
-    for (int w = 0; w < NW; ++w) m = fmax(m, S.bred[w]);
+    for (int w = 0; w < PNW; ++w) m = fmax(m, S.bred[w]);
     rowinf = m;
   }
   const double smax = k == 0 ? 1.0 : fmax(col1, sqrt(col1 * rowinf));
@@ -1640,25 +1641,25 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
   const int nblk = (n + 31) >> 5;
   const int myblk = nblk > rank ? (nblk - rank + C - 1) / C : 0;
   const int maxmine = ((nblk + C - 1) / C) * 32;
-  const int seg = (maxmine + NW - 1) / NW + 1;  // per-warp segment
-  const int stride = seg * NW;                   // uniform per-CTA list region
+  const int seg = (maxmine + PNW - 1) / PNW + 1;  // per-warp segment
+  const int stride = seg * PNW;                   // uniform per-CTA list region
   int* Fl = A.listF + (int64_t)rank * stride;
   int* Ll = A.listL + (int64_t)rank * stride;
   int R = (int)A.pstats[2];
   long long pushes = 0;
   int rounds = 0;
-  __shared__ int s_cnt[NW + 1];
+  __shared__ int s_cnt[PNW + 1];
   // warp-per-block ballot compaction of own rows into per-warp segments of
   // `out`, then an in-place gather into a contiguous, order-preserving list
   auto compact = [&](auto pred, int* out) -> int {
     int mycnt = 0;
     constexpr int U = 4;
-    for (int b0 = warp; b0 < myblk; b0 += NW * U) {
+    for (int b0 = warp; b0 < myblk; b0 += PNW * U) {
       bool hit[U];
       int v[U];
 #pragma unroll
       for (int q = 0; q < U; ++q) {
-        const int bi = b0 + q * NW;
+        const int bi = b0 + q * PNW;
         v[q] = bi < myblk ? ((rank + C * bi) << 5) + lane : n;
         hit[q] = v[q] < n && pred(v[q]);
       }
@@ -1672,14 +1673,14 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     if (lane == 0) s_cnt[warp] = mycnt;
     __syncthreads();
     int off = 0, tot = 0;
-    for (int w = 0; w < NW; ++w) {
+    for (int w = 0; w < PNW; ++w) {
       if (w < warp) off += s_cnt[w];
       tot += s_cnt[w];
     }
     // gather segments to the front (segments are disjoint and ordered by warp;
     // warp w's destination [off, off+cnt) never overlaps a later segment's
     // unread source because off <= w*seg)
-    for (int w = 1; w < NW; ++w) {
+    for (int w = 1; w < PNW; ++w) {
       __syncthreads();
       if (warp == w)
         for (int i = lane; i < mycnt; i += 32) out[off + i] = out[w * seg + i];
@@ -1715,7 +1716,7 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     __syncthreads();
     if (tid == 0) S.lcnt3[old] = 0;  // next filled in round rr + 1 (after this round's barrier)
     int myF = 0;
-    for (int q = warp; q < mycnt; q += NW) {
+    for (int q = warp; q < mycnt; q += PNW) {
       const int v = (rr > 0 && q < PCAP) ? S.plist[cur][q] : lists[cur][(int64_t)rank * stride + q];
       // key[v] is an upper bound of |r_v|_inf / max(deg v, 1) (see the
       // scatter below); read it before r, fenced, so every scatter increment
@@ -1817,7 +1818,7 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
     if (lane == 0) s_cnt[warp] = myF;
     __syncthreads();
     int nF = 0;
-    for (int w = 0; w < NW; ++w) nF += s_cnt[w];
+    for (int w = 0; w < PNW; ++w) nF += s_cnt[w];
     PROF_MARK(26);
     if (tid == 0)
       for (int r = 0; r < C; ++r) *cl.map_shared_rank(&S.found[rank][0], r) = nF;
@@ -1847,6 +1848,46 @@ DAMF_D void ppr_event(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& c
   cl.sync();
 }
 
+
+// ------------------------------------------------------------------ push kernel
+// The per-event push as its own cluster kernel (split mode): launched after a
+// one-event factor kernel, with its own register budget and twice the warps
+// of the factor kernel. A rebase or error requested by an earlier event of
+// the batch turns it into a no-op (the factor kernel stops the same way).
+constexpr int PPR_NT = 512;
+template <int C>
+struct PSmem {
+  int k, pp[2];
+  double partL[1][kMaxD];
+  double partS[4];
+  double bred[PPR_NT / 32];
+  long long found[C][2];
+  int lcnt3[3];
+  int plist[3][PCAP];
+};
+template <int C>
+__global__ void __launch_bounds__(PPR_NT, 1) damf_ppr_kernel(EventKernelArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PSmem<C>& S = *reinterpret_cast<PSmem<C>*>(smem_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  if (threadIdx.x == 0) {
+    S.k = A.ctl->k;
+    S.pp[0] = A.ctl->pp[0];
+    S.pp[1] = A.ctl->pp[1];
+    for (int i = 0; i < 3; ++i) S.lcnt3[i] = 0;
+  }
+  __syncthreads();
+  cl.sync();
+  for (int64_t e = A.e_begin; e < A.e_end; ++e) {
+    const long long stop = *(volatile long long*)&A.ctl->stop_event;
+    if (*(volatile int*)&A.ctl->err || (stop >= 0 && stop <= e)) break;
+    const EventDesc ev = A.ev[e];
+    ppr_event<C, PSmem<C>, PPR_NT>(A, S, cl, ev);
+    if (A.t_end && rank == 0 && threadIdx.x == 0) A.t_end[e] = globaltimer();
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 // FUSED: the per-event PPR push runs in the cluster after each event's
 // factor update (alpha < 1 on graphs up to 1 M rows); the factor-only
@@ -1873,7 +1914,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
   __syncthreads();
   cl.sync();  // counters zeroed before any CTA can append to them
   for (int64_t e = A.e_begin; e < A.e_end; ++e) {
-    if (*(volatile int*)&A.ctl->err) break;
+    // (split mode launches one event per kernel: an earlier launch of the
+    // batch that stopped for a rebase or failed turns this one into a no-op)
+    const long long stop = *(volatile long long*)&A.ctl->stop_event;
+    if (*(volatile int*)&A.ctl->err || (stop >= 0 && stop <= e)) break;
     const EventDesc ev = A.ev[e];
     if (A.t_begin && rank == 0 && threadIdx.x == 0) A.t_begin[e] = globaltimer();
     int err = 0;
@@ -1983,7 +2027,7 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     }
     if (FUSED) {
       cl.sync();  // factor / graph writes visible to the enhancer
-      ppr_event<C>(A, S, cl, ev);
+      ppr_event<C, Smem<C>, NT>(A, S, cl, ev);
     }
     if (A.t_end && rank == 0 && threadIdx.x == 0) A.t_end[e] = globaltimer();
     // a rebase was requested: stop after this event; the host rebases over
@@ -2064,6 +2108,33 @@ int event_cluster_size() {
 }
 
 size_t event_kernel_smem(int C) { return C == 16 ? sizeof(Smem<16>) : sizeof(Smem<8>); }
+
+cudaError_t launch_ppr_kernel(const EventKernelArgs& a, cudaStream_t s) {
+  constexpr int C = 16;
+  const size_t smem = sizeof(PSmem<C>);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(damf_ppr_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(damf_ppr_kernel<C>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(PPR_NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, damf_ppr_kernel<C>, a);
+}
 
 cudaError_t launch_event_kernel(const EventKernelArgs& a, cudaStream_t s) {
   return event_cluster_size() == 16 ? launch_c<16>(a, s) : launch_c<8>(a, s);

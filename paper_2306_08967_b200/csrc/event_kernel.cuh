@@ -57,6 +57,8 @@ struct EventKernelArgs {
 };
 
 cudaError_t launch_event_kernel(const EventKernelArgs& a, cudaStream_t s);
+// the per-event push as its own 16-CTA cluster kernel (split mode)
+cudaError_t launch_ppr_kernel(const EventKernelArgs& a, cudaStream_t s);
 int event_cluster_size();
 size_t event_kernel_smem(int C);
 
