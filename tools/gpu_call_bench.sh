@@ -1,7 +1,6 @@
-# Round-end evidence run (one gpurun call): bench line, launch lists, ncu captures.
+# Round-end evidence run (one gpurun call): bench line, launch list, ncu captures.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc $?"
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu --cfg5-events 2000 --cfg3-events 512 > gpurun_out/plain_bench_small.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --cfg5-events 2000 --cfg3-events 512 > gpurun_out/ncu_bench.log 2>&1; echo "ncu bench rc $?"
-echo "ppr launch list skipped (unchanged kernels)"
-python tools/prof_kernels.py events > gpurun_out/plain_ev.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:damf_event_kernel -s 1 -c 1 -o gpurun_out/evk_final python tools/prof_kernels.py events > gpurun_out/ncu_ev.log 2>&1; echo "ncu ev rc $?"
+python tools/prof_kernels.py events > gpurun_out/plain_ev.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:damf_ppr_kernel -s 20 -c 1 -o gpurun_out/pprk_final python tools/prof_kernels.py events > gpurun_out/ncu_pprk.log 2>&1; echo "ncu pprk rc $?"
