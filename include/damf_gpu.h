@@ -126,7 +126,9 @@ enum {
                                         + absorb_structure_delta + push, no
                                         factor update   */
   DAMF_APPLY_DEFER_PUSH = 2,         /* absorb only; caller pushes later   */
-  DAMF_APPLY_TIME_EVENTS = 4         /* record per-event device latency    */
+  DAMF_APPLY_TIME_EVENTS = 4,        /* record per-event device latency    */
+  DAMF_APPLY_LOG_ROWS = 8            /* record the modified base rows of
+                                        every rank-1 step (damf_gpu_row_log) */
 };
 
 typedef struct damf_apply_stats {
@@ -169,6 +171,16 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
  * the factor-based constructor. DAMF_E_ZERO_MATRIX for an empty graph,
  * DAMF_E_UNSUPPORTED if the sketch is numerically rank-deficient. */
 int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out);
+
+/* Engine(g, fs, es, cfg, events_applied, events_since_rebase)
+ * (engine.hpp:32-34, engine.cpp:12-16): resume from a factor state AND a saved
+ * enhancer (zb / rb: n x k fp32 host or device; ignored when alpha == 1, where
+ * Z_b mirrors X_b) with the engine's counters; no init_propagate runs.
+ * damf_gpu_load_state is this call fed from a DAMF v1 file. */
+int damf_gpu_resume(const damf_csr* g, const damf_config* cfg, int64_t k, const float* xb,
+                    const float* yb, const double* px_host, const double* py_host,
+                    const double* sigma_host, const float* zb, const float* rb,
+                    uint64_t events_applied, int64_t events_since_rebase, damf_gpu** out);
 
 void damf_gpu_destroy(damf_gpu* h);
 const char* damf_gpu_last_error(const damf_gpu* h);
@@ -213,6 +225,14 @@ int damf_gpu_load_rows(damf_gpu* h, int32_t which, int64_t row0, int64_t m, cons
  * DAMF_APPLY_TIME_EVENTS: fills min(max, count) values, returns count. */
 int64_t damf_gpu_event_latencies(damf_gpu* h, double* out_us_host, int64_t max);
 
+/* The base rows the last apply with DAMF_APPLY_LOG_ROWS modified, one
+ * (step, side, row) int64 triple per row: step = rank-1 step index within
+ * that call (deltas in handle_event order, update_engine.cpp:206-226), side
+ * 0 = X_b (the row set of ProjectionUpdate::dX), 1 = Y_b (dY), in the order
+ * the device wrote them (projection_update.hpp:17-36, types.hpp:101-116).
+ * Fills min(max, count) triples into out3_host, returns count. */
+int64_t damf_gpu_row_log(damf_gpu* h, int64_t* out3_host, int64_t max);
+
 /* Engine::context/content/enhanced (engine.hpp:45-47) for m rows:
  * out_host[m x k] fp32 (which = DAMF_X, DAMF_Y or DAMF_Z). which = DAMF_XB /
  * DAMF_YB / DAMF_ZB / DAMF_RB returns the raw base-coordinate rows. */
@@ -244,6 +264,9 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats);
 int damf_gpu_rebase(damf_gpu* h);
 
 int damf_gpu_diagnostics(damf_gpu* h, damf_diag* out);
+
+/* Engine::config() (engine.hpp:43): the RunConfig the handle runs with. */
+int damf_gpu_get_config(const damf_gpu* h, damf_config* out);
 
 /* The handle's CUDA stream (cudaStream_t as void*), for callers that time
  * or order work against it. */

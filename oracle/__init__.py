@@ -58,6 +58,11 @@ def lib():
         L.oracle_edge_update_rowlocal_p.argtypes = [C.c_int64, C.c_int64, f64p, f64p, f64p,
                                                     f64p, f64p, C.c_double, f64p, f64p, f64p,
                                                     f64p, f64p, f64p, f64p, i64p]
+        L.oracle_engine_row_log_enable.argtypes = [C.c_void_p, C.c_int]
+        L.oracle_engine_row_log.argtypes = [C.c_void_p, i64p, C.c_int64]
+        L.oracle_engine_row_log.restype = C.c_int64
+        L.oracle_engine_save_state.argtypes = [C.c_void_p, C.c_char_p]
+        L.oracle_engine_load_state.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         for fn in ("oracle_gen_mixed_stream", "oracle_gen_random_graph", "oracle_gen_sbm2"):
             getattr(L, fn).restype = C.c_void_p
         L.oracle_gen_mixed_stream.argtypes = [C.c_int64] * 4 + [C.c_uint64]
@@ -237,6 +242,34 @@ class OracleEngine:
 
     def rebase(self):
         lib().oracle_engine_rebase(self.h)
+
+    def row_log_enable(self, on=True):
+        """Record the row sets of every ProjectionUpdate's dX / dY from now on
+        (steps counted from 0 at enable)."""
+        lib().oracle_engine_row_log_enable(self.h, int(on))
+
+    def row_log(self):
+        n = lib().oracle_engine_row_log(self.h, None, 0)
+        out = np.zeros((n, 3), np.int64)
+        lib().oracle_engine_row_log(self.h, _p(out, i64p), n)
+        return out
+
+    def save_state(self, path):
+        """save_state (io.cpp:182-219), restated."""
+        st = lib().oracle_engine_save_state(self.h, str(path).encode())
+        if st:
+            raise OracleError(st, lib().oracle_last_error().decode())
+
+    @classmethod
+    def load_state(cls, path):
+        """load_state (io.cpp:221-269), restated."""
+        self = cls.__new__(cls)
+        self.h = C.c_void_p()
+        st = lib().oracle_engine_load_state(str(path).encode(), C.byref(self.h))
+        if st:
+            self.h = None
+            raise OracleError(st, lib().oracle_last_error().decode())
+        return self
 
     def score(self, u, v, enhanced=True):
         return lib().oracle_engine_score(self.h, u, v, int(enhanced))

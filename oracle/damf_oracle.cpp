@@ -1052,6 +1052,13 @@ void Engine::apply(const GraphEvent& e) {
   std::vector<Index> touched = g_.touched_by(e);
   std::vector<DeltaVectors> deltas = g_.apply_event(e);
   HandledEvent handled = handle_event(fs_, deltas);
+  for (const ProjectionUpdate& pu : handled.updates) {  // harness hook
+    if (row_log) {
+      for (Index r : pu.dX.idx) row_log->insert(row_log->end(), {row_log_step, 0, r});
+      for (Index r : pu.dY.idx) row_log->insert(row_log->end(), {row_log_step, 1, r});
+    }
+    ++row_log_step;
+  }
   for (const AppliedDelta& ad : handled.applied) {
     if (ad.x_transform) es_.apply_transform(*ad.x_transform);
     if (ad.x_rows_appended > 0) es_.append_rows(ad.x_rows_appended);

@@ -331,6 +331,11 @@ class Engine {
   double score(Index u, Index v, bool enhanced = true) const;
   void rebase();
   std::uint64_t rebases = 0;  // counter for the harness
+  // Harness hook (not in the reference): when set, apply() appends one
+  // (step, side, row) triple per row of every ProjectionUpdate's dX (side 0)
+  // and dY (side 1), steps numbered by *row_log_step across calls.
+  std::vector<std::int64_t>* row_log = nullptr;
+  std::int64_t row_log_step = 0;
 
  private:
   DynamicGraph g_;

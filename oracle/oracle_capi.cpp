@@ -2,7 +2,9 @@
 // the Python parity tests (tests/) and bench.py's cpu_baseline leg can drive
 // it with the same seeded inputs the GPU path receives. Status codes follow
 // the product ABI (include/damf_gpu.h): 0 ok, Error::Kind ordinal + 1.
+#include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -26,6 +28,7 @@ int fail_other(const std::exception& e) {
 struct OEngine {
   Engine eng;
   double last_apply_ms = 0;
+  std::vector<std::int64_t> row_log;
 };
 
 DynamicGraph build_graph(int64_t n, int undirected, int64_t arcs, const int64_t* src,
@@ -393,3 +396,140 @@ void oracle_stream_events(void* hp, int32_t* kind, int64_t* u, int64_t* v, doubl
 }
 
 }  // extern "C"
+
+// ---- harness: modified-row log (see Engine::row_log) -----------------------
+extern "C" {
+// Start (on != 0) or stop logging; starting clears the log and the step count.
+void oracle_engine_row_log_enable(void* hp, int on) {
+  auto* h = static_cast<OEngine*>(hp);
+  if (on) {
+    h->row_log.clear();
+    h->eng.row_log = &h->row_log;
+    h->eng.row_log_step = 0;
+  } else {
+    h->eng.row_log = nullptr;
+  }
+}
+// Copies min(max, count) (step, side, row) triples; returns count.
+int64_t oracle_engine_row_log(void* hp, int64_t* out, int64_t max) {
+  auto* h = static_cast<OEngine*>(hp);
+  const int64_t m = static_cast<int64_t>(h->row_log.size() / 3);
+  for (int64_t i = 0; i < 3 * std::min(m, max); ++i) out[i] = h->row_log[i];
+  return m;
+}
+}
+
+// ---- io.cpp:182-269 save_state / load_state, restated ------------------------
+namespace {
+const char kMagic[4] = {'D', 'A', 'M', 'F'};
+template <typename T>
+void wpod(std::FILE* f, T v) { std::fwrite(&v, sizeof(T), 1, f); }
+template <typename T>
+T rpod(std::FILE* f) {
+  T v{};
+  if (std::fread(&v, sizeof(T), 1, f) != 1) throw Error(Error::Kind::ParseError, "truncated state file");
+  return v;
+}
+void wmat(std::FILE* f, const Mat& m) {  // io.cpp:51-56: rows, cols, row-major data
+  wpod<std::int64_t>(f, m.r);
+  wpod<std::int64_t>(f, m.c);
+  if (!m.a.empty()) std::fwrite(m.a.data(), sizeof(double), m.a.size(), f);
+}
+Mat rmat(std::FILE* f) {  // io.cpp:58-65
+  const auto r = rpod<std::int64_t>(f);
+  const auto c = rpod<std::int64_t>(f);
+  Mat m(r, c);
+  if (!m.a.empty() && std::fread(m.a.data(), sizeof(double), m.a.size(), f) != m.a.size())
+    throw Error(Error::Kind::ParseError, "truncated state file");
+  return m;
+}
+}  // namespace
+
+extern "C" {
+int oracle_engine_save_state(void* hp, const char* path) {
+  auto* h = static_cast<OEngine*>(hp);
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(Error(Error::Kind::IoError, std::string("cannot write ") + path));
+  const Engine& e = h->eng;
+  const RunConfig& cfg = e.config();
+  std::fwrite(kMagic, 1, 4, f);
+  wpod<std::uint32_t>(f, 1);
+  wpod<std::int64_t>(f, cfg.d);
+  wpod<double>(f, cfg.alpha);
+  wpod<double>(f, cfg.eps);
+  wpod<std::uint64_t>(f, cfg.seed);
+  wpod<double>(f, cfg.rebase_cond);
+  wpod<std::int64_t>(f, cfg.rebase_every);
+  wpod<std::uint8_t>(f, cfg.undirected ? 1 : 0);
+  wpod<std::uint64_t>(f, e.events_applied());
+  wpod<std::int64_t>(f, e.events_since_rebase());
+  const FactorState& fs = e.state();
+  wpod<std::int64_t>(f, static_cast<std::int64_t>(fs.sigma().size()));  // io.cpp:67-71
+  std::fwrite(fs.sigma().data(), sizeof(double), fs.sigma().size(), f);
+  wmat(f, fs.xb());
+  wmat(f, fs.yb());
+  wmat(f, fs.px());
+  wmat(f, fs.py());
+  wmat(f, e.enhancer().zb());
+  wmat(f, e.enhancer().rb());
+  const DynamicGraph& g = e.graph();
+  wpod<std::int64_t>(f, g.node_count());
+  for (Index u = 0; u < g.node_count(); ++u) {
+    const auto& nb = g.out_neighbors(u);
+    wpod<std::int64_t>(f, static_cast<std::int64_t>(nb.size()));
+    for (const auto& [v, w] : nb) {
+      wpod<std::int64_t>(f, v);
+      wpod<double>(f, w);
+    }
+  }
+  const bool ok = std::ferror(f) == 0;
+  if (std::fclose(f) != 0 || !ok) return fail(Error(Error::Kind::IoError, std::string("write failed: ") + path));
+  return 0;
+}
+
+int oracle_engine_load_state(const char* path, void** out) {
+  *out = nullptr;
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(Error(Error::Kind::IoError, std::string("cannot open ") + path));
+  try {
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, kMagic, 4) != 0)
+      throw Error(Error::Kind::ParseError, std::string(path) + ": not a DAMF state file");
+    if (rpod<std::uint32_t>(f) != 1) throw Error(Error::Kind::ParseError, "unsupported version");
+    RunConfig cfg;
+    cfg.d = rpod<std::int64_t>(f);
+    cfg.alpha = rpod<double>(f);
+    cfg.eps = rpod<double>(f);
+    cfg.seed = rpod<std::uint64_t>(f);
+    cfg.rebase_cond = rpod<double>(f);
+    cfg.rebase_every = rpod<std::int64_t>(f);
+    cfg.undirected = rpod<std::uint8_t>(f) != 0;
+    const auto applied = rpod<std::uint64_t>(f);
+    const auto since = rpod<std::int64_t>(f);
+    const auto ks = rpod<std::int64_t>(f);
+    Vec sigma(static_cast<size_t>(ks));
+    if (ks && std::fread(sigma.data(), sizeof(double), sigma.size(), f) != sigma.size())
+      throw Error(Error::Kind::ParseError, "truncated state file");
+    Mat xb = rmat(f), yb = rmat(f), px = rmat(f), py = rmat(f), zb = rmat(f), rb = rmat(f);
+    const auto n = rpod<std::int64_t>(f);
+    DynamicGraph g(n, cfg.undirected);
+    for (Index u = 0; u < n; ++u) {
+      const auto cnt = rpod<std::int64_t>(f);
+      for (std::int64_t i = 0; i < cnt; ++i) {
+        const auto v = rpod<std::int64_t>(f);
+        const double w = rpod<double>(f);
+        g.add_arc_raw(u, v, w);
+      }
+    }
+    std::fclose(f);
+    FactorState fs(std::move(xb), std::move(yb), std::move(px), std::move(py), std::move(sigma), cfg.d);
+    EnhancerState es(EnhancerParams{cfg.alpha, cfg.eps}, std::move(zb), std::move(rb));
+    auto* h = new OEngine{Engine(std::move(g), std::move(fs), std::move(es), cfg, applied, since)};
+    *out = h;
+    return 0;
+  } catch (const Error& e) {
+    std::fclose(f);
+    return fail(e);
+  }
+}
+}

@@ -30,6 +30,7 @@ struct DevCtl {
   unsigned long long t_begin, t_end;  // %globaltimer stamps of the last event
   long long stop_event;               // first event not processed by a stopped batch
   long long dirty_n[2];               // rows of X_b / Y_b written through P^-1 since the last fold
+  long long rowlog_n;                 // entries in the modified-row log (DAMF_APPLY_LOG_ROWS)
   unsigned long long prof[32];        // per-phase SM cycles (rank 0), dev profiling
 };
 

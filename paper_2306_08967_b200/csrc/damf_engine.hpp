@@ -3,7 +3,7 @@
 // include/damf_gpu.h. A caller of the reference swaps
 //     damf::Engine eng(std::move(g), cfg);  eng.apply(e);  eng.enhanced(u);
 // for
-//     damf::gpu::Engine eng(g, cfg, factors);  eng.apply(e);  eng.enhanced(u);
+//     damf::gpu::Engine eng(g, cfg);  eng.apply(e);  eng.enhanced(u);
 // Errors are rethrown as damf::gpu::Error carrying the reference's
 // Error::Kind (types.hpp:21-41); nothing but plain pointers crosses the ABI.
 #pragma once
@@ -95,19 +95,52 @@ struct Factors {
   std::vector<double> sigma;      // k
 };
 
+// EnhancerState(params, zb, rb) (enhancer.hpp:24-25): base-coordinate PPR rows.
+struct Enhancer {
+  std::vector<float> zb, rb;      // n x k
+};
+
 class Engine {
  public:
-  Engine(const Csr& g, const RunConfig& cfg, const Factors& f) {
-    damf_csr c{g.n, (int64_t)g.targets.size(), g.offsets.data(), g.targets.data(),
-               g.weights.empty() ? nullptr : g.weights.data()};
-    damf_config dc{cfg.d, cfg.alpha, cfg.eps, cfg.seed, cfg.rebase_cond, cfg.rebase_every,
-                   cfg.undirected ? 1 : 0, 0, 0, 0};
+  // Engine(DynamicGraph g, const RunConfig&) (engine.hpp:29, engine.cpp:5-10):
+  // randomized t-SVD init on the device, then init_propagate.
+  Engine(const Csr& g, const RunConfig& cfg) : cfg_(cfg) {
+    damf_csr c = csr(g);
+    damf_config dc = config(cfg);
+    check(damf_gpu_create(&c, &dc, &h_));
+  }
+  // Engine(g, FactorState(...), EnhancerState::init_propagate(...), cfg, 0, 0)
+  Engine(const Csr& g, const RunConfig& cfg, const Factors& f) : cfg_(cfg) {
+    damf_csr c = csr(g);
+    damf_config dc = config(cfg);
     check(damf_gpu_create_from_factors(&c, &dc, f.k, f.xb.data(), f.yb.data(), f.px.data(),
                                        f.py.data(), f.sigma.data(), &h_));
   }
+  // Engine(g, fs, es, cfg, events_applied, events_since_rebase) (engine.hpp:32-34)
+  Engine(const Csr& g, const Factors& f, const Enhancer& es, const RunConfig& cfg,
+         uint64_t events_applied, int64_t events_since_rebase)
+      : cfg_(cfg) {
+    damf_csr c = csr(g);
+    damf_config dc = config(cfg);
+    check(damf_gpu_resume(&c, &dc, f.k, f.xb.data(), f.yb.data(), f.px.data(), f.py.data(),
+                          f.sigma.data(), es.zb.empty() ? nullptr : es.zb.data(),
+                          es.rb.empty() ? nullptr : es.rb.data(), events_applied,
+                          events_since_rebase, &h_));
+  }
+  // load_state (io.cpp:221-269) / save_state (io.cpp:182-219): DAMF v1 files
+  static Engine load_state(const std::string& path) {
+    Engine e;
+    e.check(damf_gpu_load_state(path.c_str(), nullptr, &e.h_));
+    damf_config c{};
+    e.check(damf_gpu_get_config(e.h_, &c));
+    e.cfg_ = RunConfig{c.d, c.alpha, c.eps, c.seed, c.rebase_cond, c.rebase_every, c.undirected != 0};
+    return e;
+  }
+  void save_state(const std::string& path) const { check(damf_gpu_save_state(h_, path.c_str())); }
+
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
-  Engine(Engine&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  Engine(Engine&& o) noexcept : h_(std::exchange(o.h_, nullptr)), cfg_(o.cfg_) {}
   ~Engine() { damf_gpu_destroy(h_); }
 
   // Engine::apply (engine.cpp:22-41)
@@ -171,7 +204,64 @@ class Engine {
 
   damf_gpu* handle() const { return h_; }
 
+  // Accessors (engine.hpp:38-43), as host copies of the device state.
+  const RunConfig& config() const { return cfg_; }
+  uint64_t events_applied() const { return (uint64_t)diagnostics().events_applied; }
+  int64_t events_since_rebase() const { return diagnostics().events_since_rebase; }
+  // graph(): the out-adjacency, sorted per row, with weighted out-degrees
+  Csr graph(std::vector<double>* out_degree = nullptr) const {
+    const damf_diag d = diagnostics();
+    Csr g;
+    g.n = d.n;
+    g.offsets.resize((size_t)d.n + 1);
+    g.targets.resize((size_t)d.arcs);
+    std::vector<double> deg((size_t)d.n);
+    check(damf_gpu_get_graph(h_, g.offsets.data(), g.targets.data(), deg.data()));
+    if (out_degree) *out_degree = std::move(deg);
+    return g;
+  }
+  // state(): X_b, Y_b, P_X, P_Y, sigma (FactorState, factor_state.hpp:68-71)
+  Factors state() const {
+    const damf_diag d = diagnostics();
+    Factors f;
+    f.k = d.k;
+    f.xb.resize((size_t)(d.n * d.k));
+    f.yb.resize((size_t)(d.n * d.k));
+    f.px.resize((size_t)(d.k * d.k));
+    f.py.resize((size_t)(d.k * d.k));
+    f.sigma.resize((size_t)d.k);
+    check(damf_gpu_get_state(h_, DAMF_XB, f.xb.data()));
+    check(damf_gpu_get_state(h_, DAMF_YB, f.yb.data()));
+    check(damf_gpu_get_state(h_, DAMF_PX, f.px.data()));
+    check(damf_gpu_get_state(h_, DAMF_PY, f.py.data()));
+    check(damf_gpu_get_state(h_, DAMF_SIGMA, f.sigma.data()));
+    return f;
+  }
+  // enhancer(): Z_b, r_b (EnhancerState, enhancer.hpp:67); alpha == 1 mirrors X_b, r_b = 0
+  Enhancer enhancer() const {
+    const damf_diag d = diagnostics();
+    Enhancer e;
+    e.zb.resize((size_t)(d.n * d.k));
+    e.rb.assign((size_t)(d.n * d.k), 0.0f);
+    if (cfg_.alpha == 1.0) {
+      check(damf_gpu_get_state(h_, DAMF_XB, e.zb.data()));
+    } else {
+      check(damf_gpu_get_state(h_, DAMF_ZB, e.zb.data()));
+      check(damf_gpu_get_state(h_, DAMF_RB, e.rb.data()));
+    }
+    return e;
+  }
+
  private:
+  Engine() = default;
+  static damf_csr csr(const Csr& g) {
+    return damf_csr{g.n, (int64_t)g.targets.size(), g.offsets.data(), g.targets.data(),
+                    g.weights.empty() ? nullptr : g.weights.data()};
+  }
+  static damf_config config(const RunConfig& cfg) {
+    return damf_config{cfg.d, cfg.alpha, cfg.eps, cfg.seed, cfg.rebase_cond, cfg.rebase_every,
+                       cfg.undirected ? 1 : 0, 0, 0, 0};
+  }
   std::vector<float> row(int32_t which, int64_t u) const {
     const int64_t k = diagnostics().k;
     std::vector<float> out((size_t)k);
@@ -179,9 +269,10 @@ class Engine {
     return out;
   }
   void check(int st) const {
-    if (st) throw Error(st, h_ ? damf_gpu_last_error(h_) : "damf_gpu_create_from_factors failed");
+    if (st) throw Error(st, h_ ? damf_gpu_last_error(h_) : "engine construction failed");
   }
   damf_gpu* h_ = nullptr;
+  RunConfig cfg_;
 };
 
 }  // namespace gpu

@@ -244,6 +244,9 @@ struct damf_gpu {
   unsigned long long *t_begin = nullptr, *t_end = nullptr;
   size_t t_cap = 0;
   std::vector<double> lat_us;
+  int64_t* rowlog = nullptr;          // device (step, side, row) triples
+  long long rowlog_cap = 0;
+  std::vector<int64_t> rowlog_h;      // the last apply's log (DAMF_APPLY_LOG_ROWS)
   uint64_t events_applied = 0;
   int64_t since_rebase = 0;
   int64_t total_pushes = 0;
@@ -454,6 +457,30 @@ int run_push(damf_gpu* h, int grid, unsigned long long* t_end, int split = 0,
   return 0;
 }
 
+__global__ void fill_f64_kernel(double* p, int64_t n, double v) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    p[x] = v;
+}
+
+// Materialise per-arc weights (all 1.0) for an engine built from an
+// unweighted CSR, on the first event that carries a non-unit weight: the
+// device CSR then stores weights like the reference's adjacency
+// (graph.hpp:93-98). Every slot of the pool is set, so relocated and
+// appended rows read consistent values.
+int ensure_weights(damf_gpu* h) {
+  if (h->out.wts) return 0;
+  for (int side = 0; side < (h->directed ? 2 : 1); ++side) {
+    DevCSR& c = side == 0 ? h->out : h->in;
+    CK(dalloc(h, &c.wts, (size_t)c.pool_size));
+    fill_f64_kernel<<<h->nsm * 8, 256, 0, h->st>>>(c.wts, c.pool_size, 1.0);
+    CK(cudaGetLastError());
+  }
+  if (!h->directed) h->in = h->out;
+  CK(cudaStreamSynchronize(h->st));
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -486,6 +513,7 @@ void damf_gpu_destroy(damf_gpu* h) {
   h->nb_w.release();
   if (h->t_begin) cudaFree(h->t_begin);
   if (h->t_end) cudaFree(h->t_end);
+  if (h->rowlog) cudaFree(h->rowlog);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -976,6 +1004,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
   int vstatus = 0;
   std::string vmsg;
   std::vector<std::pair<int64_t, double>> inl, outl;
+  bool need_w = false;  // a non-unit weight arrives at an unweighted engine
   for (int64_t i = 0; i < count && !vstatus; ++i) {
     const int kind = b->kind[i];
     EventDesc e{};
@@ -999,12 +1028,22 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         ok_count = i;
         break;
       }
+      // graph.cpp:89-90 rejects w <= 0; NaN and +Inf pass that test, and the
+      // reference then inserts the arc and throws NonFinite from the bordered
+      // SVD (svd.cpp:31-32). Both are rejected here, before any mutation.
+      if (kind == DAMF_ADD_EDGE && !std::isfinite(w) && !(w < 0.0)) {
+        vstatus = DAMF_E_NON_FINITE;
+        vmsg = "AddEdge: non-finite weight";
+        ok_count = i;
+        break;
+      }
       if (kind == DAMF_ADD_EDGE && !(w > 0.0)) {
         vstatus = DAMF_E_PARSE;
         vmsg = "AddEdge: weight must be > 0";
         ok_count = i;
         break;
       }
+      if (w != 1.0) need_w = true;
       CK(need(2, 0, 2));
       const bool two = h->cfg.undirected && u != v;
       e.u = u;
@@ -1050,15 +1089,22 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         for (auto& p : outl) inl.push_back(p);
         outl = inl;
       }
-      for (auto& p : inl)
-        if (p.first < 0 || p.first >= nn || !(p.second > 0.0)) {
-          vstatus = (p.first < 0 || p.first >= nn) ? DAMF_E_UNKNOWN_NODE : DAMF_E_PARSE;
-          vmsg = "AddNode: bad neighbour";
-        }
-      for (auto& p : outl)
-        if (p.first < 0 || p.first >= nn || !(p.second > 0.0)) {
-          vstatus = (p.first < 0 || p.first >= nn) ? DAMF_E_UNKNOWN_NODE : DAMF_E_PARSE;
-          vmsg = "AddNode: bad neighbour";
+      // graph.cpp:143-152: unknown neighbour, weight <= 0; non-finite weights
+      // are rejected up front (the reference throws NonFinite later, svd.cpp:31-32)
+      for (const auto* lst : {&inl, &outl})
+        for (auto& p : *lst) {
+          if (vstatus) break;
+          if (p.first < 0 || p.first >= nn) {
+            vstatus = DAMF_E_UNKNOWN_NODE;
+            vmsg = "AddNode: unknown node " + std::to_string(p.first);
+          } else if (!std::isfinite(p.second) && !(p.second < 0.0)) {
+            vstatus = DAMF_E_NON_FINITE;
+            vmsg = "AddNode: non-finite weight";
+          } else if (!(p.second > 0.0)) {
+            vstatus = DAMF_E_PARSE;
+            vmsg = "AddNode: weight must be > 0";
+          }
+          if (p.second != 1.0) need_w = true;
         }
       if (nn + 1 > h->n_cap) {
         vstatus = DAMF_E_TOO_LARGE;
@@ -1129,6 +1175,10 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     e.touched_cnt = (int64_t)h->touched.n - e.touched_off;
     h->ev.push(e);
   }
+  // an engine created from an unweighted CSR stores no weights (all 1.0);
+  // the first non-unit weight materialises them (graph.hpp: weights are f64)
+  if (need_w && !h->out.wts)
+    if (int r = ensure_weights(h)) return r;
   // ---- upload
   CK(h->ev.upload(h->st));
   CK(h->steps.upload(h->st));
@@ -1147,12 +1197,27 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
   }
   if (!h->ctl_fresh)
     if (int r = sync_ctl(h)) return r;
+  const bool log_rows = mode & DAMF_APPLY_LOG_ROWS;
+  if (log_rows) {
+    // every modified row is a nonzero of some b, or one c / appended row
+    const long long need = (long long)h->sp_rows.n + (long long)h->steps.n + 16;
+    if (need > h->rowlog_cap) {
+      if (h->rowlog) cudaFree(h->rowlog);
+      h->rowlog_cap = need;
+      CK(cudaMalloc(&h->rowlog, (size_t)need * 3 * sizeof(int64_t)));
+    }
+    h->h_ctl->rowlog_n = 0;
+    CK(cudaMemcpyAsync(&h->ctl->rowlog_n, &h->h_ctl->rowlog_n, sizeof(long long),
+                       cudaMemcpyHostToDevice, h->st));
+  }
   const long long rank1_0 = h->h_ctl->rank1, folds0 = h->h_ctl->folds;
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
   EventKernelArgs ea = event_args(h);
   ea.mode = mode;
   ea.t_begin = timing ? h->t_begin : nullptr;
   ea.t_end = timing ? h->t_end : nullptr;
+  ea.rowlog = log_rows ? h->rowlog : nullptr;
+  ea.rowlog_cap = log_rows ? h->rowlog_cap : 0;
   const bool ppr = !h->alpha1;
   const bool push_each = ppr && !(mode & DAMF_APPLY_DEFER_PUSH);
   int64_t rebases = 0;
@@ -1195,6 +1260,10 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
       CK(launch_event_kernel(ea, h->st));
       h->launches += 1;
     } else {
+      // whole-GPU push per event (large graphs): the host reads the control
+      // block after every event, so an event that requests a rebase (or
+      // fails) ends the launch group right there -- the kernels of later
+      // events would be no-ops (stop_event) and their absorb / push must not run
       for (int64_t e = i; e < j; ++e) {
         ea.e_begin = e;
         ea.e_end = e + 1;
@@ -1202,6 +1271,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         h->launches += 1 + (ed_absorb_nonempty(h, e) ? 1 : 0);
         // rows appended by AddNode are visible to the enhancer from here
         const EventDesc& ed = h->ev.h[e];
+        const int64_t n_prev = h->n;
         if (ed.kind == DAMF_ADD_NODE) h->n = ed.u + 1;
         PprArgs pa = ppr_args(h);
         pa.k = h->k;
@@ -1209,15 +1279,24 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         if (push_each) {
           if (int r = run_push(h, 8 * h->nsm, timing ? h->t_end + e : nullptr)) return r;
         }
+        if (int r = sync_ctl(h)) return r;
+        if (h->h_ctl->err) {
+          h->n = n_prev;
+          break;
+        }
+        if (h->h_ctl->need_rebase) {
+          h->h_ctl->stop_event = e + 1;
+          break;
+        }
       }
     }
     if (int r = sync_ctl(h)) return r;
-    // a batch kernel stops right after an event that requested a rebase
+    // a launch group stops right after an event that requested a rebase
     // (cond trigger, storage bound or an exact-inverse step): rebase over the
     // whole GPU and resume with the next event, as engine.cpp:38-40 orders it
     int64_t done = j;
-    const bool stopped = (!ppr || fused) && !h->h_ctl->err && h->h_ctl->need_rebase &&
-                         h->h_ctl->stop_event > i && h->h_ctl->stop_event < j;
+    const bool stopped = !h->h_ctl->err && h->h_ctl->need_rebase && h->h_ctl->stop_event > i &&
+                         h->h_ctl->stop_event < j;
     if (stopped) done = h->h_ctl->stop_event;
     for (int64_t e = i; e < done; ++e)
       if (h->ev.h[e].kind == DAMF_ADD_NODE) h->n = h->ev.h[e].u + 1;
@@ -1265,6 +1344,17 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     if (int r = damf_gpu_rebase(h)) return r;
     ++rebases;
   }
+  if (log_rows) {
+    // rebases inside the call do not touch the log; the mirror is fresh here
+    if (!h->ctl_fresh)
+      if (int r = sync_ctl(h)) return r;
+    const long long m = std::min<long long>(h->h_ctl->rowlog_n, h->rowlog_cap);
+    h->rowlog_h.resize((size_t)m * 3);
+    if (m) CK(cudaMemcpy(h->rowlog_h.data(), h->rowlog, (size_t)m * 3 * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost));
+  } else {
+    h->rowlog_h.clear();
+  }
   if (timing) {
     const int64_t m = s.applied;
     std::vector<unsigned long long> tb(m), te(m);
@@ -1297,6 +1387,12 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
   h->total_pushes = h->h_pstats[0];
   if (stats) *stats = s;
   return status;
+}
+
+int64_t damf_gpu_row_log(damf_gpu* h, int64_t* out, int64_t max) {
+  const int64_t m = (int64_t)h->rowlog_h.size() / 3;
+  for (int64_t i = 0; i < 3 * std::min(m, max); ++i) out[i] = h->rowlog_h[i];
+  return m;
 }
 
 int64_t damf_gpu_event_latencies(damf_gpu* h, double* out, int64_t max) {
@@ -1546,9 +1642,11 @@ int damf_gpu_get_graph(damf_gpu* h, int64_t* offsets, int32_t* targets, double* 
 // ---- state persistence: the reference's DAMF v1 binary (io.cpp:182-264) --
 // magic "DAMF", u32 version 1, RunConfig, u64 events_applied, i64
 // events_since_rebase, sigma (i64 n + f64), X_b, Y_b, P_X, P_Y, Z_b, r_b
-// (i64 rows, i64 cols, f64 column-major), then the out-adjacency (i64 n; per
-// node i64 count and (i64 v, f64 w) pairs). Files written here load in the
-// reference and vice versa (fp32 rows round-trip through fp64 exactly).
+// (i64 rows, i64 cols, f64 row-major: DenseMatrix is Eigen RowMajor,
+// types.hpp:17-18, and write_matrix dumps m.data(), io.cpp:51-56), then the
+// out-adjacency (i64 n; per node i64 count and (i64 v, f64 w) pairs). Files
+// written here load in the reference and vice versa (fp32 rows widen to fp64
+// exactly; fp64 rows from the reference are rounded to fp32 on load).
 }  // extern "C"
 namespace {
 template <typename T>
@@ -1560,19 +1658,21 @@ bool getv(std::FILE* f, T* v) {
   return std::fread(v, sizeof(T), 1, f) == 1;
 }
 void put_rows(std::FILE* f, const std::vector<float>& rm, int64_t n, int64_t k) {
+  // write_matrix (io.cpp:51-56) dumps Eigen RowMajor storage (types.hpp:17-18)
   putv<int64_t>(f, n);
   putv<int64_t>(f, k);
-  std::vector<double> col((size_t)n);
-  for (int64_t j = 0; j < k; ++j) {
-    for (int64_t i = 0; i < n; ++i) col[i] = rm[(size_t)i * k + j];
-    std::fwrite(col.data(), 8, (size_t)n, f);
+  std::vector<double> row((size_t)k);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t j = 0; j < k; ++j) row[j] = rm[(size_t)i * k + j];
+    std::fwrite(row.data(), 8, (size_t)k, f);
   }
 }
-bool get_matrix(std::FILE* f, int64_t* r, int64_t* c, std::vector<double>* colmajor) {
+// read_matrix (io.cpp:58-65): i64 rows, i64 cols, fp64 row-major
+bool get_matrix(std::FILE* f, int64_t* r, int64_t* c, std::vector<double>* rowmajor) {
   if (!getv(f, r) || !getv(f, c) || *r < 0 || *c < 0) return false;
-  colmajor->resize((size_t)(*r * *c));
+  rowmajor->resize((size_t)(*r * *c));
   return (size_t)(*r * *c) == 0 ||
-         std::fread(colmajor->data(), 8, (size_t)(*r * *c), f) == (size_t)(*r * *c);
+         std::fread(rowmajor->data(), 8, (size_t)(*r * *c), f) == (size_t)(*r * *c);
 }
 }  // namespace
 extern "C" {
@@ -1603,14 +1703,12 @@ int damf_gpu_save_state(damf_gpu* h, const char* path) {
     if (int r = damf_gpu_get_state(h, which, rows.data())) { std::fclose(f); return r; }
     put_rows(f, rows, n, k);
   }
-  std::vector<double> P((size_t)k * k), Pc((size_t)k * k);
+  std::vector<double> P((size_t)k * k);
   for (int which : {DAMF_PX, DAMF_PY}) {
     if (int r = damf_gpu_get_state(h, which, P.data())) { std::fclose(f); return r; }
-    for (int64_t i = 0; i < k; ++i)
-      for (int64_t j = 0; j < k; ++j) Pc[(size_t)j * k + i] = P[(size_t)i * k + j];
     putv<int64_t>(f, k);
     putv<int64_t>(f, k);
-    std::fwrite(Pc.data(), 8, Pc.size(), f);
+    std::fwrite(P.data(), 8, P.size(), f);  // row-major, as get_state returns it
   }
   if (h->alpha1) {  // enhancer.cpp:34-38: Z_b mirrors X_b, r_b = 0
     if (int r = damf_gpu_get_state(h, DAMF_XB, rows.data())) { std::fclose(f); return r; }
@@ -1706,37 +1804,43 @@ int damf_gpu_load_state(const char* path, const damf_config* sizing, damf_gpu** 
     off[u + 1] = (int64_t)tgt.size();
   }
   std::fclose(f);
-  // fp64 column-major -> fp32 row-major (X_b, Y_b); P row-major
-  auto rows32 = [&](const std::vector<double>& cm) {
+  // fp64 row-major -> fp32 row-major (X_b, Y_b); P stays fp64 row-major
+  auto rows32 = [&](const std::vector<double>& rm) {
     std::vector<float> o((size_t)n * k);
-    for (int64_t j = 0; j < k; ++j)
-      for (int64_t i = 0; i < n; ++i) o[(size_t)i * k + j] = (float)cm[(size_t)j * n + i];
-    return o;
-  };
-  auto rowmajor = [&](const std::vector<double>& cm) {
-    std::vector<double> o((size_t)k * k);
-    for (int64_t i = 0; i < k; ++i)
-      for (int64_t j = 0; j < k; ++j) o[(size_t)i * k + j] = cm[(size_t)j * k + i];
+    for (size_t x = 0; x < o.size(); ++x) o[x] = (float)rm[x];
     return o;
   };
   const std::vector<float> x32 = rows32(xb), y32 = rows32(yb);
-  const std::vector<double> pxr = rowmajor(px), pyr = rowmajor(py);
+  const std::vector<double>& pxr = px;
+  const std::vector<double>& pyr = py;
   damf_csr g{n, (int64_t)tgt.size(), off.data(), tgt.data(), weighted ? wts.data() : nullptr};
+  const std::vector<float> z32 = rows32(zb), r32 = rows32(rb);
+  return damf_gpu_resume(&g, &cfg, k, x32.data(), y32.data(), pxr.data(), pyr.data(), sig.data(),
+                         z32.data(), r32.data(), applied, since, out);
+}
+
+// Engine(g, fs, es, cfg, events_applied, events_since_rebase) (engine.hpp:32-34):
+// the factor state plus a saved enhancer, no init_propagate.
+int damf_gpu_resume(const damf_csr* g, const damf_config* cfg, int64_t k, const float* xb,
+                    const float* yb, const double* px, const double* py, const double* sigma,
+                    const float* zb, const float* rb, uint64_t events_applied,
+                    int64_t events_since_rebase, damf_gpu** out) {
+  *out = nullptr;
   t_skip_ppr_init = true;
-  const int st = damf_gpu_create_from_factors(&g, &cfg, k, x32.data(), y32.data(), pxr.data(),
-                                              pyr.data(), sig.data(), out);
+  const int st = damf_gpu_create_from_factors(g, cfg, k, xb, yb, px, py, sigma, out);
   t_skip_ppr_init = false;
   if (st) return st;
   damf_gpu* h = *out;
-  h->events_applied = applied;
-  h->since_rebase = since;
+  h->events_applied = events_applied;
+  h->since_rebase = events_since_rebase;
   if (!h->alpha1) {
-    // Engine(g, fs, es, ...) resumes the saved enhancer (engine.hpp:32-34)
-    const std::vector<float> z32 = rows32(zb), r32 = rows32(rb);
-    CK(cudaMemcpy2D(h->Zb, (size_t)h->d * 4, z32.data(), (size_t)k * 4, (size_t)k * 4, n,
-                    cudaMemcpyHostToDevice));
-    CK(cudaMemcpy2D(h->rb, (size_t)h->d * 4, r32.data(), (size_t)k * 4, (size_t)k * 4, n,
-                    cudaMemcpyHostToDevice));
+    // alpha == 1 mirrors Z_b = X_b (enhancer.cpp:34-38); otherwise the saved
+    // Z_b / r_b, re-keyed like EnhancerState's constructor (enhancer.cpp:11-24)
+    if (!zb || !rb) return fail(h, DAMF_E_SHAPE_MISMATCH, "resume: Z_b and r_b are required when alpha != 1");
+    CK(cudaMemcpy2D(h->Zb, (size_t)h->d * 4, zb, (size_t)k * 4, (size_t)k * 4, g->n,
+                    cudaMemcpyDefault));
+    CK(cudaMemcpy2D(h->rb, (size_t)h->d * 4, rb, (size_t)k * 4, (size_t)k * 4, g->n,
+                    cudaMemcpyDefault));
     CK(launch_ppr_keys(ppr_args(h), h->nsm, h->st));
     CK(cudaStreamSynchronize(h->st));
   }
@@ -1765,6 +1869,12 @@ int damf_gpu_diagnostics(damf_gpu* h, damf_diag* o) {
   o->total_pushes = h->h_pstats[0];
   o->device_bytes = (int64_t)h->bytes;
   o->kernel_launches = h->launches;
+  return 0;
+}
+
+int damf_gpu_get_config(const damf_gpu* h, damf_config* out) {
+  if (!h || !out) return DAMF_E_SHAPE_MISMATCH;
+  *out = h->cfg;
   return 0;
 }
 

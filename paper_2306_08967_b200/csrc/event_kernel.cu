@@ -1001,9 +1001,11 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
     }                                                                     \
   } while (0)
 
+// Returns false (nothing written) when the bordered system is not finite:
+// the reference throws NonFinite from dense_svd_small (svd.cpp:31-32).
 template <int C>
-DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& cl,
-                       const StepDesc& st) {
+DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& cl,
+                       const StepDesc& st, int64_t ev_index, int64_t step_index) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cl.block_rank();
   const int d = A.d;
@@ -1073,6 +1075,16 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   }
   wa2 = block_sum(S, wa2);
   wb2 = block_sum(S, wb2);
+  // M = diag(sigma, 0) + [w_a; r_a][w_b; r_b]^T is finite iff the gathered
+  // projections are (sigma > 0 is implied: 1/sqrt(sigma) enters w); the block
+  // sums are bit-identical in every CTA, so the cluster agrees on the exit
+  if (!isfinite(wa2) || !isfinite(wb2) || !isfinite(st.bnorm2)) {
+    if (rank == 0 && tid == 0) {
+      A.ctl->err = 7;  // NonFinite
+      A.ctl->err_event = ev_index;
+    }
+    return false;
+  }
   const double bnorm = sqrt(st.bnorm2);
   const double RA = sqrt(fmax(0.0, st.bnorm2 - wa2));
   const double rA = fmax(RA, 1e-12 * fmax(1.0, bnorm));  // update_engine.cpp:69-70,154
@@ -1263,6 +1275,30 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     sB_ += *cl.map_shared_rank(&S.partS[1], r);
   }
   cl.sync();  // B7b
+  // Modified-row log (DAMF_APPLY_LOG_ROWS): the base rows this step writes,
+  // i.e. the row sets of dX = outer(b, ex) and dY = outer(c, ey) / the
+  // appended row (types.hpp:101-116: one row per nonzero of b, none when the
+  // row vector is exactly zero; update_engine.cpp:93-117,197-202). A growing
+  // step has empty dX / dY (update_engine.cpp:98-109,186-196).
+  if (A.rowlog && rank == 0 && tid == 0 && k2 <= k) {
+    bool exnz = false, eynz = false;
+    for (int t = 0; t < k2; ++t) {
+      exnz = exnz || S.exv[t] != 0.0;
+      eynz = eynz || S.eyv[t] != 0.0;
+    }
+    auto put = [&](int side, int64_t row) {
+      const long long at = A.ctl->rowlog_n++;
+      if (at < A.rowlog_cap) {
+        A.rowlog[3 * at] = step_index;
+        A.rowlog[3 * at + 1] = side;
+        A.rowlog[3 * at + 2] = row;
+      }
+    };
+    if (exnz)
+      for (int q = 0; q < st.nb; ++q)
+        if (A.sp_vals[st.b_off + q] != 0.0) put(sA, A.sp_rows[st.b_off + q]);
+    if (eynz && (!edge || st.c_val != 0.0)) put(sB, st.c_row);
+  }
   PROF_MARK(7);
   double nH = 0, nE = 0;
   for (int t = tid; t < min(k2, k); t += NT) {
@@ -1362,6 +1398,7 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
                                        S.yA1, S.yB1, S.AHdH, S.AEdE);
         if (!ok && tid == 0) {
           A.ctl->err = 8;  // SingularProjection (factor_state.cpp:21-36)
+          A.ctl->err_event = ev_index;
         }
       }
       cl.sync();  // exact inverses visible
@@ -1524,6 +1561,7 @@ DAMF_D void rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       A.ctl->rows_y += 1;
   }
   PROF_MARK(11);
+  return true;
 }
 
 }  // namespace
@@ -2020,10 +2058,12 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     PROF_MARK(12);
     // ---- factor update (update_engine.cpp:206-226) ----------------------
     if (!(A.mode & 1)) {
-      for (int s = 0; s < ev.nsteps; ++s) {
+      bool fin = true;
+      for (int s = 0; s < ev.nsteps && fin; ++s) {
         const StepDesc st = A.steps[ev.step0 + s];
-        rank1_step<C>(A, S, cl, st);
+        fin = rank1_step<C>(A, S, cl, st, e, ev.step0 + s);
       }
+      if (!fin) break;  // NonFinite recorded in ctl; the batch stops here
     }
     if (FUSED) {
       cl.sync();  // factor / graph writes visible to the enhancer

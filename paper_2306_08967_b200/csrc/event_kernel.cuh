@@ -19,6 +19,8 @@ struct EventKernelArgs {
   unsigned long long* t_begin;  // per-event %globaltimer stamps (or null)
   unsigned long long* t_end;
   int mode;                 // DAMF_APPLY_* bits
+  int64_t* rowlog;          // (step, side 0=X / 1=Y, row) per modified base row, or null
+  long long rowlog_cap;     // triples
   // factor state
   DevCtl* ctl;
   int d, ld;

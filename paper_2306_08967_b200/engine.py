@@ -27,7 +27,7 @@ ERROR_KINDS = ["ParseError", "UnknownNode", "DuplicateEdge", "MissingEdge", "Sha
                "DegenerateLabels", "KTooLarge", "GraphTooSmall", "TooLarge", "IoError"]
 ADD_NODE, ADD_EDGE, REMOVE_EDGE = 0, 1, 2
 XB, YB, PX, PY, SIGMA, ZB, RB, X, Y, Z, QX, QY = range(12)
-APPLY_GRAPH_AND_PPR_ONLY, APPLY_DEFER_PUSH, APPLY_TIME_EVENTS = 1, 2, 4
+APPLY_GRAPH_AND_PPR_ONLY, APPLY_DEFER_PUSH, APPLY_TIME_EVENTS, APPLY_LOG_ROWS = 1, 2, 4, 8
 
 
 class DamfError(RuntimeError):
@@ -100,6 +100,8 @@ def lib():
         L.damf_gpu_apply.argtypes = [vp, C.POINTER(EventBatch), C.c_int32, C.POINTER(ApplyStats)]
         L.damf_gpu_event_latencies.argtypes = [vp, f64p, C.c_int64]
         L.damf_gpu_event_latencies.restype = C.c_int64
+        L.damf_gpu_row_log.argtypes = [vp, i64p, C.c_int64]
+        L.damf_gpu_row_log.restype = C.c_int64
         L.damf_gpu_query_rows.argtypes = [vp, C.c_int32, i64p, C.c_int64, f32p]
         L.damf_gpu_load_rows.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, vp]
         L.damf_gpu_score_pairs.argtypes = [vp, i64p, i64p, C.c_int64, C.c_int32, f64p]
@@ -262,6 +264,14 @@ class Engine:
         n = lib().damf_gpu_event_latencies(self.h, None, 0)
         out = np.zeros(n)
         lib().damf_gpu_event_latencies(self.h, _p(out, f64p), n)
+        return out
+
+    def row_log(self):
+        """(step, side, row) triples of the last apply with APPLY_LOG_ROWS:
+        the base rows each rank-1 step modified (side 0 = X_b, 1 = Y_b)."""
+        n = lib().damf_gpu_row_log(self.h, None, 0)
+        out = np.zeros((n, 3), np.int64)
+        lib().damf_gpu_row_log(self.h, _p(out, i64p), n)
         return out
 
     def diag(self):

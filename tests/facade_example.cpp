@@ -1,12 +1,16 @@
 // The C++ facade (damf::gpu::Engine) used the way a reference caller uses
-// damf::Engine: the known 2x2 edge update of test_update_engine.cpp:79-98
-// and an error of the reference's kind. Built by tests/test_facade.py.
+// damf::Engine: the known 2x2 edge update of test_update_engine.cpp:79-98,
+// an error of the reference's kind, Engine(g, cfg) (device t-SVD init,
+// engine.cpp:5-10), the resume constructor (engine.hpp:32-34) fed from the
+// accessors (engine.hpp:38-43) and a save/load round trip (io.cpp:182-269).
+// Built by tests/test_facade.py.
 #include <cmath>
 #include <cstdio>
 
 #include "../paper_2306_08967_b200/csrc/damf_engine.hpp"
 
-int main() {
+int main(int argc, char** argv) {
+  const char* path = argc > 1 ? argv[1] : "/tmp/facade_state.damf";
   damf::gpu::Csr g;
   g.n = 2;
   g.offsets = {0, 0, 0};
@@ -34,6 +38,42 @@ int main() {
     std::printf("caught %s (kind %d)\n", e.what(), (int)e.kind);
     ok = ok && e.kind == damf::gpu::Error::Kind::DuplicateEdge && e.event_index == 0;
   }
+
+  // Engine(g, cfg) on a 6-cycle plus chords (undirected), then the resume
+  // constructor from its own accessors: both answer the same queries
+  damf::gpu::Csr ring;
+  ring.n = 6;
+  std::vector<std::vector<int32_t>> adj(6);
+  auto link = [&](int a, int b) { adj[a].push_back(b); adj[b].push_back(a); };
+  for (int i = 0; i < 6; ++i) link(i, (i + 1) % 6);
+  link(0, 3);
+  link(1, 4);
+  ring.offsets.push_back(0);
+  for (auto& r : adj) {
+    for (int v : r) ring.targets.push_back(v);
+    ring.offsets.push_back((int64_t)ring.targets.size());
+  }
+  damf::gpu::RunConfig rc;
+  rc.d = 3;
+  rc.alpha = 0.3;
+  rc.eps = 1e-7;
+  rc.undirected = true;
+  damf::gpu::Engine a(ring, rc);
+  a.apply(damf::gpu::GraphEvent::add_edge(2, 5));
+  damf::gpu::Engine b(a.graph(), a.state(), a.enhancer(), a.config(), a.events_applied(),
+                      a.events_since_rebase());
+  double diff = 0;
+  for (int u = 0; u < 6; ++u)
+    for (int v = 0; v < 6; ++v) diff = std::fmax(diff, std::abs(a.score(u, v) - b.score(u, v)));
+  std::printf("Engine(g, cfg): k=%lld events=%llu; resumed copy max score diff %.3g\n",
+              (long long)a.diagnostics().k, (unsigned long long)b.events_applied(), diff);
+  ok = ok && diff < 1e-6 && b.events_applied() == 1;
+  a.save_state(path);
+  damf::gpu::Engine c = damf::gpu::Engine::load_state(path);
+  double diff2 = 0;
+  for (int u = 0; u < 6; ++u) diff2 = std::fmax(diff2, std::abs(a.score(u, u) - c.score(u, u)));
+  std::printf("load_state: alpha %.2f, max score diff %.3g\n", c.config().alpha, diff2);
+  ok = ok && diff2 < 1e-6 && c.config().alpha == 0.3 && c.config().undirected;
   std::printf(ok ? "facade ok\n" : "facade FAILED\n");
   return ok ? 0 : 1;
 }

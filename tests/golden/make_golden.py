@@ -13,7 +13,10 @@ reproduces them.
 
 Fixtures
   stream_directed.npz   eval.cpp:648-705 mixed stream (directed; node adds,
-                        edge adds, removals), d = 12, alpha = 0.3, eps 1e-6
+                        edge adds, removals), d = 12, alpha = 0.3, eps 1e-6;
+                        stream fixtures also hold `rowlog`, the (step, side,
+                        row) triples of every ProjectionUpdate's dX / dY
+                        (types.hpp:101-116)
   stream_undirected.npz random undirected graph (eval.cpp:616-631) + edge
                         insertions / removals, d = 16, alpha = 0.15, eps 1e-5
   init_tsvd.npz         FactorState::init_from_graph (svd.cpp:47-96) sigma and
@@ -43,13 +46,14 @@ def stream_fixture(name, g, ev, d, alpha, eps, seed):
     off, tgt, w = g.csr()
     init = {"xb0": oe.get(oe.XB), "yb0": oe.get(oe.YB), "px0": oe.get(oe.PX), "py0": oe.get(oe.PY),
             "sigma0": oe.get(oe.SIGMA)}
+    oe.row_log_enable()  # the dX / dY row sets of every rank-1 step
     oe.apply(ev)
     off1, ids1, deg1 = oe.graph_sets()
     np.savez_compressed(
         os.path.join(OUT, name), n=g.n, off=off, tgt=tgt, w=w, undirected=int(g.undirected), d=d,
         alpha=alpha, eps=eps, seed=seed, **init, **events_dict(ev),
         x=oe.get(oe.X), y=oe.get(oe.Y), z=oe.get(oe.Z), sigma=oe.get(oe.SIGMA),
-        g_off=off1, g_ids=ids1, g_deg=deg1)
+        g_off=off1, g_ids=ids1, g_deg=deg1, rowlog=oe.row_log())
 
 
 def main():

@@ -71,3 +71,34 @@ def dense_defect(n, off, tgt, deg, x, z, alpha):
             dfc = dfc + (1 - alpha) / deg[u] * nb
         worst = max(worst, np.abs(dfc).max() / max(deg[u], 1.0))
     return worst
+
+
+def sorted_rowlog(log):
+    """(step, side, row) triples in lexicographic order: the per-step dX / dY
+    row SETS (the write order inside a step is not part of the contract)."""
+    log = np.asarray(log, np.int64).reshape(-1, 3)
+    return log[np.lexsort((log[:, 2], log[:, 1], log[:, 0]))]
+
+
+def assert_rowlog_equal(dev, ora, what=""):
+    a, b = sorted_rowlog(dev), sorted_rowlog(ora)
+    if not np.array_equal(a, b):
+        sa = {tuple(r) for r in a.tolist()}
+        sb = {tuple(r) for r in b.tolist()}
+        raise AssertionError(f"{what} modified-row sets differ: device-only {sorted(sa - sb)[:8]}, "
+                             f"oracle-only {sorted(sb - sa)[:8]} ({len(a)} vs {len(b)} rows)")
+
+
+def weighted_defect(n, off, tgt, w, deg, x, z, alpha):
+    """dense_defect_bound (eval.cpp:591-610) with arc weights: per row
+    |alpha X + (1-alpha)/deg sum_v w_uv Z[v] - Z|_inf / max(deg, 1), fp64."""
+    import scipy.sparse as sp
+    x = np.asarray(x, np.float64)
+    z = np.asarray(z, np.float64)
+    src = np.repeat(np.arange(n), np.diff(off))
+    A = sp.csr_matrix((np.ones(len(tgt)) if w is None else np.asarray(w, np.float64),
+                       (src, np.asarray(tgt, np.int64))), shape=(n, n))
+    dfc = alpha * x - z
+    nz = deg > 0
+    dfc[nz] += ((1 - alpha) / deg[nz])[:, None] * (A @ z)[nz]
+    return (np.abs(dfc).max(1) / np.maximum(deg, 1.0)).max()

@@ -1,5 +1,7 @@
 """The header-only C++ facade (damf_engine.hpp) compiles against the C ABI
-and, on a GPU, reproduces a reference known answer through it."""
+and, on a GPU, reproduces a reference known answer through it, and runs the
+reference's three constructors (engine.hpp:29-34), accessors and DAMF v1
+persistence."""
 import os
 import subprocess
 
@@ -22,8 +24,9 @@ def test_facade_compiles_and_links():
 
 
 @pytest.mark.gpu
-def test_facade_known_answer_on_gpu():
+def test_facade_known_answer_on_gpu(tmp_path):
     build()
-    r = subprocess.run([EXE], capture_output=True, text=True, timeout=120)
+    r = subprocess.run([EXE, str(tmp_path / "facade.damf")], capture_output=True, text=True,
+                       timeout=120)
     print(r.stdout)
     assert r.returncode == 0 and "facade ok" in r.stdout

@@ -34,7 +34,9 @@ def test_oracle_reproduces_stream_fixture(name):
     oe = oracle.OracleEngine(graph(f), d=int(f["d"]), alpha=float(f["alpha"]), eps=float(f["eps"]),
                              seed=int(f["seed"]))
     assert np.allclose(oe.get(oe.SIGMA), f["sigma0"], rtol=1e-12, atol=0)
+    oe.row_log_enable()
     oe.apply(events(f))
+    assert np.array_equal(oe.row_log(), f["rowlog"])
     for key, which in (("x", oe.X), ("y", oe.Y), ("z", oe.Z), ("sigma", oe.SIGMA)):
         got = oe.get(which)
         assert np.abs(got - f[key]).max() <= 1e-12 * max(1.0, np.abs(f[key]).max()), key

@@ -11,7 +11,7 @@ import os
 import numpy as np
 import pytest
 
-from helpers import dense_defect, rel_frob, sampled_product_rel, sigma_rel
+from helpers import assert_rowlog_equal, dense_defect, rel_frob, sampled_product_rel, sigma_rel
 from paper_2306_08967_b200 import engine as ge
 from paper_2306_08967_b200.workloads import EventList
 
@@ -42,8 +42,10 @@ def test_stream_matches_golden(name):
                   eps=eps, undirected=bool(int(f["undirected"])), node_capacity=256)
     ev = EventList(*(f["ev_" + k] for k in ("kind", "u", "v", "w", "in_off", "in_ids", "in_w",
                                             "out_off", "out_ids", "out_w")))
-    st = e.apply(ev)
+    st = e.apply(ev, mode=ge.APPLY_LOG_ROWS)
     assert st["applied"] == len(ev), st
+    # the modified base rows of every rank-1 step, bit-exact (dX / dY sets)
+    assert_rowlog_equal(e.row_log(), f["rowlog"], name)
     off, ids, deg = e.graph_sets()
     assert np.array_equal(off, f["g_off"]) and np.array_equal(ids.astype(np.int64), f["g_ids"])
     assert np.array_equal(deg, f["g_deg"])

@@ -1,0 +1,348 @@
+"""Device vs oracle on the paths the configuration streams rarely reach:
+weighted graphs, periodic / forced rebases with alpha < 1, rank growth and
+shrinkage (eager folds) with and without the enhancer, failing events in the
+middle of an enhanced batch, non-finite inputs, the whole-GPU push path
+(node capacity above 2^20) with rebases requested mid-batch, and the
+modified-row sets of every rank-1 step (bit-exact).
+
+Every case runs the fp64 oracle (oracle/, pinned to the reference's doctest
+known answers) on the same inputs. Tolerances (stated per assert): products
+on sampled entries 1e-4 relative Frobenius, sigma 1e-6 relative, adjacency /
+degrees / row sets bit-exact, PPR by the reference's defect bound
+eps * (1 + 1e-6) (eval.cpp:591-610) plus the fp32 storage slack 2e-7."""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import (assert_rowlog_equal, gpu_from_oracle, product, rel_frob, sampled_product_rel,
+                     sigma_rel, weighted_defect)
+from paper_2306_08967_b200 import engine as ge
+from paper_2306_08967_b200.workloads import EventList
+
+pytestmark = pytest.mark.gpu
+F = ("kind", "u", "v", "w", "in_off", "in_ids", "in_w", "out_off", "out_ids", "out_w")
+
+
+def to_dev(ev):
+    return EventList(*(getattr(ev, f) for f in F))
+
+
+def defect_of(e, alpha):
+    off, ids, deg = e.graph_sets()
+    w = graph_weights(e)
+    return weighted_defect(e.n, off, ids, w, deg, e.get(ge.X), e.get(ge.Z), alpha)
+
+
+def graph_weights(e):
+    """Per-arc weights in graph_sets order (targets sorted per row), read from
+    the device's own DAMF v1 file (the C ABI exports weights only there)."""
+    off, ids, _ = e.graph_sets()
+    w = np.zeros(len(ids))
+    for u, row in enumerate(open_adj(e)):
+        w[off[u]:off[u + 1]] = [x[1] for x in sorted(row)]
+    return w
+
+
+def open_adj(e):
+    import os
+    import struct
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "s.damf")
+        e.save_state(p)
+        b = open(p, "rb").read()
+    pos = 4 + 4 + struct.calcsize("<qddQdqBQq")
+    (k,) = struct.unpack_from("<q", b, pos)
+    pos += 8 + 8 * k
+    for _ in range(6):
+        r, c = struct.unpack_from("<qq", b, pos)
+        pos += 16 + 8 * r * c
+    (n,) = struct.unpack_from("<q", b, pos)
+    pos += 8
+    adj = []
+    for _ in range(n):
+        (c,) = struct.unpack_from("<q", b, pos)
+        pos += 8
+        row = []
+        for _ in range(c):
+            v, w = struct.unpack_from("<qd", b, pos)
+            pos += 16
+            row.append((v, w))
+        adj.append(row)
+    return adj
+
+
+def compare(e, oe, what, wp_tol=1e-4):
+    p = sampled_product_rel(e.get(ge.X), e.get(ge.Y), oe.get(oe.X), oe.get(oe.Y))
+    s = sigma_rel(e.get(ge.SIGMA), oe.get(oe.SIGMA))
+    off, ids, deg = e.graph_sets()
+    oo, io, do = oe.graph_sets()
+    print(f"{what}: product {p:.2e} sigma {s:.2e} k {e.k}/{oe.dims()[1]}")
+    assert e.n == oe.dims()[0] and e.k == oe.dims()[1]
+    assert np.array_equal(off, oo) and np.array_equal(ids.astype(np.int64), io)
+    assert np.array_equal(deg, do)
+    assert p <= wp_tol and s <= 1e-6
+
+
+# ---------------------------------------------------------------- row sets
+@pytest.mark.parametrize("seed,d,alpha", [(4242, 16, 1.0), (77, 10, 0.3)])
+def test_mixed_stream_row_sets_bit_exact(seed, d, alpha):
+    # eval.cpp:648-705 mixed stream (node adds incl. zero-row neighbours whose
+    # dX / dY are empty, edge adds, removals), one apply call per 40 events
+    g, ev = oracle.gen_mixed_stream(140, 110, 420, 240, seed)
+    oe = oracle.OracleEngine(g, d=d, alpha=alpha, eps=1e-6, seed=seed)
+    e = gpu_from_oracle(g, oe, d=d, alpha=alpha, eps=1e-6)
+    total = 0
+    for a in range(0, len(ev), 40):
+        part = ev.slice(a, min(len(ev), a + 40))
+        oe.row_log_enable()
+        oe.apply(part)
+        e.apply(to_dev(part), mode=ge.APPLY_LOG_ROWS)
+        assert_rowlog_equal(e.row_log(), oe.row_log(), f"events {a}..")
+        total += len(oe.row_log())
+    print("rows compared", total)
+    compare(e, oe, "mixed stream")
+
+
+# ---------------------------------------------------------------- probe cases
+def random_case(d, alpha, weighted, every, undirected, seed, n=220, m=1400, events=150):
+    rng = np.random.default_rng(seed)
+    src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    key = (np.unique(np.minimum(src, dst) * n + np.maximum(src, dst)) if undirected
+           else np.unique(src * n + dst))
+    a, b = key // n, key % n
+    w = rng.uniform(0.5, 2.0, len(a)) if weighted else np.ones(len(a))
+    if undirected:
+        g = oracle.Graph(n, np.concatenate([a, b]), np.concatenate([b, a]), np.concatenate([w, w]),
+                         True)
+    else:
+        g = oracle.Graph(n, a, b, w, False)
+    have = set(zip(a.tolist(), b.tolist()))
+    kinds, us, vs, ws = [], [], [], []
+    while len(us) < events:
+        x, y = (int(t) for t in rng.integers(0, n, 2))
+        if x == y:
+            continue
+        k2 = (min(x, y), max(x, y)) if undirected else (x, y)
+        if k2 in have:
+            kinds.append(2)
+            have.discard(k2)
+        else:
+            kinds.append(1)
+            have.add(k2)
+        us.append(x)
+        vs.append(y)
+        ws.append(float(rng.uniform(0.5, 2.0)) if weighted else 1.0)
+    return g, oracle.Events.edges(np.array(kinds, np.int32), us, vs, ws)
+
+
+CASES = [("weighted-undirected-a1", 16, 1.0, True, 50000, True),
+         ("weighted-directed-a.3", 16, 0.3, True, 50000, False),
+         ("weighted-undirected-a.15", 12, 0.15, True, 50000, True),
+         ("rebase-every-40-a.3", 16, 0.3, False, 40, True),
+         ("rebase-every-40-a1", 24, 1.0, False, 40, False),
+         ("d2-a.3", 2, 0.3, False, 50000, True),
+         ("d1-a1", 1, 1.0, False, 50000, False),
+         ("d64-directed-a.2", 64, 0.2, False, 50000, False)]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_probe_cases_match_oracle(case):
+    name, d, alpha, weighted, every, undirected = case
+    g, ev = random_case(d, alpha, weighted, every, undirected, seed=d * 7 + int(alpha * 10) + every)
+    oe = oracle.OracleEngine(g, d=d, alpha=alpha, eps=1e-6, seed=d, rebase_every=every)
+    e = gpu_from_oracle(g, oe, d=d, alpha=alpha, eps=1e-6, rebase_every=every)
+    oe.row_log_enable()
+    st = e.apply(to_dev(ev), mode=ge.APPLY_LOG_ROWS)
+    oe.apply(ev)
+    assert st["applied"] == len(ev)
+    if every < 50000:
+        assert st["rebases"] >= len(ev) // every
+    assert_rowlog_equal(e.row_log(), oe.row_log(), name)
+    compare(e, oe, name)
+    if alpha < 1:
+        dfc = defect_of(e, alpha)
+        print(name, "weighted defect", dfc)
+        assert dfc <= 1e-6 * (1 + 1e-6) + 2e-7
+
+
+@pytest.mark.parametrize("undirected,alpha", [(True, 0.3), (False, 0.25), (True, 1.0)])
+def test_failing_event_mid_enhanced_batch(undirected, alpha):
+    # a DuplicateEdge in the middle of a batch: earlier events stay applied
+    # (the reference's per-event throw), the rest of the stream then agrees
+    g = oracle.gen_random_graph(300, 2400, 9, undirected=undirected)
+    oe = oracle.OracleEngine(g, d=12, alpha=alpha, eps=1e-6, seed=9)
+    e = gpu_from_oracle(g, oe, d=12, alpha=alpha, eps=1e-6)
+    off, tgt, _ = g.csr()
+    rng = np.random.default_rng(2)
+    us, vs = [], []
+    while len(us) < 30:
+        a, b = (int(x) for x in rng.integers(0, g.n, 2))
+        if (a != b and not np.any(tgt[off[a]:off[a + 1]] == b) and (a, b) not in zip(us, vs)
+                and (b, a) not in zip(us, vs)):
+            us.append(a)
+            vs.append(b)
+    ev = oracle.Events.edges(1, us[:10] + [us[3]] + us[10:20], vs[:10] + [vs[3]] + vs[10:20])
+    with pytest.raises(ge.DamfError) as ex:
+        e.apply(to_dev(ev))
+    assert ex.value.kind == "DuplicateEdge" and ex.value.index == 10
+    with pytest.raises(oracle.OracleError) as exo:
+        oe.apply(ev)
+    assert exo.value.index == 10
+    rest = oracle.Events.edges(1, us[20:], vs[20:])
+    e.apply(to_dev(rest))
+    oe.apply(rest)
+    compare(e, oe, f"after failure ({undirected}, {alpha})")
+    assert e.diag()["events_applied"] == 20
+    if alpha < 1:
+        assert defect_of(e, alpha) <= 1e-6 * (1 + 1e-6) + 2e-7
+
+
+# ---------------------------------------------------------------- rank changes
+def path_graph_case(alpha, undirected):
+    # 0-1-2 path (rank 2 at d = 2); removing an edge drops the rank (eager
+    # shrink, factor_state.cpp:168-192), re-adding it grows it back
+    # (update_engine.cpp:98-109,186-196, enhancer.cpp:178-194 for alpha < 1)
+    if undirected:
+        g = oracle.Graph(4, [0, 1, 1, 2, 2, 3], [1, 0, 2, 1, 3, 2], None, True)
+    else:
+        g = oracle.Graph(4, [0, 1, 2], [1, 2, 3], None, False)
+    return g
+
+
+@pytest.mark.parametrize("alpha,undirected", [(1.0, False), (0.3, False), (0.3, True)])
+def test_rank_shrink_and_regrow(alpha, undirected):
+    g = path_graph_case(alpha, undirected)
+    d = 3
+    oe = oracle.OracleEngine(g, d=d, alpha=alpha, eps=1e-8, seed=1)
+    e = gpu_from_oracle(g, oe, d=d, alpha=alpha, eps=1e-8, node_capacity=16)
+    k0 = oe.dims()[1]
+    steps = [(2, 1, 2), (2, 2, 3), (1, 1, 2), (1, 2, 3), (1, 0, 3), (2, 0, 1)]
+    ks = []
+    for kind, u, v in steps:
+        ev = oracle.Events.edges(kind, [u], [v])
+        oe.row_log_enable()
+        oe.apply(ev)
+        st = e.apply(to_dev(ev), mode=ge.APPLY_LOG_ROWS)
+        assert_rowlog_equal(e.row_log(), oe.row_log(), f"{kind} {u} {v}")
+        ks.append((e.k, oe.dims()[1], st["eager_folds"]))
+        P = product(e.get(ge.X), e.get(ge.Y))
+        Po = product(oe.get(oe.X), oe.get(oe.Y))
+        assert e.k == oe.dims()[1]
+        assert np.abs(P - Po).max() <= 1e-5 * max(1.0, np.abs(Po).max())
+        if alpha < 1:
+            z, zo = e.get(ge.Z).astype(np.float64), oe.get(oe.Z)
+            # both pushed to eps = 1e-8 from the same start: order noise only
+            assert np.abs(z - zo).max() <= 1e-5
+            assert defect_of(e, alpha) <= 1e-8 * (1 + 1e-6) + 2e-7
+    print("k0", k0, "(device k, oracle k, eager folds) per step:", ks)
+    assert min(k for k, _, _ in ks) < k0 or max(k for k, _, _ in ks) > k0
+    assert any(f > 0 for _, _, f in ks)
+
+
+def test_grow_with_enhancer_on_isolated_pair():
+    # fresh edges between isolated nodes grow the rank with alpha < 1
+    # (grow_column: r_b gains alpha * b in the new column, enhancer.cpp:178-194)
+    g = oracle.Graph(6, [1], [0], None, False)
+    oe = oracle.OracleEngine(g, d=4, alpha=0.4, eps=1e-9, seed=3)
+    e = gpu_from_oracle(g, oe, d=4, alpha=0.4, eps=1e-9, node_capacity=8)
+    for u, v in ((2, 3), (4, 5), (0, 1), (3, 4)):
+        ev = oracle.Events.edges(1, [u], [v])
+        oe.apply(ev)
+        e.apply(to_dev(ev))
+        assert e.k == oe.dims()[1]
+        assert np.abs(e.get(ge.Z).astype(np.float64) - oe.get(oe.Z)).max() <= 1e-6
+    compare(e, oe, "grow with enhancer")
+
+
+def test_periodic_rebase_with_enhancer_transforms_z_and_r():
+    # Engine::rebase with alpha < 1: Z_b, r_b <- . P_X (enhancer.cpp:196-206);
+    # queries are transparent to it (test_enhancer.cpp:166-196)
+    g, ev = random_case(12, 0.3, False, 7, True, seed=5, n=160, m=900, events=60)
+    oe = oracle.OracleEngine(g, d=12, alpha=0.3, eps=1e-7, seed=5, rebase_every=7)
+    e = gpu_from_oracle(g, oe, d=12, alpha=0.3, eps=1e-7, rebase_every=7)
+    st = e.apply(to_dev(ev))
+    oe.apply(ev)
+    assert st["rebases"] == len(ev) // 7
+    compare(e, oe, "rebase every 7")
+    z, zo = e.get(ge.Z).astype(np.float64), oe.get(oe.Z)
+    print("Z vs oracle", rel_frob(z, zo))
+    assert rel_frob(z, zo) <= 1e-4
+    assert defect_of(e, 0.3) <= 1e-7 * (1 + 1e-6) + 2e-7
+
+
+# ------------------------------------------------- whole-GPU push + rebases
+def test_large_capacity_push_path_resumes_after_requested_rebases():
+    # node capacity above 2^20 routes alpha < 1 through the whole-GPU push
+    # (one cooperative push per event); rebase_cond = 1 makes every event
+    # request a rebase (engine.cpp:38-40), so each launch group stops after
+    # one event and the batch must resume exactly there
+    g, ev = random_case(8, 0.3, False, 50000, True, seed=21, n=200, m=1200, events=40)
+    oe = oracle.OracleEngine(g, d=8, alpha=0.3, eps=1e-6, seed=21, rebase_cond=1.0)
+    e = gpu_from_oracle(g, oe, d=8, alpha=0.3, eps=1e-6, rebase_cond=1.0,
+                        node_capacity=(1 << 20) + 64)
+    st = e.apply(to_dev(ev))
+    oe.apply(ev)
+    print("applied", st)
+    assert st["applied"] == len(ev) and st["rebases"] >= len(ev) - 1
+    assert e.diag()["events_applied"] == len(ev)
+    compare(e, oe, "whole-GPU push, rebase per event")
+    assert defect_of(e, 0.3) <= 1e-6 * (1 + 1e-6) + 2e-7
+
+
+# ------------------------------------------------------------- weights / errors
+def test_unweighted_engine_takes_weighted_events():
+    # an engine built from an unweighted CSR stores no weights; weighted adds
+    # and their removals must still leave X Y^T and the degrees exact
+    g, _ = random_case(10, 0.3, False, 50000, True, seed=8, n=150, m=800, events=1)
+    oe = oracle.OracleEngine(g, d=10, alpha=0.3, eps=1e-6, seed=8)
+    e = gpu_from_oracle(g, oe, d=10, alpha=0.3, eps=1e-6)
+    off, tgt, _ = g.csr()
+    rng = np.random.default_rng(3)
+    pairs = []
+    while len(pairs) < 12:
+        a, b = (int(x) for x in rng.integers(0, g.n, 2))
+        if a != b and not np.any(tgt[off[a]:off[a + 1]] == b) and (a, b) not in pairs and (b, a) not in pairs:
+            pairs.append((a, b))
+    ws = rng.uniform(0.25, 3.0, len(pairs))
+    add = oracle.Events.edges(1, [p[0] for p in pairs], [p[1] for p in pairs], ws)
+    rem = oracle.Events.edges(2, [p[0] for p in pairs[:6]], [p[1] for p in pairs[:6]])
+    for ev in (add, rem):
+        oe.apply(ev)
+        e.apply(to_dev(ev))
+    compare(e, oe, "weighted events on an unweighted engine")
+    assert defect_of(e, 0.3) <= 1e-6 * (1 + 1e-6) + 2e-7
+
+
+def test_non_finite_inputs():
+    g = oracle.gen_random_graph(60, 300, 4, undirected=True)
+    oe = oracle.OracleEngine(g, d=6, alpha=1.0, seed=4)
+    e = gpu_from_oracle(g, oe, d=6, alpha=1.0, eps=1e-5)
+    off, tgt, _ = g.csr()
+    free = [(a, b) for a in range(60) for b in range(a + 1, 60) if not np.any(tgt[off[a]:off[a + 1]] == b)]
+    # +Inf weight: NonFinite before anything is mutated (svd.cpp:31-32)
+    with pytest.raises(ge.DamfError) as ex:
+        e.apply(EventList.edges(ge.ADD_EDGE, [free[0][0]], [free[0][1]], [np.inf]))
+    assert ex.value.kind == "NonFinite" and ex.value.index == 0
+    # NaN passes the reference's `w <= 0` test (graph.cpp:89-90) and fails in
+    # the SVD: NonFinite as well
+    with pytest.raises(ge.DamfError) as ex:
+        e.apply(EventList.edges(ge.ADD_EDGE, [free[1][0]], [free[1][1]], [np.nan]))
+    assert ex.value.kind == "NonFinite"
+    with pytest.raises(ge.DamfError) as ex:
+        e.apply(EventList.edges(ge.ADD_EDGE, [free[2][0]], [free[2][1]], [-1.0]))
+    assert ex.value.kind == "ParseError"
+    # a NaN base row reaches the bordered system: the device reports
+    # NonFinite for that event, earlier events of the batch stay applied
+    bad = free[3][0]
+    row = np.full((1, e.k), np.nan, np.float32)
+    e.load_rows(ge.XB, bad, row)
+    ok_pair = next(p for p in free[4:] if bad not in p)
+    ev = EventList.edges(ge.ADD_EDGE, [ok_pair[0], bad], [ok_pair[1], free[3][1]])
+    with pytest.raises(ge.DamfError) as ex:
+        e.apply(ev)
+    assert ex.value.kind == "NonFinite" and ex.value.index == 1
+    assert e.diag()["events_applied"] == 1
+    assert np.all(np.isfinite(e.get(ge.SIGMA)))

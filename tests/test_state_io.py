@@ -2,9 +2,12 @@
 
 The format is parsed / written here independently from the library (the
 layout of save_state: magic, version, RunConfig, counters, sigma, X_b, Y_b,
-P_X, P_Y, Z_b, r_b column-major fp64, then the adjacency), so a file the
-device writes is readable as the reference's, and a file laid out like the
-reference's (built from the oracle's fp64 state) resumes on the device."""
+P_X, P_Y, Z_b, r_b as i64 rows, i64 cols and fp64 data in Eigen RowMajor order
+-- DenseMatrix is RowMajor, types.hpp:17-18, and write_matrix dumps m.data(),
+io.cpp:51-56 -- then the adjacency), so a file the device writes is readable
+as the reference's, and a file laid out like the reference's resumes on the
+device. The oracle restates save_state / load_state too: files cross between
+the two in both directions bit-identically."""
 import os
 import struct
 
@@ -38,7 +41,7 @@ def read_damf(path):
 
     def mat():
         r, c = take("<qq")
-        return np.array(take(f"<{r * c}d")).reshape(c, r).T
+        return np.array(take(f"<{r * c}d")).reshape(r, c)  # row-major
 
     xb, yb, px, py, zb, rb = (mat() for _ in range(6))
     (n,) = take("<q")
@@ -60,7 +63,7 @@ def write_damf(path, st):
         f.write(struct.pack("<q", len(st["sigma"])) + np.asarray(st["sigma"], "<f8").tobytes())
         for m in (st["xb"], st["yb"], st["px"], st["py"], st["zb"], st["rb"]):
             m = np.asarray(m, np.float64)
-            f.write(struct.pack("<qq", *m.shape) + np.asfortranarray(m).tobytes(order="F"))
+            f.write(struct.pack("<qq", *m.shape) + np.ascontiguousarray(m).tobytes(order="C"))
         f.write(struct.pack("<q", len(st["adj"])))
         for row in st["adj"]:
             f.write(struct.pack("<q", len(row)))
@@ -118,3 +121,56 @@ def test_reference_layout_file_resumes_on_device(tmp_path):
     wp = rel_frob(product(e.get(ge.X), e.get(ge.Y)), product(oe.get(oe.X), oe.get(oe.Y)))
     print("after 20 more events: product vs oracle", wp)
     assert wp <= 1e-5
+
+
+def test_non_square_layout_is_row_major(tmp_path):
+    # n != k: a transposed or column-major file cannot pass this
+    g, ev = oracle.gen_mixed_stream(90, 70, 300, 10, 5)
+    oe = oracle.OracleEngine(g, d=6, alpha=0.3, eps=1e-6, seed=5)
+    e = gpu_from_oracle(g, oe, d=6, alpha=0.3, eps=1e-6)
+    path = str(tmp_path / "s.damf")
+    e.save_state(path)
+    raw = open(path, "rb").read()
+    st = read_damf(path)
+    xb = e.get(ge.XB).astype(np.float64)
+    assert st["xb"].shape == xb.shape and xb.shape[0] != xb.shape[1]
+    # the first row of X_b is the first k doubles of its payload
+    i = raw.index(struct.pack("<qq", *xb.shape)) + 16
+    assert np.array_equal(np.frombuffer(raw[i:i + 8 * xb.shape[1]], "<f8"), xb[0])
+
+
+def test_oracle_file_resumes_on_device_bit_identically(tmp_path):
+    # the oracle's restatement of save_state (io.cpp:182-219) writes the
+    # reference's file; the device loads it: fp32 rows = fp64 rows rounded,
+    # P / sigma and the adjacency exactly, and the device's own save_state
+    # of that engine loads back into the oracle with the same state
+    g, ev = oracle.gen_mixed_stream(160, 130, 520, 50, 13)
+    oe = oracle.OracleEngine(g, d=9, alpha=0.2, eps=1e-7, seed=13)
+    oe.apply(ev.slice(0, 30))
+    path = str(tmp_path / "oracle.damf")
+    oe.save_state(path)
+    e = ge.Engine.load_state(path, node_capacity=64)
+    for which, ow in ((ge.XB, oe.XB), (ge.YB, oe.YB), (ge.ZB, oe.ZB), (ge.RB, oe.RB)):
+        assert np.array_equal(e.get(which), oe.get(ow).astype(np.float32)), which
+    for which, ow in ((ge.PX, oe.PX), (ge.PY, oe.PY), (ge.SIGMA, oe.SIGMA)):
+        assert np.array_equal(e.get(which), oe.get(ow)), which
+    off_o, ids_o, deg_o = oe.graph_sets()
+    off_g, ids_g, deg_g = e.graph_sets()
+    assert np.array_equal(off_o, off_g) and np.array_equal(ids_o, ids_g.astype(np.int64))
+    assert np.array_equal(deg_o, deg_g)
+    dg = e.diag()
+    assert dg["events_applied"] == 30 and dg["events_since_rebase"] == 30
+    # device -> file -> oracle
+    path2 = str(tmp_path / "device.damf")
+    e.save_state(path2)
+    o2 = oracle.OracleEngine.load_state(path2)
+    for which, ow in ((ge.XB, oe.XB), (ge.YB, oe.YB), (ge.ZB, oe.ZB), (ge.RB, oe.RB)):
+        assert np.array_equal(o2.get(ow), e.get(which).astype(np.float64)), which
+    assert np.array_equal(o2.get(o2.PX), oe.get(oe.PX))
+    off2, ids2, _ = o2.graph_sets()
+    assert np.array_equal(off2, off_o) and np.array_equal(np.sort(ids2), np.sort(ids_o))
+    # both continue the stream and agree
+    e.apply(ev.slice(30, 50))
+    oe.apply(ev.slice(30, 50))
+    wp = rel_frob(product(e.get(ge.X), e.get(ge.Y)), product(oe.get(oe.X), oe.get(oe.Y)))
+    assert wp <= 1e-5, wp
