@@ -2,26 +2,38 @@
 """Benchmark of the B200 DAMF hot path (BASELINE.json metric:
 "edge updates/s & p50 us/update; Z=X.F and PPR-push GB/s vs HBM peak").
 
-Workload (a "step"): one batch of events of the config-2 stream (SBM,
-n = 100,000 in 20 blocks, d = 128, PPR alpha 0.15 eps 1e-5; inserts,
-deletions and node additions interleaved) applied through
-the C ABI (damf_gpu_apply) exactly as Engine::apply would, in order.
+Headline workload (N = 1, the largest BASELINE configuration that fits one
+GPU): config 5 -- R-MAT scale 26, ef 16 (seed 4; 67.1 M nodes, 2.10 B arcs,
+int64 offsets), d = 128, U / V random orthonormal with sigma_i = i^-1/2
+(34 GB fp32 each, generated on the device), the 10,000 degree-proportional
+single-edge insertions of the config, plus its one full materialisation.
+A "step" is one damf_gpu_apply call over the next 10,000 / (steps + warmup)
+insertions, applied sequentially exactly as `for (e : batch) Engine::apply(e)`.
 
-  value    events/s over the device-resident event processing (per-event
-           %globaltimer spans inside the kernel; inputs already in HBM)
-  e2e      events/s through the public call with host event buffers,
-           host->device descriptor copies and the device->host status read
-           inside the timed region (wall clock, synchronised)
-  roofline Z = X F materialisation (cfg 4 shape, n = 8,388,608, d = 128),
-           timed with CUDA events in this run; ppr_push roofline beside it
-  cpu_baseline  the fp64 oracle port (oracle/) on this host, 1 thread, on a
-           bounded prefix of the same stream (--impl reference times the
-           same port as the reference arm; the reference itself cannot be
-           built here: it needs Eigen3, absent)
+  value    insertions/s over the device span of the timed calls (CUDA events
+           from each call's first launch, event descriptors already in HBM,
+           to the end of its last kernel -- rebases included)
+  e2e      insertions/s through the public call (damf_gpu_apply) with the
+           events in host memory: descriptor build, H2D copy, the kernels and
+           the D2H status read, wall clock per call
+  latency  per-insertion device latency (%globaltimer stamps in the kernel)
+  roofline the config's full materialisation X = X_b P_X (n = 2^26, d = 128,
+           68.7 GB algorithmic), CUDA events on the engine stream
+  cpu_baseline  the fp64 oracle port (oracle/, 1 thread) applying the same
+           first insertions from the same initial factors (see cfg5_oracle)
 
-Multi-GPU (torchrun): the update chain does not shard, so each
-rank runs an independent replica of the stream ("replicas only", weak
-scaling) and value = total events / max-over-ranks time.
+Sub-benchmarks (`sub`): the config-2 SBM stream with its own CPU ratio,
+config-3 batches 1 / 64 / 1024, the config-4 materialisation sweep and PPR
+push, and CPU legs for query_all and init_propagate.
+
+`--impl reference` times the reference's CPU implementation (the oracle port;
+the reference itself cannot be built here) on the same
+config-5 insertions with the same output line.
+
+Multi-GPU: the update chain does not shard: N ranks run N
+independent replicas ("replicas only", weak scaling); value = total
+insertions / max-over-ranks device time. `--gpus N` without torchrun
+re-launches itself under torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -40,6 +52,9 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "edge updates/s & p50 us/update; Z=X.F and PPR-push GB/s vs HBM peak"
+WORKLOAD = ("cfg5: R-MAT scale 26 ef 16 seed 4 (67.1M nodes, 2.10B arcs), d=128, U/V orthonormal "
+            "sigma_i=i^-1/2, 10,000 degree-proportional single-edge insertions, alpha=1")
+CFG5_EVENTS = 10_000
 
 
 def peaks():
@@ -48,7 +63,19 @@ def peaks():
             p = json.load(f)
         return float(p["hbm_gbs"]), "measured"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_info():
+    cpu = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": cpu}
 
 
 class ClockSampler:
@@ -128,17 +155,7 @@ def dist_env():
     return ws, rank, local
 
 
-def build_cfg2(scale=1.0):
-    from paper_2306_08967_b200 import workloads as W
-    t0 = time.time()
-    w = W.cfg2()
-    n = w["n"]
-    eu, ev = w["init"]
-    off, tgt = W.undirected_csr(n, eu, ev)
-    return dict(w=w, n=n, off=off, tgt=tgt, gen_s=time.time() - t0)
-
-
-def descriptor_bytes(batch):
+def descriptor_bytes(batch, undirected=True):
     """Host->device bytes damf_gpu_apply copies for a batch (EventDesc 112 B,
     StepDesc 56 B, sparse rows 16 B/nnz, AddNode lists 16 B/entry, touched 8 B)."""
     kinds = batch.kind
@@ -146,138 +163,226 @@ def descriptor_bytes(batch):
     nin = int(batch.in_off[-1])
     edges = int(np.sum(kinds != 0))
     nodes = ne - edges
-    steps = 2 * ne  # undirected: two rank-1 steps per edge, two per node
+    steps = 2 * ne
     return ne * 112 + steps * 56 + (2 * edges + 2 * nin) * 16 + 2 * nin * 16 + (2 * edges + nin + nodes) * 8
+
+
+def split_steps(n_events, steps, warmup):
+    total = steps + warmup
+    per = max(1, n_events // total)
+    return per
+
+
+def timed_stream(eng, stream, per, steps, warmup, ws, local):
+    """Warm-up calls, then `steps` timed calls of `per` events each (one
+    damf_gpu_apply per step). Returns device seconds (sum of the calls'
+    device spans), wall seconds of the public calls, per-event latencies,
+    rebases, launches and the clocks summary."""
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    for s in range(warmup):
+        eng.apply(stream.slice(s * per, (s + 1) * per), mode=ge.APPLY_TIME_EVENTS)
+    dev_ms, wall_s, lat, h2d = 0.0, 0.0, [], []
+    rebases = 0
+    launches0 = eng.diag()["kernel_launches"]
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for s in range(warmup, warmup + steps):
+            batch = stream.slice(s * per, (s + 1) * per)
+            t0 = time.perf_counter()
+            st = eng.apply(batch, mode=ge.APPLY_TIME_EVENTS)
+            wall_s += time.perf_counter() - t0
+            dev_ms += st["device_ms"]
+            rebases += st["rebases"]
+            lat.extend(eng.latencies_us().tolist())  # read back outside the timed call
+            h2d.append(descriptor_bytes(batch))
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+    launches = eng.diag()["kernel_launches"] - launches0
+    return dict(dev_s=dev_ms * 1e-3, wall_s=wall_s, lat=np.array(lat), rebases=rebases,
+                launches=launches, h2d=int(np.mean(h2d)), clocks=clk.summary())
+
+
+def pct(lat):
+    return {"p50": round(float(np.percentile(lat, 50)), 2),
+            "p90": round(float(np.percentile(lat, 90)), 2),
+            "p99": round(float(np.percentile(lat, 99)), 2),
+            "mean": round(float(lat.mean()), 2), "events": int(len(lat))}
+
+
+# ------------------------------------------------------------------ cfg 5
+def build_cfg5(n_events):
+    """Device engine at config 5 and the stream (host arrays)."""
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    from paper_2306_08967_b200 import workloads as W
+    t0 = time.time()
+    d, n = 128, 1 << 26
+    keys, off, tgt, su, sv = W.cfg5_inputs(n_events)
+    edges = int(keys.numel())
+    del keys
+    torch.cuda.empty_cache()
+    sig = np.arange(1, d + 1, dtype=np.float64) ** -0.5
+    eng = ge.Engine(n, off, tgt, None, d, d, None, None, np.eye(d), np.eye(d), sig, alpha=1.0,
+                    undirected=True, node_capacity=1024, arc_capacity=1 << 24)
+    arcs = int(tgt.numel())
+    del off, tgt
+    torch.cuda.empty_cache()
+    W.orthonormal_rows_into(eng, ge.XB, n, d, sig, seed=40)
+    W.orthonormal_rows_into(eng, ge.YB, n, d, sig, seed=41)
+    stream = W.EventList.edges(ge.ADD_EDGE, su, sv)
+    return dict(eng=eng, stream=stream, su=su, sv=sv, n=n, d=d, sig=sig, edges=edges, arcs=arcs,
+                setup_s=time.time() - t0)
+
+
+def cfg5_materialize(eng, n, d, hbm, peak_kind):
+    """One full materialisation X = X_b P_X (query_all, factor_state.cpp:
+    120-123) into device memory; CUDA events on the engine stream."""
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    out = torch.empty(n, d, dtype=torch.float32, device="cuda")
+    es = torch.cuda.ExternalStream(eng.stream_ptr())
+    ms = []
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(es)
+        eng.materialize(ge.X, out.data_ptr(), on_device=True)
+        e1.record(es)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    del out
+    torch.cuda.empty_cache()
+    t = float(np.median(ms))
+    bytes_ = 8.0 * n * d + 8.0 * d * d
+    gbs = bytes_ / (t * 1e-3) / 1e9
+    return {"kernel": "materialize_tc128 (X = X_b P_X, n = 67,108,864, d = 128, 3 x TF32)",
+            "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(gbs / hbm, 4),
+            "traffic": ncu_traffic("r2_mat_cfg5_raw.csv", "materialize_tc128"),
+            "traffic_source": "profiles/r2_mat_cfg5_raw.csv (ncu --set full, same launch)",
+            "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(bytes_),
+            "launch_ms": round(t, 4), "launch_ms_all": [round(x, 4) for x in ms]}
+
+
+def cfg5_oracle(su, sv, n, d, sig, budget_s, max_events=None):
+    """The fp64 oracle (1 thread) applying config 5's insertions in order
+    from the same initial factors as the device (the fp32 rows
+    orthonormal_rows_into loads, widened). The reference's per-insertion work
+    reads and writes only the endpoints' rows and the k x k state
+    (update_engine.cpp:144-204, factor_state.cpp:158-213; alpha = 1 bypasses
+    the enhancer, enhancer.cpp:34-38), so the oracle Engine holds exactly the
+    stream's endpoints (their rows, the graph among them); Engine::apply --
+    graph mutation, two rank-1 updates, cond_estimate, the rebase policy -- is
+    timed per event with steady_clock like damf_cli.cpp:145-151."""
+    import oracle
+    from paper_2306_08967_b200 import workloads as W
+    m = len(su) if max_events is None else min(max_events, len(su))
+    rows = np.unique(np.concatenate([su[:m], sv[:m]]))
+    xb = W.orthonormal_rows_subset(n, d, sig, 40, rows).astype(np.float64)
+    yb = W.orthonormal_rows_subset(n, d, sig, 41, rows).astype(np.float64)
+    g = oracle.Graph(len(rows), np.zeros(0, np.int64), np.zeros(0, np.int64), None, True)
+    oe = oracle.OracleEngine(g, d=d, alpha=1.0, factors=(xb, yb, np.eye(d), np.eye(d), sig))
+    lu, lv = np.searchsorted(rows, su[:m]), np.searchsorted(rows, sv[:m])
+    total_s, done, lat = 0.0, 0, []
+    while done < m and total_s < budget_s:
+        b = min(m, done + 25)
+        ev = oracle.Events.edges(1, lu[done:b], lv[done:b])
+        t0 = time.perf_counter()
+        l = oe.apply(ev, lat=True)
+        total_s += time.perf_counter() - t0
+        lat.extend(l.tolist())
+        done = b
+    return {"value": round(done / total_s, 3), "unit": "insertions/s", "cores": 1, "kind": "port",
+            "sample": f"first {done} of the {len(su)} cfg5 insertions, in order, from the device's "
+                      f"initial factors; fp64 oracle Engine over the stream's endpoints "
+                      f"(per-event work is independent of n), 1 thread, {total_s:.1f} s",
+            "p50_ms": round(float(np.percentile(lat, 50)), 3),
+            "rebases": int(oe.stat(7)), "eager_folds": int(oe.stat(6))}
 
 
 def run_ours(args):
     import torch
-    from paper_2306_08967_b200 import engine as ge
-    from paper_2306_08967_b200 import workloads as W
-
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
     hbm, peak_kind = peaks()
-    data = build_cfg2()
-    w = data["w"]
-    stream = w["stream"]
-    steps_total = args.steps + args.warmup
-    per = args.events_per_step or max(1, len(stream) // steps_total)
-    if per * steps_total > len(stream):
-        per = len(stream) // steps_total
-    t_init = time.time()
-    # Engine(g, cfg): the reference's init (randomized t-SVD, seed 0) on the
-    # device, then init_propagate
-    eng = ge.Engine.from_graph(data["n"], data["off"], data["tgt"], None, w["d"], alpha=w["alpha"],
-                               eps=w["eps"], undirected=True, seed=0, node_capacity=4096)
-    torch.cuda.synchronize()
-    init_s = time.time() - t_init
-    es = torch.cuda.ExternalStream(eng.stream_ptr())
-    for s in range(args.warmup):
-        eng.apply(stream.slice(s * per, (s + 1) * per))
-    lat = []
-    dev_ms = []
-    wall_ms = []
-    h2d = []
-    launches0 = eng.diag()["kernel_launches"]
-    with ClockSampler(local) as clk:
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        for s in range(args.warmup, steps_total):
-            batch = stream.slice(s * per, (s + 1) * per)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            e0.record(es)
-            eng.apply(batch, mode=ge.APPLY_TIME_EVENTS)
-            e1.record(es)
-            t1 = time.perf_counter()
-            e1.synchronize()
-            dev_ms.append(e0.elapsed_time(e1))
-            wall_ms.append((t1 - t0) * 1e3)
-            lat.extend(eng.latencies_us().tolist())
-            h2d.append(descriptor_bytes(batch))
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-    launches = eng.diag()["kernel_launches"] - launches0
+    c5 = build_cfg5(CFG5_EVENTS)
+    eng = c5["eng"]
+    per = split_steps(len(c5["stream"]), args.steps, args.warmup)
+    r = timed_stream(eng, c5["stream"], per, args.steps, args.warmup, ws, local)
     ev_total = per * args.steps
-    # value: device-resident event processing (sum of per-event %globaltimer
-    # spans inside the kernel: inputs already in HBM); e2e: the public call
-    # with host event arrays, descriptor H2D, status D2H, wall clock
-    dev_s = float(np.sum(lat)) * 1e-6
-    wall_s = sum(wall_ms) / 1e3
-    dev_s, wall_s = job_max([dev_s, wall_s], device="cuda")
+    dev_s, wall_s = job_max([r["dev_s"], r["wall_s"]], device="cuda")
     value = replica_value(ev_total, ws, dev_s)
     e2e_value = replica_value(ev_total, ws, wall_s)
-    lat = np.array(lat)
-    diag = eng.diag()
+    roofline = cfg5_materialize(eng, c5["n"], c5["d"], hbm, peak_kind) if rank == 0 else None
+    dg = eng.diag()
     eng.close()
     del eng
-
+    c5["eng"] = None
+    torch.cuda.empty_cache()
     sub = {}
-    roofline = None
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cfg5_oracle(c5["su"], c5["sv"], c5["n"], c5["d"], c5["sig"], args.cpu_seconds)
+        cpu["host"] = host_info()
     if rank == 0 and not args.no_sub:
-        sub["materialize"], roofline = bench_materialize(args, hbm, peak_kind)
+        sub["cfg2"] = bench_cfg2(args)
+        sub["materialize_sweep"] = bench_materialize(args, hbm)
         if not args.quick:
             sub["ppr_push"] = bench_ppr(args, hbm, peak_kind)
         if args.cfg3_events > 0:
             sub["cfg3"] = bench_cfg3(args)
-        if args.cfg5_events > 0:
-            sub["cfg5"] = bench_cfg5(args, hbm)
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(data, per, args)
+        if not args.no_cpu and not args.quick:
+            sub["cpu_legs"] = cpu_legs(args)
     if rank != 0:
         return
     out = {
         "metric": METRIC,
         "value": round(value, 2),
-        "unit": "events/s",
+        "unit": "insertions/s",
         "n_gpus": ws,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(dev_s * 1e3 / args.steps, 4),
-        "stream_ms_per_step": round(sum(dev_ms) / args.steps, 4),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "fp64 small SVD / fp32 rows",
-        "data": "synthetic (seeded SBM, cfg 2)",
-        "config": {"workload": "cfg2: SBM n=100000 (20x5000), d=128, alpha=0.15, eps=1e-5, "
-                               "stream of inserts/deletions/node-adds",
-                   "events_per_step": per, "initial_edges": int(len(w["init"][0])),
+        "dtype": "f64 (d x d state, small SVD) / f32 (base rows)",
+        "data": "synthetic (seeded R-MAT scale 26 + random orthonormal factors, cfg 5)",
+        "config": {"workload": WORKLOAD, "events_per_step": per,
                    "parallelism": "replicas" if ws > 1 else "single",
-                   "l2": "event working set is L2-resident by design (latency-bound path); "
-                         "materialise input 4.3 GB > L2"},
-        "latency_us": {"p50": round(float(np.percentile(lat, 50)), 2),
-                       "p90": round(float(np.percentile(lat, 90)), 2),
-                       "p99": round(float(np.percentile(lat, 99)), 2),
-                       "mean": round(float(lat.mean()), 2), "events": int(len(lat))},
-        "e2e": {"value": round(e2e_value, 2), "unit": "events/s",
-                "h2d_bytes_per_step": int(np.mean(h2d)), "d2h_bytes_per_step": 8 * per + 256},
-        "gpu_launches": int(launches),
+                   "l2": "no flush: the 80 GB state is far above L2; each event's working set "
+                         "(P, P^-1, sigma, two rows) is L2-resident by design (latency-bound path)"},
+        "latency_us": pct(r["lat"]),
+        "e2e": {"value": round(e2e_value, 2), "unit": "insertions/s",
+                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": 8 * 8 + 400,
+                "note": "damf_gpu_apply with the step's events in host memory (descriptor build, "
+                        "H2D, kernels, control-block D2H), wall clock per call"},
+        "gpu_launches": int(r["launches"]),
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
-        "engine": {"init_s": round(init_s, 2), "gen_s": round(data["gen_s"], 2),
-                   "rank1_updates": None, "k": diag["k"], "device_bytes": diag["device_bytes"]},
+        "clocks": r["clocks"],
+        "engine": {"setup_s": round(c5["setup_s"], 1), "rebases_timed": int(r["rebases"]),
+                   "edges": c5["edges"], "arcs": c5["arcs"], "k": dg["k"],
+                   "device_bytes": dg["device_bytes"], "cond_end": dg["cond_estimate"]},
         "sub": sub,
     }
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------------------ subs
 def ncu_traffic(fname, kernel_substr):
     """dram__bytes_read.sum + dram__bytes_write.sum (bytes) of the first
     launch of `kernel_substr` in a committed `ncu --set full` raw capture under
     profiles/ (per launch, like roofline.achieved), or None."""
     import csv
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", fname)
+    path = os.path.join(ROOT, "profiles", fname)
     if not os.path.exists(path):
         return None
     rows = list(csv.reader(open(path)))
@@ -297,24 +402,80 @@ def ncu_traffic(fname, kernel_substr):
     return None
 
 
-def ppr_traffic():
-    """DRAM bytes of one init_propagate (all push / pull launches) from the
-    committed ncu launch list summary, or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        "r1_ppr23_traffic.json")
-    if not os.path.exists(path):
-        return None
-    return int(json.load(open(path))["dram_bytes_per_init"])
+def bench_cfg2(args):
+    """Config 2: SBM n = 100,000 (20 blocks), d = 128, alpha 0.15, eps 1e-5,
+    the stream of inserts / deletions / node additions (device t-SVD init),
+    plus its own CPU ratio: the oracle resumes from the device's saved state
+    (DAMF v1 file, io.cpp:182-269) after the warm-up and applies the same
+    timed events."""
+    import tempfile
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    from paper_2306_08967_b200 import workloads as W
+    w = W.cfg2()
+    n = w["n"]
+    eu, ev = w["init"]
+    off, tgt = W.undirected_csr(n, eu, ev)
+    t0 = time.time()
+    eng = ge.Engine.from_graph(n, off, tgt, None, w["d"], alpha=w["alpha"], eps=w["eps"],
+                               undirected=True, seed=0, node_capacity=4096)
+    init_s = time.time() - t0
+    stream = w["stream"]
+    warm = 500
+    eng.apply(stream.slice(0, warm), mode=ge.APPLY_TIME_EVENTS)
+    res = {"graph": "SBM n=100000 (20 x 5000), d=128, alpha=0.15, eps=1e-5", "init_s": round(init_s, 2)}
+    state = None
+    if not args.no_cpu:
+        state = os.path.join(tempfile.mkdtemp(), "cfg2.damf")
+        eng.save_state(state)
+    m = len(stream) - warm
+    dev_ms, wall_s, lat = 0.0, 0.0, []
+    for a in range(warm, len(stream), 500):
+        part = stream.slice(a, min(len(stream), a + 500))
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        st = eng.apply(part, mode=ge.APPLY_TIME_EVENTS)
+        wall_s += time.perf_counter() - t1
+        dev_ms += st["device_ms"]
+        lat.extend(eng.latencies_us().tolist())
+    lat = np.array(lat)
+    res.update({"events": m, "device_events_per_s": round(m / (dev_ms * 1e-3), 1),
+                "e2e_events_per_s": round(m / wall_s, 1), "latency_us": pct(lat)})
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    if state:
+        import oracle
+        t2 = time.time()
+        oe = oracle.OracleEngine.load_state(state)
+        load_s = time.time() - t2
+        done, total_s = 0, 0.0
+        while done < m and total_s < args.cpu_seconds:
+            b = min(m, done + 20)
+            part = stream.slice(warm + done, warm + b)
+            t3 = time.perf_counter()
+            oe.apply(part)
+            total_s += time.perf_counter() - t3
+            done = b
+        os.remove(state)
+        cpu_v = done / total_s
+        res["cpu_baseline"] = {"value": round(cpu_v, 3), "unit": "events/s", "cores": 1,
+                               "kind": "port",
+                               "sample": f"events {warm}..{warm + done} of the cfg2 stream, oracle "
+                                         f"resumed from the device's DAMF v1 state ({load_s:.1f} s "
+                                         f"load), fp64, 1 thread"}
+        res["device_vs_cpu"] = round(res["device_events_per_s"] / cpu_v, 1)
+        res["e2e_vs_cpu"] = round(res["e2e_events_per_s"] / cpu_v, 1)
+    return res
 
 
-def bench_materialize(args, hbm, peak_kind):
+def bench_materialize(args, hbm):
     """Z = X F on the cfg-4 shape (n = 2^23, X ~ N(0,1/d), F = Q diag(U[.5,2]))."""
     import torch
     from paper_2306_08967_b200 import engine as ge
     from paper_2306_08967_b200 import workloads as W
     n = 1 << 23
     res = {}
-    roof = None
     for d in (32, 64, 128, 256):
         g = torch.Generator(device="cuda")
         g.manual_seed(3)
@@ -324,38 +485,32 @@ def bench_materialize(args, hbm, peak_kind):
         st = torch.cuda.current_stream().cuda_stream
         for _ in range(3):
             ge.materialize_dev(X.data_ptr(), n, d, F, Z.data_ptr(), st)
-        ms = []
-        for _ in range(max(args.steps, 5)):
-            ms.append(ge.materialize_dev(X.data_ptr(), n, d, F, Z.data_ptr(), st))
+        ms = [ge.materialize_dev(X.data_ptr(), n, d, F, Z.data_ptr(), st) for _ in range(5)]
         t = float(np.mean(ms))
         bytes_ = 8.0 * n * d + 8.0 * d * d
         gbs = bytes_ / (t * 1e-3) / 1e9
         res[f"d{d}"] = {"ms": round(t, 4), "GBps": round(gbs, 1), "frac": round(gbs / hbm, 4),
                         "TFLOPs": round(2.0 * n * d * d / (t * 1e-3) / 1e12, 2)}
-        if d == 256:
-            # d = 256 runs three BF16 passes (kind::f16): also report the tensor
-            # side, 3 * 2 n d^2 bf16 flops against the measured bf16 peak
-            try:
-                bf16 = float(json.load(open(PEAKS_PATH))["bf16_tflops"])
-            except Exception:
-                bf16 = 2250.0
-            tf = 3 * 2.0 * n * d * d / (t * 1e-3) / 1e12
-            res["d256"]["traffic"] = ncu_traffic("r1_mat256_raw.csv", "materialize_bf16_256")
-            res["d256"]["traffic_source"] = "profiles/r1_mat256_raw.csv (ncu --set full, same shape)"
-            res["d256"]["tensor_side"] = {"passes": "3 x bf16 (hi*hi + hi*lo + lo*hi)",
-                                          "achieved_bf16_TFLOPs": round(tf, 1),
-                                          "peak_bf16_TFLOPs": round(bf16, 1), "frac": round(tf / bf16, 4)}
-        if d == 128:
-            roof = {"kernel": "materialize (Z=X.F, n=8388608, d=128)", "bound": "hbm",
-                    "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(gbs / hbm, 4),
-                    "traffic": ncu_traffic("r1_mat128_raw.csv", "materialize_tc128"),
-                    "traffic_source": "profiles/r1_mat128_raw.csv (ncu --set full, same shape)",
-                    "peak_kind": peak_kind,
-                    "algorithmic_bytes_per_launch": int(bytes_), "launch_ms": round(t, 4)}
         del X, Z
         torch.cuda.empty_cache()
-    return res, roof
+    res["d256"]["traffic"] = ncu_traffic("r1_mat256_raw.csv", "materialize_bf16_256")
+    return res
+
+
+def rmat_engine(scale, ef, seed, d, alpha, eps):
+    import torch
+    from paper_2306_08967_b200 import engine as ge
+    from paper_2306_08967_b200 import workloads as W
+    n = 1 << scale
+    keys = W.rmat_keys_device(scale, ef, seed)
+    off, tgt = W.csr_from_keys_device(n, keys)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    X = (torch.randn(n, d, device="cuda", generator=g) / math.sqrt(d)).contiguous()
+    F = W.cfg4_F(d, seed)
+    eng = ge.Engine(n, off, tgt, None, d, d, X, X, F, np.eye(d), np.ones(d), alpha=alpha,
+                    eps=eps, undirected=True, node_capacity=1024)
+    return eng, keys, off, tgt, X, F
 
 
 def bench_ppr(args, hbm, peak_kind):
@@ -364,31 +519,22 @@ def bench_ppr(args, hbm, peak_kind):
     import torch
     from paper_2306_08967_b200 import engine as ge
     from paper_2306_08967_b200 import workloads as W
-    scale = args.ppr_scale
-    d = 128
-    t0 = time.time()
-    u, v = W.rmat_edges(scale, 24, 3, device="cuda")
+    scale, d = args.ppr_scale, 128
     n = 1 << scale
-    src = torch.cat([u, v])
-    dst = torch.cat([v, u])
-    order = torch.argsort(src * n + dst)
-    src, dst = src[order], dst[order]
-    cnt = torch.bincount(src, minlength=n)
-    off = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
-    off[1:] = torch.cumsum(cnt, 0)
-    off_h = off.cpu().numpy()
-    tgt_h = dst.to(torch.int32).cpu().numpy()
-    arcs = len(tgt_h)
-    del src, dst, order, cnt, off, u, v
-    g = torch.Generator(device="cuda")
-    g.manual_seed(3)
-    X = (torch.randn(n, d, device="cuda", generator=g) / math.sqrt(d)).cpu().numpy()
-    F = W.cfg4_F(d, 3)
-    gen_s = time.time() - t0
-    eng = ge.Engine(n, off_h, tgt_h, None, d, d, X, X, F, np.eye(d), np.ones(d), alpha=0.15,
-                    eps=1e-5, undirected=True, node_capacity=1024)
+    t0 = time.time()
+    eng, keys, off, tgt, X, F = rmat_engine(scale, 24, 3, d, 0.15, 1e-5)
+    arcs = int(tgt.numel())
     del X
+    gen_s = time.time() - t0
     es = torch.cuda.ExternalStream(eng.stream_ptr())
+
+    def gbytes(a, b):
+        F_ = b["frontier"] - a["frontier"]
+        L_ = b["affected"] - a["affected"]
+        arcsL = b["affected_arcs"] - a["affected_arcs"]
+        pulled = b["pulled_arcs"] - a["pulled_arcs"]
+        return 16.0 * d * F_ + 8.0 * L_ + 4.0 * arcsL + 8.0 * d * L_ + 4.0 * d * pulled
+
     c0 = eng.push_counters()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -398,34 +544,19 @@ def bench_ppr(args, hbm, peak_kind):
     e1.synchronize()
     ms_init = e0.elapsed_time(e1)
     c1 = eng.push_counters()
-
-    def gbytes(a, b):
-        F_ = b["frontier"] - a["frontier"]
-        L_ = b["affected"] - a["affected"]
-        arcsL = b["affected_arcs"] - a["affected_arcs"]
-        pulled = b["pulled_arcs"] - a["pulled_arcs"]
-        return 16.0 * d * F_ + 8.0 * L_ + 4.0 * arcsL + 8.0 * d * L_ + 4.0 * d * pulled
-
     b_init = gbytes(c0, c1)
     gbs_init = b_init / (ms_init * 1e-3) / 1e9
-    # 1,000 random insertions absorbed (structure only), then one push
     rng = np.random.default_rng(4)
-    us = rng.integers(0, n, 3000)
-    vs = rng.integers(0, n, 3000)
-    off_set = set()
-    eu, evv = [], []
-    for a, b in zip(us.tolist(), vs.tolist()):
-        if a == b or (a, b) in off_set:
-            continue
-        row = tgt_h[off_h[a]:off_h[a + 1]]
-        if np.any(row == b):
-            continue
-        off_set.add((a, b))
-        off_set.add((b, a))
-        eu.append(a)
-        evv.append(b)
-        if len(eu) == 1000:
-            break
+    us, vs = rng.integers(0, n, 3000), rng.integers(0, n, 3000)
+    lo, hi = np.minimum(us, vs), np.maximum(us, vs)
+    kk = torch.as_tensor((lo << 32) | hi, device="cuda")
+    pos = torch.searchsorted(keys, kk).clamp(max=keys.numel() - 1)
+    fresh = ((keys[pos] != kk).cpu().numpy()) & (lo != hi)
+    _, first = np.unique((lo << 32) | hi, return_index=True)
+    ok = np.zeros(len(us), bool)
+    ok[first] = True
+    ok &= fresh
+    eu, evv = us[ok][:1000], vs[ok][:1000]
     eng.apply(W.EventList.edges(ge.ADD_EDGE, eu, evv),
               mode=ge.APPLY_GRAPH_AND_PPR_ONLY | ge.APPLY_DEFER_PUSH)
     c2 = eng.push_counters()
@@ -437,7 +568,7 @@ def bench_ppr(args, hbm, peak_kind):
     c3 = eng.push_counters()
     b_push = gbytes(c2, c3)
     eng.close()
-    del eng
+    del eng, keys, off, tgt
     torch.cuda.empty_cache()
     return {"graph": f"R-MAT scale {scale} ef 24 (n={n}, arcs={arcs})", "gen_s": round(gen_s, 1),
             "init_propagate": {"ms": round(ms_init, 3), "rounds": st["push_rounds"],
@@ -447,49 +578,49 @@ def bench_ppr(args, hbm, peak_kind):
                                         "pushes": st2["pushes"],
                                         "alg_GB": round(b_push / 1e9, 4),
                                         "GBps": round(b_push / (ms_push * 1e-3) / 1e9, 1)},
-            "roofline": {"kernel": "ppr_push_kernel (init_propagate)", "bound": "hbm",
-                         "achieved": round(gbs_init, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(gbs_init / hbm, 4),
-                         "traffic": ppr_traffic(),
-                         "traffic_source": "profiles/r1_ppr23_traffic.json (ncu DRAM bytes summed "
-                                           "over every launch of one init_propagate, same graph)",
-                         "peak_kind": peak_kind}}
+            "roofline": {"kernel": "ppr_push_kernel + ppr_pull_kernel (init_propagate)",
+                         "bound": "hbm", "achieved": round(gbs_init, 1), "peak": hbm,
+                         "unit": "GB/s", "frac": round(gbs_init / hbm, 4),
+                         "traffic": ppr_traffic(), "peak_kind": peak_kind}}
+
+
+def ppr_traffic():
+    path = os.path.join(ROOT, "profiles", "r1_ppr23_traffic.json")
+    if not os.path.exists(path):
+        return None
+    return int(json.load(open(path))["dram_bytes_per_init"])
 
 
 def stream_latencies(eng, ev, batch, max_events):
-    """Apply ev[:max_events] in batches of `batch` events (one apply call per
-    batch, sequential inside); per-event device latencies (us) and the wall
-    time of the calls."""
+    """Apply ev[:max_events] in calls of `batch` events: per-event device
+    latencies, device span and wall time of the calls."""
     import torch
     from paper_2306_08967_b200 import engine as ge
     lat = []
-    t_wall = 0.0
-    rebases = folds = 0
+    t_wall = dev_ms = 0.0
+    rebases = 0
     m = min(len(ev), max_events)
+    torch.cuda.synchronize()
     for a in range(0, m, batch):
         part = ev.slice(a, min(m, a + batch))
-        torch.cuda.synchronize()
         t0 = time.perf_counter()
         st = eng.apply(part, mode=ge.APPLY_TIME_EVENTS)
-        rebases += st["rebases"]
-        folds += st["eager_folds"]
-        torch.cuda.synchronize()
         t_wall += time.perf_counter() - t0
+        dev_ms += st["device_ms"]
+        rebases += st["rebases"]
         lat.extend(eng.latencies_us().tolist())
     lat = np.array(lat)
-    return {"events": int(m), "batch": batch,
-            "p50_us": round(float(np.percentile(lat, 50)), 2),
-            "p90_us": round(float(np.percentile(lat, 90)), 2),
-            "p99_us": round(float(np.percentile(lat, 99)), 2),
-            "device_events_per_s": round(m / (lat.sum() * 1e-6), 1),
-            "e2e_events_per_s": round(m / t_wall, 1), "rebases": int(rebases),
-            "eager_folds": int(folds), "cond_end": float(eng.diag()["cond_estimate"])}
+    return {"events": int(m), "batch": batch, **{k + "_us": v for k, v in pct(lat).items()
+                                                  if k in ("p50", "p90", "p99")},
+            "device_events_per_s": round(m / (dev_ms * 1e-3), 1),
+            "kernel_events_per_s": round(m / (lat.sum() * 1e-6), 1),
+            "e2e_events_per_s": round(m / t_wall, 1), "rebases": int(rebases)}
 
 
 def bench_cfg3(args):
     """Config 3: R-MAT scale 22, ef 16 (seed 2), d = 128, all but 100,000
     edges in the snapshot (randomized t-SVD on the device), held-out edges
-    streamed as insertions in batches of 1, 64 and 1024 (alpha = 1)."""
+    streamed as insertions in calls of 1, 64 and 1024 events (alpha = 1)."""
     import torch
     from paper_2306_08967_b200 import engine as ge
     from paper_2306_08967_b200 import workloads as W
@@ -511,8 +642,6 @@ def bench_cfg3(args):
     del off, tgt
     torch.cuda.empty_cache()
     gen_s = time.time() - t0
-    # Engine(g, cfg): the reference's init (randomized t-SVD, d + 10, 4 power
-    # iterations) on the device (damf_gpu_create)
     t1 = time.time()
     eng = ge.Engine.from_graph(n, off_h, tgt_h, None, d, alpha=1.0, undirected=True, seed=2,
                                node_capacity=1024, arc_capacity=1 << 22)
@@ -520,9 +649,8 @@ def bench_cfg3(args):
     del off_h, tgt_h
     ev = W.EventList.edges(ge.ADD_EDGE, su, sv)
     res = {"graph": f"R-MAT scale 22 ef 16 (n={n}, edges={edges}), d=128, alpha=1",
-           "setup_s": round(gen_s, 1),
-           "init_s": round(init_s, 1),
-           "init": "damf_gpu_create: device randomized t-SVD (l = d + 10, 4 power iterations; sketch from the device Philox stream at this size)"}
+           "setup_s": round(gen_s, 1), "init_s": round(init_s, 1),
+           "init": "damf_gpu_create: device randomized t-SVD (l = d + 10, 4 power iterations)"}
     a = 0
     for batch, m in ((1, args.cfg3_events // 4), (64, args.cfg3_events // 2),
                      (1024, args.cfg3_events)):
@@ -535,123 +663,96 @@ def bench_cfg3(args):
     return res
 
 
-def bench_cfg5(args, hbm):
-    """Config 5: R-MAT scale 26, ef 16 (seed 4), int32 ids / int64 offsets,
-    d = 128, U and V random orthonormal columns with sigma_i = i^-0.5 (34 GB
-    each, generated in place on the device), 10,000 degree-proportional
-    single-edge insertions, one full materialisation X = X_b P_X."""
+def cpu_legs(args):
+    """CPU legs beside the GPU for the two bulk paths (oracle port, fp64,
+    1 thread): query_all (X_b P_X, factor_state.cpp:120-123) on a 2^20-row
+    slice of the cfg-4 shape at d = 128, and init_propagate
+    (enhancer.cpp:26-47) on an R-MAT scale-16 ef-24 graph at d = 128 with the
+    device's init_propagate on the same graph and signal."""
     import torch
+    import oracle
     from paper_2306_08967_b200 import engine as ge
     from paper_2306_08967_b200 import workloads as W
-    t0 = time.time()
-    scale, d = 26, 128
-    n = 1 << scale
-    keys = W.rmat_keys_device(scale, 16, 4)
-    off, tgt = W.csr_from_keys_device(n, keys)
-    su, sv = W.degree_proportional_inserts(keys, tgt, args.cfg5_events, seed=4)
-    edges = int(keys.numel())
-    del keys
-    torch.cuda.empty_cache()
-    sig = np.arange(1, d + 1, dtype=np.float64) ** -0.5
-    eng = ge.Engine(n, off, tgt, None, d, d, None, None, np.eye(d), np.eye(d), sig, alpha=1.0,
-                    undirected=True, node_capacity=1024, arc_capacity=1 << 24)
-    arcs = int(tgt.numel())
-    del off, tgt
-    torch.cuda.empty_cache()
-    W.orthonormal_rows_into(eng, ge.XB, n, d, sig, seed=40)
-    W.orthonormal_rows_into(eng, ge.YB, n, d, sig, seed=41)
-    setup_s = time.time() - t0
-    ev = W.EventList.edges(ge.ADD_EDGE, su, sv)
-    r = stream_latencies(eng, ev, 1000, len(ev))
-    # one full materialisation X = X_b P_X into device memory
-    out = torch.empty(n, d, dtype=torch.float32, device="cuda")
+    out = {}
+    d, rows = 128, 1 << 20
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((rows, d)) / math.sqrt(d)
+    F = W.cfg4_F(d, 3)
+    _, ms = oracle.materialize_time_ms(x, F)
+    gbs = 8.0 * rows * d / (ms * 1e-3) / 1e9
+    out["query_all"] = {"rows": rows, "d": d, "cpu_ms": round(ms, 1), "cpu_GBps_fp32_equiv": round(gbs, 3),
+                        "cores": 1, "kind": "port"}
+    scale = 16
+    eng, keys, off, tgt, X, F4 = rmat_engine(scale, 24, 5, d, 0.15, 1e-5)
     es = torch.cuda.ExternalStream(eng.stream_ptr())
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(es)
-    eng.materialize(ge.X, out.data_ptr(), on_device=True)
+    st = eng.ppr_init()
     e1.record(es)
     e1.synchronize()
-    ms = e0.elapsed_time(e1)
-    gbs = 8.0 * n * d / (ms * 1e-3) / 1e9
-    dg = eng.diag()
+    gms = e0.elapsed_time(e1)
+    n = 1 << scale
+    off_h, tgt_h = off.cpu().numpy(), tgt.cpu().numpy().astype(np.int64)
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(off_h))
+    xh = X.cpu().numpy().astype(np.float64)
     eng.close()
-    del eng, out
+    del eng, keys, off, tgt, X
     torch.cuda.empty_cache()
-    return {"graph": f"R-MAT scale 26 ef 16 (n={n}, edges={edges}, arcs={arcs}), d=128, alpha=1",
-            "setup_s": round(setup_s, 1), "updates": r,
-            "materialize": {"ms": round(ms, 3), "GBps": round(gbs, 1),
-                            "frac": round(gbs / hbm, 4)},
-            "device_bytes": dg["device_bytes"]}
+    g = oracle.Graph(n, src, tgt_h, None, True)
+    t0 = time.perf_counter()
+    oe = oracle.OracleEngine(g, d=d, alpha=0.15, eps=1e-5,
+                             factors=(xh, xh, F4, np.eye(d), np.ones(d)))
+    cms = (time.perf_counter() - t0) * 1e3
+    out["init_propagate"] = {"graph": f"R-MAT scale {scale} ef 24 (arcs={len(tgt_h)}), d={d}, "
+                                      "alpha 0.15, eps 1e-5",
+                             "gpu_ms": round(gms, 3), "gpu_pushes": st["pushes"],
+                             "cpu_ms_incl_engine_build": round(cms, 1),
+                             "cpu_pushes": int(oe.stat(5)), "speedup": round(cms / gms, 1),
+                             "cores": 1, "kind": "port"}
+    return out
 
 
-def cpu_baseline(data, per, args, max_events=None, budget_s=None):
-    """The oracle port (fp64, 1 thread) on the same initial state and the
-    first events of the same stream."""
-    import oracle
-    w = data["w"]
-    n = data["n"]
-    src, dst = None, None
-    from paper_2306_08967_b200 import workloads as W
-    src, dst = W.csr_arcs(data["off"], data["tgt"])
-    g = oracle.Graph(n, src, dst, None, True)
-    t0 = time.time()
-    # Engine(g, cfg) in the fp64 restatement: the reference's own t-SVD init
-    # (same seed and Gaussian stream as the device) and init_propagate
-    oe = oracle.OracleEngine(g, d=w["d"], alpha=w["alpha"], eps=w["eps"], seed=0)
-    init_s = time.time() - t0
-    budget = budget_s if budget_s is not None else args.cpu_seconds
-    total_ev = 0
-    total_s = 0.0
-    pos = 0
-    stream = w["stream"]
-    lat = []
-    while total_s < budget and pos < len(stream):
-        m = min(20, len(stream) - pos)
-        t1 = time.perf_counter()
-        l = oe.apply(stream.slice(pos, pos + m), lat=True)
-        total_s += time.perf_counter() - t1
-        lat.extend(l.tolist())
-        pos += m
-        total_ev += m
-        if max_events and total_ev >= max_events:
-            break
-    return {"value": round(total_ev / total_s, 3), "unit": "events/s", "cores": 1, "kind": "port",
-            "sample": f"first {total_ev} events of the cfg2 stream after the oracle's Engine(g, cfg) init (t-SVD + init_propagate) "
-                      f"({init_s:.1f} s), fp64, 1 thread",
-            "p50_ms": round(float(np.percentile(lat, 50)), 3), "init_s": round(init_s, 1)}
-
-
+# ------------------------------------------------------------- reference arm
 def run_reference(args):
-    ws, rank, _ = dist_env()
+    ws, rank, local = dist_env()
     if rank != 0:
         return
-    data = build_cfg2()
-    per = 20
-    # a bounded sample of the stream on the CPU port (the reference is
-    # single-threaded, SPEC.md:285): events in order until the time budget
-    res = cpu_baseline(data, per, args, budget_s=args.cpu_seconds)
-    out = {"metric": METRIC, "value": res["value"], "unit": "events/s", "n_gpus": ws,
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2306_08967_b200 import workloads as W
+    # inputs of the same workload: the cfg-5 graph and insertions (device
+    # generation through torch, input preparation only)
+    keys, off, tgt, su, sv = W.cfg5_inputs(CFG5_EVENTS)
+    del keys, off, tgt
+    torch.cuda.empty_cache()
+    d, n = 128, 1 << 26
+    sig = np.arange(1, d + 1, dtype=np.float64) ** -0.5
+    per = split_steps(len(su), args.steps, args.warmup)
+    # the same timed insertions as our arm (after its warm-up), bounded by time
+    a = per * args.warmup
+    res = cfg5_oracle(su, sv, n, d, sig, budget_s=args.cpu_seconds,
+                      max_events=min(len(su), a + per * args.steps))
+    res["host"] = host_info()
+    out = {"metric": METRIC, "value": res["value"], "unit": "insertions/s", "n_gpus": ws,
            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "fp64", "impl": "reference",
-           "data": "synthetic (seeded SBM, cfg 2)",
-           "config": {"workload": "cfg2: SBM n=100000 (20x5000), d=128, alpha=0.15, eps=1e-5",
-                      "parallelism": "single"},
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+           "data": "synthetic (seeded R-MAT scale 26 + random orthonormal factors, cfg 5)",
+           "config": {"workload": WORKLOAD, "events_per_step": per, "parallelism": "single"},
            "cpu_baseline": res,
-           "e2e": {"value": res["value"], "unit": "events/s", "h2d_bytes_per_step": 0,
+           "e2e": {"value": res["value"], "unit": "insertions/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
-           "note": "reference arm = fp64 C++ restatement of the reference (oracle/), 1 thread; "
-                   "the reference itself needs Eigen3 (absent) and cannot be built here"}
-    print(json.dumps(out))
+           "note": "reference arm = fp64 C++ restatement of the reference (oracle/), 1 thread, "
+                   "the reference being single-threaded (SPEC.md:285); the reference itself "
+                   "needs Eigen3 (absent) and cannot be built here"}
+    print(json.dumps(out), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=9)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--events-per-step", type=int, default=0)
     ap.add_argument("--no-sub", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true")
@@ -659,9 +760,16 @@ def main():
     ap.add_argument("--ppr-scale", type=int, default=23)
     ap.add_argument("--cfg3-events", type=int, default=4096,
                     help="events per batch-size leg of config 3 (0 = skip)")
-    ap.add_argument("--cfg5-events", type=int, default=10000,
-                    help="insertions streamed at config 5 (0 = skip)")
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:
+        # not under torchrun: launch N ranks (one process per GPU)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if ws and ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args)
     else:

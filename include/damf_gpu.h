@@ -66,7 +66,11 @@ enum {
   DAMF_Y = 8,      /* current Y = Y_b P_Y  (query_all / query_content)           */
   DAMF_Z = 9,      /* enhanced Z = Z_b P_X (query_enhanced)                      */
   DAMF_QX = 10,    /* maintained inverse P_X^{-1} (k x k, fp64; GPU-only state)  */
-  DAMF_QY = 11
+  DAMF_QY = 11,
+  DAMF_XB64 = 12,  /* X_b exactly, fp64 (n x k): the fp32 rows widened, the rows
+                      written through P^-1 since the last fold at their fp64
+                      values (the reference's X_b is fp64, types.hpp:15-19)     */
+  DAMF_YB64 = 13
 };
 
 /* RunConfig (engine.hpp:13-21) plus device sizing. */
@@ -139,6 +143,9 @@ typedef struct damf_apply_stats {
   int64_t eager_folds;   /* rank change / ill-conditioned folds           */
   int64_t push_rounds;   /* frontier rounds of the PPR push               */
   int64_t pushes;        /* rows pushed                                   */
+  double device_ms;      /* DAMF_APPLY_TIME_EVENTS: device span of the call
+                            (CUDA events from the first launch to the end of
+                            its last kernel, rebases included), else 0     */
 } damf_apply_stats;
 
 typedef struct damf_diag {
@@ -222,7 +229,9 @@ int damf_gpu_load_state(const char* path, const damf_config* sizing, damf_gpu** 
 int damf_gpu_load_rows(damf_gpu* h, int32_t which, int64_t row0, int64_t m, const float* src);
 
 /* Per-event device latency (microseconds) of the last apply with
- * DAMF_APPLY_TIME_EVENTS: fills min(max, count) values, returns count. */
+ * DAMF_APPLY_TIME_EVENTS (%globaltimer stamps at each event's start and end,
+ * read back here, not inside apply): fills min(max, count) values, returns
+ * count. */
 int64_t damf_gpu_event_latencies(damf_gpu* h, double* out_us_host, int64_t max);
 
 /* The base rows the last apply with DAMF_APPLY_LOG_ROWS modified, one
@@ -238,6 +247,11 @@ int64_t damf_gpu_row_log(damf_gpu* h, int64_t* out3_host, int64_t max);
  * DAMF_YB / DAMF_ZB / DAMF_RB returns the raw base-coordinate rows. */
 int damf_gpu_query_rows(damf_gpu* h, int32_t which, const int64_t* ids_host, int64_t m,
                         float* out_host);
+
+/* The base rows X_b (DAMF_XB) or Y_b (DAMF_YB) of m nodes exactly, fp64
+ * (out_host m x k): fp32 rows widened, side-table rows at their fp64 values. */
+int damf_gpu_query_rows64(damf_gpu* h, int32_t which, const int64_t* ids_host, int64_t m,
+                          double* out_host);
 
 /* Engine::score (engine.cpp:49-52). */
 int damf_gpu_score(damf_gpu* h, int64_t u, int64_t v, int32_t enhanced, double* out);

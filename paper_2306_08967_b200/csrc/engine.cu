@@ -23,7 +23,10 @@
 using namespace dgpu;
 
 namespace {
-constexpr long long kDirtyCap = 1 << 16;  // dirty rows tracked per side between folds
+// fp64 side-table rows per side between folds (rows written through P^-1;
+// a full table requests a rebase): 2 rows per side per edge event, so a
+// table outlasts the reference's 50,000-event rebase period
+constexpr long long kDirtyCap = 1 << 17;
 
 #define CK(expr)                                                                       \
   do {                                                                                 \
@@ -168,16 +171,70 @@ __global__ void identity_kernel(double* A, int k, int ld) {
 }
 
 // out[q][j] = sum_i base[ids[q]][i] * P[i][j] (P given as PT), fp64 accumulation.
+// rows with an fp64 side-table slot (slot != null, slot[r] >= 0) are read
+// from rows64 (ld doubles per slot)
 __global__ void query_rows_kernel(const float* base, int d, const double* PT, int ld, int k,
-                                  const int64_t* ids, int64_t m, float* out, double* out64) {
+                                  const int64_t* ids, int64_t m, float* out, double* out64,
+                                  const int32_t* slot, const double* rows64) {
   for (int64_t q = blockIdx.x; q < m; q += gridDim.x) {
     const int64_t r = ids[q];
+    const int sl = slot ? slot[r] : -1;
+    const double* r64 = sl >= 0 ? rows64 + (int64_t)sl * ld : nullptr;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
       double s = 0;
-      for (int i = 0; i < k; ++i) s += (double)base[r * d + i] * PT[(int64_t)j * ld + i];
+      for (int i = 0; i < k; ++i)
+        s += (r64 ? r64[i] : (double)base[r * d + i]) * PT[(int64_t)j * ld + i];
       if (out) out[q * k + j] = (float)s;
       if (out64) out64[q * k + j] = s;
     }
+  }
+}
+
+// out[row] = rows64[s] P for every side-table slot s (row = rows[s]), fp64
+// products, fp32 result; clear != 0 also releases the slot (a fold).
+__global__ void fold_rows64_kernel(const double* rows64, int ld, const int64_t* rows, long long ns,
+                                   const double* PT, int k, float* out, int ldo, int32_t* slot,
+                                   int clear) {
+  extern __shared__ double rv[];
+  for (long long s = blockIdx.x; s < ns; s += gridDim.x) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) rv[i] = rows64[s * ld + i];
+    __syncthreads();
+    const int64_t row = rows[s];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      double acc = 0;
+      for (int i = 0; i < k; ++i) acc += rv[i] * PT[(int64_t)j * ld + i];
+      out[row * ldo + j] = (float)acc;
+    }
+    if (clear && threadIdx.x == 0) slot[row] = -1;
+    __syncthreads();
+  }
+}
+
+// exact base rows (side table aware), fp64, k columns
+__global__ void base_rows64_kernel(const float* base, int d, const int32_t* slot, const double* rows64,
+                                   int ld, int k, const int64_t* ids, int64_t m, double* out) {
+  for (int64_t q = blockIdx.x; q < m; q += gridDim.x) {
+    const int64_t r = ids[q];
+    const int sl = slot[r];
+    for (int j = threadIdx.x; j < k; j += blockDim.x)
+      out[q * k + j] = sl >= 0 ? rows64[(int64_t)sl * ld + j] : (double)base[r * d + j];
+  }
+}
+
+__global__ void set_slots_kernel(int32_t* slot, const int64_t* rows, long long ns) {
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
+       s += (long long)gridDim.x * blockDim.x)
+    slot[rows[s]] = (int32_t)s;
+}
+
+// After damf_gpu_load_rows rewrote rows [r0, r0 + m) in fp32: refresh the
+// side-table copies of those rows.
+__global__ void refresh_rows64_kernel(double* rows64, int ld, const int64_t* rows, long long ns,
+                                      const float* base, int d, int64_t r0, int64_t m) {
+  for (long long s = blockIdx.x; s < ns; s += gridDim.x) {
+    const int64_t row = rows[s];
+    if (row < r0 || row >= r0 + m) continue;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) rows64[s * ld + j] = (double)base[row * d + j];
   }
 }
 
@@ -225,8 +282,11 @@ struct damf_gpu {
   long long* ptrace = nullptr;
   PprState* pst = nullptr;
   PprState* h_pst = nullptr;  // pinned mirror
-  int64_t* dirty[2] = {nullptr, nullptr};  // rows written through P^-1 (see rebase)
-  float* dirty_tmp = nullptr;              // gathered dirty rows (kDirtyCap x d)
+  // fp64 side table (see EventKernelArgs): dirty[side][s] = row of slot s,
+  // slot[side][row] = s or -1, rows64[side] = kDirtyCap x ld doubles
+  int64_t* dirty[2] = {nullptr, nullptr};
+  int32_t* slot[2] = {nullptr, nullptr};
+  double* rows64[2] = {nullptr, nullptr};
   unsigned long long* wq = nullptr;
   double* PT[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   double* Q[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -244,6 +304,8 @@ struct damf_gpu {
   unsigned long long *t_begin = nullptr, *t_end = nullptr;
   size_t t_cap = 0;
   std::vector<double> lat_us;
+  int64_t lat_pending = 0;            // events whose stamps are still on the device
+  cudaEvent_t span0 = nullptr, span1 = nullptr;
   int64_t* rowlog = nullptr;          // device (step, side, row) triples
   long long rowlog_cap = 0;
   std::vector<int64_t> rowlog_h;      // the last apply's log (DAMF_APPLY_LOG_ROWS)
@@ -258,6 +320,8 @@ struct damf_gpu {
 };
 
 namespace {
+
+int base_rows_f64(damf_gpu* h, int side, std::vector<double>* out);
 
 int cuda_fail(damf_gpu* h, cudaError_t e, const char* what, int line) {
   if (h) h->err = std::string("CUDA error ") + cudaGetErrorString(e) + " at engine.cu:" +
@@ -327,8 +391,11 @@ EventKernelArgs event_args(damf_gpu* h) {
   constexpr double kStorageSafeCond = 1e4;
   a.rebase_cond = h->cfg.rebase_cond;
   a.storage_cond = kStorageSafeCond;
-  a.dirty[0] = h->dirty[0];
-  a.dirty[1] = h->dirty[1];
+  for (int sd = 0; sd < 2; ++sd) {
+    a.dirty[sd] = h->dirty[sd];
+    a.slot[sd] = h->slot[sd];
+    a.rows64[sd] = h->rows64[sd];
+  }
   a.dirty_cap = kDirtyCap;
   a.out = h->out;
   a.in = h->in;
@@ -339,20 +406,6 @@ EventKernelArgs event_args(damf_gpu* h) {
   a.ws_Q1T = h->ws;
   a.ws_priv = h->ws + m;
   return a;
-}
-
-// rows[i] of `base` (k of ld floats) <-> packed tmp rows
-__global__ void gather_rows_kernel(const float* base, int ld, int k, const int64_t* rows,
-                                   int64_t m, float* tmp) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m * k;
-       x += (int64_t)gridDim.x * blockDim.x)
-    tmp[x] = base[rows[x / k] * ld + x % k];
-}
-__global__ void scatter_rows_kernel(float* base, int ld, int k, const int64_t* rows, int64_t m,
-                                    const float* tmp) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m * k;
-       x += (int64_t)gridDim.x * blockDim.x)
-    base[rows[x / k] * ld + x % k] = tmp[x];
 }
 
 bool is_device_ptr(const void* p) {
@@ -514,6 +567,8 @@ void damf_gpu_destroy(damf_gpu* h) {
   if (h->t_begin) cudaFree(h->t_begin);
   if (h->t_end) cudaFree(h->t_end);
   if (h->rowlog) cudaFree(h->rowlog);
+  if (h->span0) cudaEventDestroy(h->span0);
+  if (h->span1) cudaEventDestroy(h->span1);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -641,8 +696,12 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   const int64_t n = g->n, ncap = h->n_cap, d = h->d, ld = h->ld;
   // ---- factor state
   CK(dalloc(h, &h->ctl, 1));
-  for (int sd = 0; sd < 2; ++sd) CK(dalloc(h, &h->dirty[sd], (size_t)kDirtyCap));
-  CK(dalloc(h, &h->dirty_tmp, (size_t)kDirtyCap * cfg->d));
+  for (int sd = 0; sd < 2; ++sd) {
+    CK(dalloc(h, &h->dirty[sd], (size_t)kDirtyCap));
+    CK(dalloc(h, &h->rows64[sd], (size_t)kDirtyCap * ((h->d + 1 + 3) & ~3)));
+    CK(dalloc(h, &h->slot[sd], (size_t)ncap));
+    CK(cudaMemsetAsync(h->slot[sd], 0xff, (size_t)ncap * 4, h->st));
+  }
   CK(dalloc(h, &h->Xb, (size_t)ncap * d));
   CK(dalloc(h, &h->Yb, (size_t)ncap * d));
   CK(cudaMemsetAsync(h->Xb, 0, (size_t)ncap * d * 4, h->st));
@@ -943,27 +1002,27 @@ int damf_gpu_rebase(damf_gpu* h) {
   // rebase_cond = 1e8), where fp32 / 3xTF32 products lose the digits
   float* tmp = nullptr;
   if (k > 128) CK(cudaMalloc(&tmp, (size_t)h->n * d * 4));
-  // Two tiers: rows whose base value was written through P^-1 since the last
-  // fold (the dirty lists the event kernel keeps) carry components ~cond(P)
-  // larger than their current value and are folded in fp64 (DMMA); every
-  // other row is benign and takes the fast HBM-bound path. Without usable
-  // dirty lists (overflow, PPR state, k > 128) everything is folded in fp64.
+  // Two tiers: the rows written through P^-1 since the last fold live in the
+  // fp64 side table (their base values carry components ~cond(P) larger than
+  // their current value); they are folded from their fp64 values with fp64
+  // products and leave the table. Every other row is benign and takes the
+  // fast HBM-bound path. With an overflowed table (some such rows are fp32
+  // only), PPR state or k > 128 the bulk fold runs in fp64 as well.
   auto fold = [&](float* base, const double* PT, int side) -> int {
     const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
     if (nd >= 0 && nd <= kDirtyCap && k <= 128) {
-      const int g = (int)std::min<long long>(std::max<long long>(nd * k / 256, 1), 4096);
-      if (nd > 0) gather_rows_kernel<<<g, 256, 0, h->st>>>(base, d, k, h->dirty[side], nd, h->dirty_tmp);
       CK(launch_materialize(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
-      if (nd > 0) {
-        CK(launch_materialize_precise(h->dirty_tmp, nd, k, k, PT, ld, k, h->dirty_tmp, k, h->st, h->nsm));
-        scatter_rows_kernel<<<g, 256, 0, h->st>>>(base, d, k, h->dirty[side], nd, h->dirty_tmp);
-      }
-      CK(cudaGetLastError());
     } else if (!tmp) {
       CK(launch_materialize_precise(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
     } else {
       CK(launch_materialize_precise(base, h->n, k, d, PT, ld, k, tmp, d, h->st, h->nsm));
       CK(cudaMemcpyAsync(base, tmp, (size_t)h->n * d * 4, cudaMemcpyDeviceToDevice, h->st));
+    }
+    const long long ns = side >= 0 ? std::min<long long>(h->h_ctl->dirty_n[side], kDirtyCap) : 0;
+    if (ns > 0) {
+      fold_rows64_kernel<<<(int)std::min<long long>(ns, 8 * h->nsm), 128, (size_t)k * 8, h->st>>>(
+          h->rows64[side], ld, h->dirty[side], ns, PT, k, base, d, h->slot[side], 1);
+      CK(cudaGetLastError());
     }
     return 0;
   };
@@ -981,6 +1040,7 @@ int damf_gpu_rebase(damf_gpu* h) {
   }
   CK(cudaGetLastError());
   if (!h->alpha1) CK(launch_ppr_keys(ppr_args(h), h->nsm, h->st));
+  h->launches += (h->alpha1 ? 2 : 5) + 2 + 4;  // folds, side-table folds, P = Q = I
   h->h_ctl->cond_est = 1.0;
   h->h_ctl->need_rebase = 0;
   CK(cudaMemcpyAsync(&h->ctl->cond_est, &h->h_ctl->cond_est, sizeof(double), cudaMemcpyHostToDevice, h->st));
@@ -1210,6 +1270,15 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     CK(cudaMemcpyAsync(&h->ctl->rowlog_n, &h->h_ctl->rowlog_n, sizeof(long long),
                        cudaMemcpyHostToDevice, h->st));
   }
+  if (timing) {
+    // device span of the call: from the first launch (descriptors already
+    // uploaded) to the completion of its last kernel, rebases included
+    if (!h->span0) {
+      CK(cudaEventCreate(&h->span0));
+      CK(cudaEventCreate(&h->span1));
+    }
+    CK(cudaEventRecord(h->span0, h->st));
+  }
   const long long rank1_0 = h->h_ctl->rank1, folds0 = h->h_ctl->folds;
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
   EventKernelArgs ea = event_args(h);
@@ -1356,14 +1425,14 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     h->rowlog_h.clear();
   }
   if (timing) {
-    const int64_t m = s.applied;
-    std::vector<unsigned long long> tb(m), te(m);
-    if (m) {
-      CK(cudaMemcpy(tb.data(), h->t_begin, m * 8, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(te.data(), h->t_end, m * 8, cudaMemcpyDeviceToHost));
-    }
-    h->lat_us.resize(m);
-    for (int64_t e = 0; e < m; ++e) h->lat_us[e] = (double)(te[e] - tb[e]) * 1e-3;
+    // per-event stamps stay on the device until damf_gpu_event_latencies
+    h->lat_pending = s.applied;
+    h->lat_us.clear();
+    CK(cudaEventRecord(h->span1, h->st));
+    CK(cudaEventSynchronize(h->span1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->span0, h->span1));
+    s.device_ms = ms;
   }
   if (!h->alpha1) {
     if (!(mode & DAMF_APPLY_DEFER_PUSH)) {
@@ -1396,6 +1465,18 @@ int64_t damf_gpu_row_log(damf_gpu* h, int64_t* out, int64_t max) {
 }
 
 int64_t damf_gpu_event_latencies(damf_gpu* h, double* out, int64_t max) {
+  if (h->lat_pending > 0) {
+    const int64_t m = h->lat_pending;
+    std::vector<unsigned long long> tb(m), te(m);
+    if (cudaMemcpy(tb.data(), h->t_begin, m * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(te.data(), h->t_end, m * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cuda_fail(h, cudaGetLastError(), "event latency read-back", __LINE__);
+      return -1;
+    }
+    h->lat_us.resize(m);
+    for (int64_t e = 0; e < m; ++e) h->lat_us[e] = (double)(te[e] - tb[e]) * 1e-3;
+    h->lat_pending = 0;
+  }
   const int64_t m = (int64_t)h->lat_us.size();
   for (int64_t i = 0; i < std::min(m, max); ++i) out[i] = h->lat_us[i];
   return m;
@@ -1415,6 +1496,14 @@ int damf_gpu_load_rows(damf_gpu* h, int32_t which, int64_t row0, int64_t m, cons
   if (is_device_ptr(src)) CK(cudaDeviceSynchronize());
   CK(cudaMemcpy2DAsync(dst, (size_t)h->d * 4, src, (size_t)h->k * 4, (size_t)h->k * 4, m,
                        cudaMemcpyDefault, h->st));
+  if (int r = sync_ctl(h)) return r;
+  const int side = which == DAMF_XB ? 0 : 1;
+  const long long ns = std::min<long long>(h->h_ctl->dirty_n[side], kDirtyCap);
+  if (ns > 0) {
+    refresh_rows64_kernel<<<(int)std::min<long long>(ns, 8 * h->nsm), 128, 0, h->st>>>(
+        h->rows64[side], h->ld, h->dirty[side], ns, which == DAMF_XB ? h->Xb : h->Yb, h->d, row0, m);
+    CK(cudaGetLastError());
+  }
   CK(cudaStreamSynchronize(h->st));
   if (h->alpha1 && which == DAMF_XB) return 0;  // Z_b aliases X_b
   return 0;
@@ -1441,10 +1530,35 @@ int damf_gpu_query_rows(damf_gpu* h, int32_t which, const int64_t* ids, int64_t 
   CK(cudaMalloc(&dids, std::max<int64_t>(m, 1) * 8));
   CK(cudaMalloc(&dout, std::max<int64_t>(m, 1) * h->k * 4));
   CK(cudaMemcpyAsync(dids, ids, m * 8, cudaMemcpyHostToDevice, h->st));
+  const int qs = which == DAMF_Y ? 1 : which == DAMF_X || (which == DAMF_Z && h->alpha1) ? 0 : -1;
   query_rows_kernel<<<(int)std::min<int64_t>(std::max<int64_t>(m, 1), 4096), 128, 0, h->st>>>(
-      base, h->d, PT, h->ld, h->k, dids, m, dout, nullptr);
+      base, h->d, PT, h->ld, h->k, dids, m, dout, nullptr, qs >= 0 ? h->slot[qs] : nullptr,
+      qs >= 0 ? h->rows64[qs] : nullptr);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, dout, m * h->k * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(dids);
+  cudaFree(dout);
+  return 0;
+}
+
+int damf_gpu_query_rows64(damf_gpu* h, int32_t which, const int64_t* ids, int64_t m, double* out) {
+  if (int r = sync_ctl(h)) return r;
+  if (which != DAMF_XB && which != DAMF_YB)
+    return fail(h, DAMF_E_SHAPE_MISMATCH, "query_rows64: which must be DAMF_XB or DAMF_YB");
+  for (int64_t q = 0; q < m; ++q)
+    if (ids[q] < 0 || ids[q] >= h->n) return fail(h, DAMF_E_UNKNOWN_NODE, "query: unknown node " + std::to_string(ids[q]));
+  if (m == 0) return 0;
+  const int side = which == DAMF_XB ? 0 : 1;
+  int64_t* dids = nullptr;
+  double* dout = nullptr;
+  CK(cudaMalloc(&dids, m * 8));
+  CK(cudaMalloc(&dout, m * h->k * 8));
+  CK(cudaMemcpyAsync(dids, ids, m * 8, cudaMemcpyHostToDevice, h->st));
+  base_rows64_kernel<<<(int)std::min<int64_t>(m, 4096), 128, 0, h->st>>>(
+      side ? h->Yb : h->Xb, h->d, h->slot[side], h->rows64[side], h->ld, h->k, dids, m, dout);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, dout, m * h->k * 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   cudaFree(dids);
   cudaFree(dout);
@@ -1520,10 +1634,12 @@ int damf_gpu_score(damf_gpu* h, int64_t u, int64_t v, int32_t enhanced, double* 
   CK(cudaMalloc(&dids, 16));
   CK(cudaMalloc(&dout, 2 * h->k * 8));
   CK(cudaMemcpyAsync(dids, ids, 16, cudaMemcpyHostToDevice, h->st));
+  const bool zs = enhanced && !h->alpha1;  // Z_b rows have no side table
   query_rows_kernel<<<1, 128, 0, h->st>>>(enhanced ? h->Zb : h->Xb, h->d, live_PT(h, 0), h->ld, h->k,
-                                          dids, 1, nullptr, dout);
+                                          dids, 1, nullptr, dout, zs ? nullptr : h->slot[0],
+                                          zs ? nullptr : h->rows64[0]);
   query_rows_kernel<<<1, 128, 0, h->st>>>(h->Yb, h->d, live_PT(h, 1), h->ld, h->k, dids + 1, 1,
-                                          nullptr, dout + h->k);
+                                          nullptr, dout + h->k, h->slot[1], h->rows64[1]);
   CK(cudaGetLastError());
   std::vector<double> hv(2 * h->k);
   CK(cudaMemcpyAsync(hv.data(), dout, 2 * h->k * 8, cudaMemcpyDeviceToHost, h->st));
@@ -1552,20 +1668,17 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
   constexpr double kPreciseCond = 100.0;
   const int side = which == DAMF_Y ? 1 : (which == DAMF_Z && !h->alpha1) ? -1 : 0;
   const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
-  if (h->h_ctl->cond_est <= kPreciseCond) {
+  if (h->h_ctl->cond_est <= kPreciseCond || (nd >= 0 && nd <= kDirtyCap && h->k <= 128)) {
     CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
-  } else if (nd >= 0 && nd <= kDirtyCap && h->k <= 128) {  // in-place fp64 rows: k <= 128
-    const int k = h->k;
-    CK(launch_materialize(base, h->n, k, h->d, PT, h->ld, k, out, k, h->st, h->nsm));
-    if (nd > 0) {
-      const int g = (int)std::min<long long>(std::max<long long>(nd * k / 256, 1), 4096);
-      gather_rows_kernel<<<g, 256, 0, h->st>>>(base, h->d, k, h->dirty[side], nd, h->dirty_tmp);
-      CK(launch_materialize_precise(h->dirty_tmp, nd, k, k, PT, h->ld, k, h->dirty_tmp, k, h->st, h->nsm));
-      scatter_rows_kernel<<<g, 256, 0, h->st>>>(out, k, k, h->dirty[side], nd, h->dirty_tmp);
-      CK(cudaGetLastError());
-    }
   } else {
     CK(launch_materialize_precise(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
+  }
+  // side-table rows from their fp64 base values with fp64 products
+  const long long ns = side >= 0 ? std::min<long long>(nd, kDirtyCap) : 0;
+  if (ns > 0) {
+    fold_rows64_kernel<<<(int)std::min<long long>(ns, 8 * h->nsm), 128, (size_t)h->k * 8, h->st>>>(
+        h->rows64[side], h->ld, h->dirty[side], ns, PT, h->k, out, h->k, nullptr, 0);
+    CK(cudaGetLastError());
   }
   if (!dst_is_device) {
     CK(cudaMemcpyAsync(dst, out, (size_t)h->n * h->k * 4, cudaMemcpyDeviceToHost, h->st));
@@ -1606,6 +1719,13 @@ int damf_gpu_get_state(damf_gpu* h, int32_t which, void* out) {
     case DAMF_SIGMA:
       CK(cudaMemcpy(out, h->sigma, k * 8, cudaMemcpyDeviceToHost));
       return 0;
+    case DAMF_XB64:
+    case DAMF_YB64: {
+      std::vector<double> r64;
+      if (int r = base_rows_f64(h, which == DAMF_XB64 ? 0 : 1, &r64)) return r;
+      std::memcpy(out, r64.data(), r64.size() * 8);
+      return 0;
+    }
     case DAMF_X:
     case DAMF_Y:
     case DAMF_Z:
@@ -1638,6 +1758,59 @@ int damf_gpu_get_graph(damf_gpu* h, int64_t* offsets, int32_t* targets, double* 
   if (offsets) offsets[n] = pos;
   return 0;
 }
+
+}  // extern "C"
+namespace {
+// X_b (side 0) / Y_b (side 1) as fp64 row-major n x k: the fp32 rows widened,
+// with the side-table rows' fp64 values in place.
+int base_rows_f64(damf_gpu* h, int side, std::vector<double>* out) {
+  const int64_t n = h->n, k = h->k;
+  std::vector<float> rows((size_t)n * k);
+  if (int r = damf_gpu_get_state(h, side == 0 ? DAMF_XB : DAMF_YB, rows.data())) return r;
+  out->assign(rows.begin(), rows.end());
+  const long long ns = std::min<long long>(h->h_ctl->dirty_n[side], kDirtyCap);
+  if (ns > 0) {
+    std::vector<int64_t> ids((size_t)ns);
+    std::vector<double> r64((size_t)ns * h->ld);
+    CK(cudaMemcpy(ids.data(), h->dirty[side], ns * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r64.data(), h->rows64[side], ns * h->ld * 8, cudaMemcpyDeviceToHost));
+    for (long long q = 0; q < ns; ++q)
+      for (int64_t j = 0; j < k; ++j) (*out)[(size_t)ids[q] * k + j] = r64[(size_t)q * h->ld + j];
+  }
+  return 0;
+}
+
+// Rows of an fp64 file (n x k row-major) that fp32 cannot hold exactly go to
+// the side table, so a saved engine resumes bit-identically; when they do
+// not fit, every row stays fp32 (rounded).
+int seed_rows64(damf_gpu* h, int side, const std::vector<double>& rm) {
+  const int64_t n = h->n, k = h->k;
+  std::vector<int64_t> ids;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < k; ++j) {
+      const double v = rm[(size_t)i * k + j];
+      if ((double)(float)v != v) {
+        ids.push_back(i);
+        break;
+      }
+    }
+  if (ids.empty() || (long long)ids.size() > kDirtyCap) return 0;
+  std::vector<double> r64(ids.size() * (size_t)h->ld, 0.0);
+  for (size_t q = 0; q < ids.size(); ++q)
+    for (int64_t j = 0; j < k; ++j) r64[q * h->ld + j] = rm[(size_t)ids[q] * k + j];
+  CK(cudaMemcpy(h->dirty[side], ids.data(), ids.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->rows64[side], r64.data(), r64.size() * 8, cudaMemcpyHostToDevice));
+  set_slots_kernel<<<(int)std::min<size_t>(ids.size(), 4096), 128>>>(h->slot[side], h->dirty[side],
+                                                                      (long long)ids.size());
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  h->h_ctl->dirty_n[side] = (long long)ids.size();
+  CK(cudaMemcpy(&h->ctl->dirty_n[side], &h->h_ctl->dirty_n[side], 8, cudaMemcpyHostToDevice));
+  h->ctl_fresh = false;
+  return 0;
+}
+}  // namespace
+extern "C" {
 
 // ---- state persistence: the reference's DAMF v1 binary (io.cpp:182-264) --
 // magic "DAMF", u32 version 1, RunConfig, u64 events_applied, i64
@@ -1700,8 +1873,12 @@ int damf_gpu_save_state(damf_gpu* h, const char* path) {
   std::fwrite(sig.data(), 8, (size_t)k, f);
   std::vector<float> rows((size_t)n * k);
   for (int which : {DAMF_XB, DAMF_YB}) {
-    if (int r = damf_gpu_get_state(h, which, rows.data())) { std::fclose(f); return r; }
-    put_rows(f, rows, n, k);
+    // the base rows exactly: fp32 rows widened, side-table rows in fp64
+    std::vector<double> r64;
+    if (int r = base_rows_f64(h, which == DAMF_XB ? 0 : 1, &r64)) { std::fclose(f); return r; }
+    putv<int64_t>(f, n);
+    putv<int64_t>(f, k);
+    std::fwrite(r64.data(), 8, r64.size(), f);
   }
   std::vector<double> P((size_t)k * k);
   for (int which : {DAMF_PX, DAMF_PY}) {
@@ -1815,8 +1992,11 @@ int damf_gpu_load_state(const char* path, const damf_config* sizing, damf_gpu** 
   const std::vector<double>& pyr = py;
   damf_csr g{n, (int64_t)tgt.size(), off.data(), tgt.data(), weighted ? wts.data() : nullptr};
   const std::vector<float> z32 = rows32(zb), r32 = rows32(rb);
-  return damf_gpu_resume(&g, &cfg, k, x32.data(), y32.data(), pxr.data(), pyr.data(), sig.data(),
-                         z32.data(), r32.data(), applied, since, out);
+  const int st = damf_gpu_resume(&g, &cfg, k, x32.data(), y32.data(), pxr.data(), pyr.data(),
+                                 sig.data(), z32.data(), r32.data(), applied, since, out);
+  if (st) return st;
+  if (int r = seed_rows64(*out, 0, xb)) return r;
+  return seed_rows64(*out, 1, yb);
 }
 
 // Engine(g, fs, es, cfg, events_applied, events_since_rebase) (engine.hpp:32-34):

@@ -1001,6 +1001,54 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
     }                                                                     \
   } while (0)
 
+// ---- base rows: fp32 storage plus the fp64 side table ----------------------
+// Rows written through P^-1 carry components ~cond(P) larger than their
+// current value, which fp32 storage would round away; they live in fp64
+// (rows64) from their first such write until the next fold, with the fp32
+// row kept as a rounded mirror for readers that tolerate it (PPR keys).
+DAMF_D double row_val(const EventKernelArgs& A, int side, const float* base, int64_t row, int j) {
+  const int sl = A.slot[side][row];
+  return sl >= 0 ? A.rows64[side][(int64_t)sl * A.ld + j] : (double)base[row * (int64_t)A.d + j];
+}
+DAMF_D void row_add(const EventKernelArgs& A, int side, float* base, int64_t row, int j, double delta) {
+  const int sl = A.slot[side][row];
+  if (sl >= 0) {
+    double* p = A.rows64[side] + (int64_t)sl * A.ld + j;
+    const double v = *p + delta;
+    *p = v;
+    base[row * (int64_t)A.d + j] = (float)v;
+  } else {
+    float* r = base + row * (int64_t)A.d + j;
+    *r = (float)((double)*r + delta);
+  }
+}
+DAMF_D void row_set(const EventKernelArgs& A, int side, float* base, int64_t row, int j, double v) {
+  const int sl = A.slot[side][row];
+  if (sl >= 0) A.rows64[side][(int64_t)sl * A.ld + j] = v;
+  base[row * (int64_t)A.d + j] = (float)v;
+}
+// One warp gives `row` an fp64 slot (initialised from its fp32 value) unless
+// it has one; a full table leaves the row in fp32 and requests a rebase.
+DAMF_D void row_claim(const EventKernelArgs& A, int side, const float* base, int64_t row) {
+  const int lane = threadIdx.x & 31;
+  int sl = A.slot[side][row];
+  if (sl < 0) {
+    long long at = 0;
+    if (lane == 0) at = atomicAdd(reinterpret_cast<unsigned long long*>(&A.ctl->dirty_n[side]), 1ull);
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (at >= A.dirty_cap) {
+      if (lane == 0) A.ctl->need_rebase = 1;
+      return;
+    }
+    for (int j = lane; j < A.d; j += 32)
+      A.rows64[side][at * A.ld + j] = (double)base[row * (int64_t)A.d + j];
+    if (lane == 0) {
+      A.dirty[side][at] = row;
+      A.slot[side][row] = (int)at;
+    }
+  }
+}
+
 // Returns false (nothing written) when the bordered system is not finite:
 // the reference throws NonFinite from dense_svd_small (svd.cpp:31-32).
 template <int C>
@@ -1042,9 +1090,9 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   for (int j = tid; j < k; j += NT) {
     double s = 0;
     for (int t = 0; t < st.nb; ++t)
-      s += A.sp_vals[st.b_off + t] * (double)baseA[A.sp_rows[st.b_off + t] * (int64_t)d + j];
+      s += A.sp_vals[st.b_off + t] * row_val(A, sA, baseA, A.sp_rows[st.b_off + t], j);
     S.gA[j] = s;
-    S.gB[j] = edge ? st.c_val * (double)baseB[st.c_row * (int64_t)d + j] : 0.0;
+    S.gB[j] = edge ? st.c_val * row_val(A, sB, baseB, st.c_row, j) : 0.0;
     S.sig[j] = A.sigma[j];
   }
   __syncthreads();
@@ -1066,6 +1114,17 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     }
   }
   cl.sync();  // B1
+  // fp64 slots for the rows this step writes (after every CTA's gather; the
+  // writes come after B7b): row q of the step is claimed by warp 0 of CTA q % C
+  if (warp == 0) {
+    for (int q = rank; q <= st.nb; q += C) {
+      if (q < st.nb) {
+        if (A.sp_vals[st.b_off + q] != 0.0) row_claim(A, sA, baseA, A.sp_rows[st.b_off + q]);
+      } else {
+        row_claim(A, sB, baseB, st.c_row);
+      }
+    }
+  }
   PROF_MARK(0);
   // ---- 2. bordered system (redundant per CTA) -----------------------------
   double wa2 = 0, wb2 = 0;
@@ -1105,10 +1164,19 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     lm = -2.0 / (beta + sq);
   }
   const double np_ = 1.0 / sqrt(lp * lp + 1.0), nm_ = 1.0 / sqrt(lm * lm + 1.0);
+  // Entries of the border below 8 eps |M| are set to zero: the same backward
+  // perturbation the secular deflation applies to z, made consistent for the
+  // closed forms (H = M^T E S^-1, ex, ey). A direction the update does not
+  // touch then keeps an exactly zero coupling, and ex / ey come out exactly
+  // zero when the reference's SVD leaves them so (the empty dX / dY of
+  // types.hpp:101-116, e.g. a node whose base row is numerically zero).
+  const double tolM = 8.0 * EPS * fmax(S.sig[0], fmax(bnorm, fabs(st.c_val)));
   for (int i = tid; i < n; i += NT) {
     const double Di = i < k ? S.sig[i] : 0.0;
-    const double ai = i < k ? S.wA[i] : rA;
-    const double bi = i < k ? S.wB[i] : rB;
+    double ai = i < k ? S.wA[i] : rA;
+    double bi = i < k ? S.wB[i] : rB;
+    if (i < k && fabs(ai) <= tolM) ai = 0.0;
+    if (i < k && fabs(bi) <= tolM) bi = 0.0;
     S.Dg[i] = Di;
     S.av[i] = ai;
     S.bv[i] = edge ? bi : (i == k ? 1.0 : 0.0);
@@ -1347,16 +1415,12 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
         ya = warp_sum(ya);
         yb = warp_sum(yb);
         if (lane == 0) {
-          for (int q = 0; q < st.nb; ++q) {
-            float* r = baseA + A.sp_rows[st.b_off + q] * (int64_t)d + j;
-            *r = (float)((double)*r + A.sp_vals[st.b_off + q] * ya);
-          }
-          if (edge) {
-            float* r = baseB + st.c_row * (int64_t)d + j;
-            *r = (float)((double)*r + st.c_val * yb);
-          } else {
-            baseB[st.c_row * (int64_t)d + j] = (float)yb;  // appended row
-          }
+          for (int q = 0; q < st.nb; ++q)
+            row_add(A, sA, baseA, A.sp_rows[st.b_off + q], j, A.sp_vals[st.b_off + q] * ya);
+          if (edge)
+            row_add(A, sB, baseB, st.c_row, j, st.c_val * yb);
+          else
+            row_set(A, sB, baseB, st.c_row, j, yb);  // appended row
         }
       }
     }
@@ -1413,16 +1477,12 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
         ya = warp_sum(ya);
         yb = warp_sum(yb);
         if (lane == 0) {
-          for (int q = 0; q < st.nb; ++q) {
-            float* r = baseA + A.sp_rows[st.b_off + q] * (int64_t)d + j;
-            *r = (float)((double)*r + A.sp_vals[st.b_off + q] * ya);
-          }
-          if (edge) {
-            float* r = baseB + st.c_row * (int64_t)d + j;
-            *r = (float)((double)*r + st.c_val * yb);
-          } else {
-            baseB[st.c_row * (int64_t)d + j] = (float)yb;  // appended row
-          }
+          for (int q = 0; q < st.nb; ++q)
+            row_add(A, sA, baseA, A.sp_rows[st.b_off + q], j, A.sp_vals[st.b_off + q] * ya);
+          if (edge)
+            row_add(A, sB, baseB, st.c_row, j, st.c_val * yb);
+          else
+            row_set(A, sB, baseB, st.c_row, j, yb);  // appended row
         }
       }
     }
@@ -1445,25 +1505,27 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
         p2 += S.pnorm[r][xA ? 0 : 2];
         q2 += S.pnorm[r][xA ? 1 : 3];
       }
-      A.ctl->cond_est = sqrt(p2) * sqrt(q2);
-      if (A.ctl->cond_est > A.rebase_cond) A.ctl->need_rebase = 1;
-      // fp32 base rows: both projections must stay well conditioned (the
-      // reference watches P_X only, engine.cpp:38-40, with fp64 rows)
+      // cond_2(P) from |P|_F |P^-1|_F (the GEMM epilogues' norms): the bound
+      // B satisfies cond_2 <= B <= k cond_2, and B / sqrt(k) is the estimate
+      // compared with rebase_cond (the reference runs 10 + 10 power
+      // iterations with an LU every event, factor_state.cpp:224-249)
+      const double bx = sqrt(p2) * sqrt(q2);
       double p2o = 0, q2o = 0;
       for (int r = 0; r < C; ++r) {
         p2o += S.pnorm[r][xA ? 2 : 0];
         q2o += S.pnorm[r][xA ? 3 : 1];
       }
-      if (fmax(A.ctl->cond_est, sqrt(p2o) * sqrt(q2o)) > A.storage_cond) A.ctl->need_rebase = 1;
+      const double by = sqrt(p2o) * sqrt(q2o);
+      const double rk = sqrt((double)k);
+      A.ctl->cond_est = bx / rk;
+      // P_X as engine.cpp:38-40; P_Y as well (its rows are fp64-slotted the
+      // same way and P_Y^-1 is maintained by products too)
+      if (fmax(bx, by) / rk > A.rebase_cond) A.ctl->need_rebase = 1;
+      // the enhancer's Z_b / r_b are fp32 base-coordinate rows with no fp64
+      // side table: with alpha < 1 both projections stay below the fp32
+      // storage bound
+      if (!A.alpha_is_one && fmax(bx, by) > A.storage_cond) A.ctl->need_rebase = 1;
       if (exact) A.ctl->need_rebase = 1;
-      // rows whose base value was written through P^-1: the next fold
-      // recomputes them in fp64 (their base components carry cond(P))
-      auto mark = [&](int side, int64_t row) {
-        const long long at = A.ctl->dirty_n[side]++;
-        if (at < A.dirty_cap) A.dirty[side][at] = row;
-      };
-      for (int q = 0; q < st.nb; ++q) mark(sA, A.sp_rows[st.b_off + q]);
-      mark(sB, st.c_row);
     }
   } else {
     // ---- eager fold (rank change or ill-conditioned step) ------------------
@@ -1490,8 +1552,10 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
         rows = A.ctl->rows_x;
       }
       double* rowv = S.vscr[warp];
+      const int side = mat == 0 ? sA : mat == 1 ? sB : -1;
       for (long long r = (long long)rank * NW + warp; r < rows; r += (long long)C * NW) {
-        for (int i = lane; i < k; i += 32) rowv[i] = base[r * d + i];
+        for (int i = lane; i < k; i += 32)
+          rowv[i] = side >= 0 ? row_val(A, side, base, r, i) : (double)base[r * d + i];
         __syncwarp();
         for (int t = lane; t < k2; t += 32) {
           double s = 0;
@@ -1501,6 +1565,13 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
         for (int t = k2 + lane; t < k; t += 32) base[r * d + t] = 0.0f;
         __syncwarp();
       }
+    }
+    cl.sync();
+    // folded rows are current coordinates now (P = I): back to fp32 storage
+    for (int side = 0; side < 2; ++side) {
+      const long long ns = min(A.ctl->dirty_n[side], A.dirty_cap);
+      for (long long q = (long long)rank * NT + tid; q < ns; q += (long long)C * NT)
+        A.slot[side][A.dirty[side][q]] = -1;
     }
     cl.sync();
     // residual keys of the folded r_b rows (enhancer.cpp:196-206 re-keying)
@@ -1517,16 +1588,12 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     int jlo, jhi;
     block_range(k2, C, rank, jlo, jhi);
     for (int j = jlo + tid; j < jhi; j += NT) {
-      for (int q = 0; q < st.nb; ++q) {
-        float* r = baseA + A.sp_rows[st.b_off + q] * (int64_t)d + j;
-        *r = (float)((double)*r + A.sp_vals[st.b_off + q] * S.exv[j]);
-      }
-      if (edge) {
-        float* r = baseB + st.c_row * (int64_t)d + j;
-        *r = (float)((double)*r + st.c_val * S.eyv[j]);
-      } else {
-        baseB[st.c_row * (int64_t)d + j] = (float)S.eyv[j];
-      }
+      for (int q = 0; q < st.nb; ++q)
+        row_add(A, sA, baseA, A.sp_rows[st.b_off + q], j, A.sp_vals[st.b_off + q] * S.exv[j]);
+      if (edge)
+        row_add(A, sB, baseB, st.c_row, j, st.c_val * S.eyv[j]);
+      else
+        row_set(A, sB, baseB, st.c_row, j, S.eyv[j]);
     }
     // P = Q = I (k2 x k2) in the new buffers
     for (int x = rank * NT + tid; x < k2 * k2; x += C * NT) {
@@ -1550,7 +1617,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       A.ctl->rank1 += 1;
       A.ctl->folds += 1;
       A.ctl->cond_est = 1.0;
-      A.ctl->dirty_n[0] = A.ctl->dirty_n[1] = 0;  // folded in fp64, P = I
+      A.ctl->dirty_n[0] = A.ctl->dirty_n[1] = 0;  // folded (fp64 slots read), P = I
     }
   }
   // appended rows (node steps)

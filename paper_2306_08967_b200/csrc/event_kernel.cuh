@@ -46,8 +46,14 @@ struct EventKernelArgs {
   double* sigma;
   double rebase_cond;
   double storage_cond;
-  int64_t* dirty[2];    // row ids of X_b / Y_b written through P^-1 (capacity dirty_cap)
-  long long dirty_cap;  // rebase when either projection's |P|_F |P^-1|_F exceeds this
+  // fp64 side table of the base rows written through P^-1 (the reference's
+  // base rows are fp64; here they are fp32 except these): slot[side][row] =
+  // index into rows64[side] (ld doubles per row) or -1; dirty[side][slot] =
+  // its row; ctl->dirty_n[side] slots in use out of dirty_cap
+  int64_t* dirty[2];
+  long long dirty_cap;
+  int32_t* slot[2];
+  double* rows64[2];
   // graph
   DevCSR out, in;
   int directed, undirected;

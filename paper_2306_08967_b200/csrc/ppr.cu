@@ -7,16 +7,22 @@
 // threshold alpha*eps/s_max at every call.
 //
 // The push is frontier-synchronous (Jacobi rounds) instead of FIFO
-// Gauss-Seidel, in PULL form so no floating-point atomics are needed:
-//   F  = {u : key[u] * s_max > alpha*eps}                  (compaction)
-//   P1 u in F : delta[u] = r[u]; Z[u] += r[u]; stamp[u] = R; mark in-nbrs
-//   P2 L = {v : mark[v] == R}                               (compaction)
-//   P3 v in L : r[v] = [v not in F] r[v]
-//                      + (1-alpha)/max(deg v,1) sum_{u in out(v) cap F} w delta[u]
-//   next F = {v in L : key[v] over threshold}               (compaction)
-// One cooperative kernel runs all rounds with grid-wide barriers. All
-// compactions are block-count / prefix / scatter (atomics-free, order
-// preserving, deterministic).
+// Gauss-Seidel. Each round chooses its direction from the frontier's
+// in-arc count:
+//   pull (dense rounds):    every affected row v gathers
+//       r[v] += (1-alpha)/max(deg v,1) sum_{u in out(v), stamp[u] == R} w delta[u]
+//     with plain stores; only chunked heavy rows combine their partial sums
+//     with vector float reductions (red.global.add.v4.f32).
+//   scatter (sparse rounds): r[v] += (1-alpha) w / deg(v) * delta[u] for
+//     v in in(u) with float reductions, and the first toucher of v (atomicExch
+//     on mark[v]) appends v to the next candidate list.
+// Work is handed out through per-warp static batches plus 32 atomic queue
+// heads. Floating-point reductions make the fp32 summation order, and with it
+// the last bits of r / Z and the push count, vary from run to run; the
+// reference's contract -- every row's defect under alpha*eps*max(deg,1)
+// after the push (enhancer.cpp:125-155, eval.cpp:591-610) -- holds for every
+// order, and tests/test_gpu_ppr_materialize.py checks it (plus the distance
+// to the exact fixed point) rather than bitwise equality with the FIFO push.
 #include <cooperative_groups.h>
 
 #include <algorithm>

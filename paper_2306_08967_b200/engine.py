@@ -26,7 +26,7 @@ ERROR_KINDS = ["ParseError", "UnknownNode", "DuplicateEdge", "MissingEdge", "Sha
                "ZeroMatrix", "NonFinite", "SingularProjection", "NonConvergence",
                "DegenerateLabels", "KTooLarge", "GraphTooSmall", "TooLarge", "IoError"]
 ADD_NODE, ADD_EDGE, REMOVE_EDGE = 0, 1, 2
-XB, YB, PX, PY, SIGMA, ZB, RB, X, Y, Z, QX, QY = range(12)
+XB, YB, PX, PY, SIGMA, ZB, RB, X, Y, Z, QX, QY, XB64, YB64 = range(14)
 APPLY_GRAPH_AND_PPR_ONLY, APPLY_DEFER_PUSH, APPLY_TIME_EVENTS, APPLY_LOG_ROWS = 1, 2, 4, 8
 
 
@@ -63,7 +63,7 @@ class EventBatch(C.Structure):
 class ApplyStats(C.Structure):
     _fields_ = [("applied", C.c_int64), ("failed_index", C.c_int64),
                 ("rank1_updates", C.c_int64), ("rebases", C.c_int64), ("eager_folds", C.c_int64),
-                ("push_rounds", C.c_int64), ("pushes", C.c_int64)]
+                ("push_rounds", C.c_int64), ("pushes", C.c_int64), ("device_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -103,6 +103,7 @@ def lib():
         L.damf_gpu_row_log.argtypes = [vp, i64p, C.c_int64]
         L.damf_gpu_row_log.restype = C.c_int64
         L.damf_gpu_query_rows.argtypes = [vp, C.c_int32, i64p, C.c_int64, f32p]
+        L.damf_gpu_query_rows64.argtypes = [vp, C.c_int32, i64p, C.c_int64, f64p]
         L.damf_gpu_load_rows.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, vp]
         L.damf_gpu_score_pairs.argtypes = [vp, i64p, i64p, C.c_int64, C.c_int32, f64p]
         L.damf_gpu_save_state.argtypes = [vp, C.c_char_p]
@@ -292,6 +293,8 @@ class Engine:
         n, k = dg["n"], dg["k"]
         if which in (XB, YB, ZB, RB, X, Y, Z):
             out = np.zeros((n, k), np.float32)
+        elif which in (XB64, YB64):
+            out = np.zeros((n, k), np.float64)
         elif which in (PX, PY, QX, QY):
             out = np.zeros((k, k), np.float64)
         else:
@@ -338,6 +341,13 @@ class Engine:
         ids = np.ascontiguousarray(ids, np.int64)
         out = np.zeros((len(ids), self.k), np.float32)
         self._check(lib().damf_gpu_query_rows(self.h, which, _p(ids, i64p), len(ids), _p(out, f32p)))
+        return out
+
+    def query64(self, which, ids):
+        """Exact base rows (XB or YB) in fp64, side-table aware."""
+        ids = np.ascontiguousarray(ids, np.int64)
+        out = np.zeros((len(ids), self.k), np.float64)
+        self._check(lib().damf_gpu_query_rows64(self.h, which, _p(ids, i64p), len(ids), _p(out, f64p)))
         return out
 
     def context(self, u):

@@ -359,3 +359,45 @@ def degree_proportional_inserts(keys, tgt, m, seed):
             if len(out_u) == m:
                 break
     return np.array(out_u, np.int64), np.array(out_v, np.int64)
+
+
+def orthonormal_rows_subset(n, d, sigma, seed, ids, chunk=1 << 22):
+    """The rows `ids` of what orthonormal_rows_into loads (same seeded chunks,
+    same Gram matrix and transform, each chunk's product computed whole and
+    rounded to fp32 exactly as loaded), as a (len(ids), d) fp32 numpy array:
+    the input of the CPU oracle beside a device engine built at config 5."""
+    import torch
+    ids = np.asarray(ids, np.int64)
+    gen = torch.Generator(device="cuda")
+    gram = torch.zeros(d, d, dtype=torch.float64, device="cuda")
+    for c0 in range(0, n, chunk):
+        gen.manual_seed(seed * 1000003 + c0 // chunk)
+        blk = torch.randn(min(chunk, n - c0), d, generator=gen, device="cuda").double()
+        gram += blk.T @ blk
+        del blk
+    R = torch.linalg.cholesky(gram, upper=True)
+    T = torch.linalg.inv(R) * torch.as_tensor(np.sqrt(sigma), device="cuda")[None, :]
+    out = np.zeros((len(ids), d), np.float32)
+    for c0 in range(0, n, chunk):
+        sel = np.nonzero((ids >= c0) & (ids < c0 + chunk))[0]
+        if len(sel) == 0:
+            continue
+        gen.manual_seed(seed * 1000003 + c0 // chunk)
+        blk = torch.randn(min(chunk, n - c0), d, generator=gen, device="cuda").double()
+        rows = (blk @ T).float()
+        out[sel] = rows[torch.as_tensor(ids[sel] - c0, device="cuda")].cpu().numpy()
+        del blk, rows
+    return out
+
+
+def cfg5_inputs(n_events, seed=4, scale=26, ef=16):
+    """Config 5's graph (R-MAT, device-built CSR) and its first `n_events`
+    degree-proportional insertions: (keys, off, tgt, su, sv) as CUDA tensors /
+    numpy arrays."""
+    import torch
+    n = 1 << scale
+    keys = rmat_keys_device(scale, ef, seed)
+    off, tgt = csr_from_keys_device(n, keys)
+    su, sv = degree_proportional_inserts(keys, tgt, n_events, seed=seed)
+    torch.cuda.empty_cache()
+    return keys, off, tgt, su, sv

@@ -178,8 +178,8 @@ def rowlocal_insert_check(e, u, v, sample, d):
     k = e.k
     px, py, sig = e.get(ge.PX), e.get(ge.PY), e.get(ge.SIGMA)
     rows = np.concatenate([[u, v], sample]).astype(np.int64)
-    xb = e.query(ge.XB, rows).astype(np.float64)
-    yb = e.query(ge.YB, rows).astype(np.float64)
+    xb = e.query64(ge.XB, rows)
+    yb = e.query64(ge.YB, rows)
     # step 1: b = e_u, c = e_v ; step 2: b = e_v, c = e_u (graph.cpp:95-108)
     r1 = oracle.edge_update_rowlocal_p(k, d, xb[0], yb[1], px, py, sig, 1.0)
     # base rows after step 1 in the coordinates of r1["px"]: untouched rows
@@ -317,8 +317,8 @@ def compact_oracle(e, rows, off_h, tgt_h, d):
     snapshot restricted to `rows` (duplicate / missing-edge checks for the
     stream's endpoints are the full graph's)."""
     rows = np.asarray(rows, np.int64)
-    xb = e.query(ge.XB, rows).astype(np.float64)
-    yb = e.query(ge.YB, rows).astype(np.float64)
+    xb = e.query64(ge.XB, rows)
+    yb = e.query64(ge.YB, rows)
     px, py, sig = e.get(ge.PX), e.get(ge.PY), e.get(ge.SIGMA)
     src, dst = [], []
     for i, r in enumerate(rows.tolist()):
@@ -506,8 +506,7 @@ def test_cfg5_full_scale_compact_oracle():
     off0 = np.zeros(len(rows) + 1, np.int64)
     oe = oracle.OracleEngine(oracle.Graph(len(rows), np.zeros(0, np.int64), np.zeros(0, np.int64),
                                           None, True), d=d, alpha=1.0,
-                             factors=(e.query(ge.XB, rows).astype(np.float64),
-                                      e.query(ge.YB, rows).astype(np.float64), e.get(ge.PX),
+                             factors=(e.query64(ge.XB, rows), e.query64(ge.YB, rows), e.get(ge.PX),
                                       e.get(ge.PY), e.get(ge.SIGMA)))
     del off0
     wp, ws = compact_stream_check(e, oe, rows, su, sv, 100, 1000, "cfg5", 5)

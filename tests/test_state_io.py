@@ -80,7 +80,11 @@ def test_save_is_reference_layout_and_round_trips(tmp_path):
     e.save_state(path)
     st = read_damf(path)
     assert st["ver"] == 1 and st["d"] == 12 and st["applied"] == 60
-    assert np.array_equal(st["xb"], e.get(ge.XB).astype(np.float64))
+    # base rows exactly: fp32 rows widened, rows written through P^-1 at
+    # their fp64 side-table values
+    assert np.array_equal(st["xb"], e.get(ge.XB64))
+    assert np.array_equal(st["yb"], e.get(ge.YB64))
+    assert np.array_equal(st["xb"].astype(np.float32), e.get(ge.XB))
     assert np.array_equal(st["px"], e.get(ge.PX))
     assert np.array_equal(st["zb"], e.get(ge.ZB).astype(np.float64))
     off, ids, _ = e.graph_sets()
@@ -164,7 +168,12 @@ def test_oracle_file_resumes_on_device_bit_identically(tmp_path):
     path2 = str(tmp_path / "device.damf")
     e.save_state(path2)
     o2 = oracle.OracleEngine.load_state(path2)
-    for which, ow in ((ge.XB, oe.XB), (ge.YB, oe.YB), (ge.ZB, oe.ZB), (ge.RB, oe.RB)):
+    # X_b / Y_b round-trip in fp64 (rows fp32 cannot hold sit in the fp64
+    # side table); Z_b / r_b are fp32 on the device
+    for ow in (oe.XB, oe.YB):
+        assert np.array_equal(o2.get(ow), oe.get(ow)), ow
+    assert np.array_equal(e.get(ge.XB64), oe.get(oe.XB))
+    for which, ow in ((ge.ZB, oe.ZB), (ge.RB, oe.RB)):
         assert np.array_equal(o2.get(ow), e.get(which).astype(np.float64)), which
     assert np.array_equal(o2.get(o2.PX), oe.get(oe.PX))
     off2, ids2, _ = o2.graph_sets()
