@@ -23,7 +23,8 @@ struct DevCtl {
   long long rank1;    // rank-1 steps run
   long long folds;    // eager folds (rank change / ill-conditioned F)
   long long rows_x, rows_y;  // X_b / Y_b row counts
-  double cond_est;    // running cond(P_X) upper estimate
+  double cond_est;    // running cond(P_X) estimate (|P|_F |P^-1|_F / sqrt(k))
+  double cond_est_y;  // the same for P_Y
   int need_rebase;    // set when cond_est > rebase_cond
   int pad;
   double smax;        // proj_row_bound(P_X) at the end of the last step

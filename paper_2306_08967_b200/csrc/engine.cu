@@ -1008,9 +1008,15 @@ int damf_gpu_rebase(damf_gpu* h) {
   // products and leave the table. Every other row is benign and takes the
   // fast HBM-bound path. With an overflowed table (some such rows are fp32
   // only), PPR state or k > 128 the bulk fold runs in fp64 as well.
+  // The fast path (3 x TF32 products, fp32 accumulation) errs by ~2^-22 of
+  // sum |x_i P_ij|, which exceeds |x P| by up to cond(P): above
+  // kFastFoldCond every row is folded with fp64 products instead (DMMA).
+  constexpr double kFastFoldCond = 100.0;
+  const double condx = h->h_ctl->cond_est, condy = h->h_ctl->cond_est_y;
   auto fold = [&](float* base, const double* PT, int side) -> int {
     const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
-    if (nd >= 0 && nd <= kDirtyCap && k <= 128) {
+    const double cond = side == 1 ? condy : condx;
+    if (nd >= 0 && nd <= kDirtyCap && k <= 128 && cond <= kFastFoldCond) {
       CK(launch_materialize(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
     } else if (!tmp) {
       CK(launch_materialize_precise(base, h->n, k, d, PT, ld, k, base, d, h->st, h->nsm));
@@ -1041,9 +1047,9 @@ int damf_gpu_rebase(damf_gpu* h) {
   CK(cudaGetLastError());
   if (!h->alpha1) CK(launch_ppr_keys(ppr_args(h), h->nsm, h->st));
   h->launches += (h->alpha1 ? 2 : 5) + 2 + 4;  // folds, side-table folds, P = Q = I
-  h->h_ctl->cond_est = 1.0;
+  h->h_ctl->cond_est = h->h_ctl->cond_est_y = 1.0;
   h->h_ctl->need_rebase = 0;
-  CK(cudaMemcpyAsync(&h->ctl->cond_est, &h->h_ctl->cond_est, sizeof(double), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(&h->ctl->cond_est, &h->h_ctl->cond_est, 2 * sizeof(double), cudaMemcpyHostToDevice, h->st));
   CK(cudaMemcpyAsync(&h->ctl->need_rebase, &h->h_ctl->need_rebase, sizeof(int), cudaMemcpyHostToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (tmp) cudaFree(tmp);
@@ -1665,10 +1671,15 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
   // (benign rows) and, above kPreciseCond, the dirty rows (written through
   // P^-1 since the last fold) are recomputed in fp64 and patched in; without
   // a usable dirty list (PPR state, overflow) the whole fold is fp64.
-  constexpr double kPreciseCond = 100.0;
+  // A one-shot query tolerates the fast path's ~sqrt(k) 2^-22 relative error
+  // on typical rows up to a moderate cond(P) (rows in P's small singular
+  // directions lose ~log10(cond) digits); above kPreciseCond every row takes
+  // fp64 products. Side-table rows are always folded from fp64.
+  constexpr double kPreciseCond = 1e4;
   const int side = which == DAMF_Y ? 1 : (which == DAMF_Z && !h->alpha1) ? -1 : 0;
   const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
-  if (h->h_ctl->cond_est <= kPreciseCond || (nd >= 0 && nd <= kDirtyCap && h->k <= 128)) {
+  const double cond = side == 1 ? h->h_ctl->cond_est_y : h->h_ctl->cond_est;
+  if (cond <= kPreciseCond) {
     CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
   } else {
     CK(launch_materialize_precise(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));

@@ -72,10 +72,10 @@ struct Smem {
   int kidx[NPAD], defl[NPAD], src[NPAD], org[NPAD];
   double tau[NPAD], zhat[NPAD], lamA[NPAD], lamB[NPAD];
   double s2[NPAD], exv[NPAD], eyv[NPAD], dH[NPAD], dE[NPAD];
-  double AHdH[NPAD], AEdE[NPAD], yA1[NPAD], yB1[NPAD];
+  double cH[NPAD], cE[NPAD], yA1[NPAD], yB1[NPAD];  // dropped columns of H / E (top k)
   int rot_p[NPAD], rot_q[NPAD];
   double rot_c[NPAD], rot_s[NPAD];
-  double partL[4][kMaxD];         // this CTA's partial column sums
+  double partL[2][kMaxD];         // this CTA's partial column sums
   double partS[4];                // this CTA's partial scalars
   double pnorm[C][4];
   double priv[4][PROWS * PLD];    // owned rows of Q2T/F, E/G^-1, H/F^-1, G
@@ -443,8 +443,9 @@ DAMF_D void rows_gemms(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0,
 // Q = P^-1 (row-major, ld) for P given transposed (PT[j][i] = P[i][j]):
 // Gauss-Jordan with partial pivoting in place in Q, pivot row and column
 // factors staged in shared memory (prow, fcol, perm: >= k doubles each).
-// Used for the rare steps whose closed-form inverse would be ill-conditioned
-// (1 - |d|^2 below 1e-10); returns false if P is singular.
+// Used for the rare steps whose kept block is numerically singular (|h| <=
+// 1e-12, see rank1_step) or whose H column k is unreliable; returns false if
+// P is singular.
 DAMF_D bool gj_inverse_cta(const double* PT, double* Q, int k, int ld, double* prow, double* fcol,
                            double* perm, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1277,35 +1278,50 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       *cl.map_shared_rank(S.dE + t, lane) = dEt;
     }
   }
-  // gE = 1 - |d_E|^2 equals E[k][k]^2 for the dropped column (E orthogonal);
-  // the direct form keeps its relative accuracy when |d_E| -> 1, where the
-  // subtraction cancels and the closed-form G^-1 (and with it the maintained
-  // P_Y^-1) would drift event by event.
-  if (edge && k2 == k && k >= olo && k < ohi && warp == 0 && lane < C)
-    *cl.map_shared_rank(S.dE + k, lane) = prow(1, k)[k];
+  // The dropped (k+1)-th singular pair, broadcast by its owner (the last CTA):
+  // c_H = H[0:k, k], h_H = H[k][k] and (edge) c_E, h_E from E. For the kept
+  // k x k block A of an orthogonal (k+1) x (k+1) matrix with bottom row d,
+  // A d^T = -c h and 1 - |d|^2 = h^2, so
+  //     A^-1 = A^T - d^T c / h
+  // whose error grows like 1/|h| = cond(A); the form A^T + d^T (A d^T)^T / (1 - |d|^2)
+  // squares it (A d^T is a cancelling sum of size |h|, then divided by h^2).
+  // At config 5 the kept block routinely has h ~ 1e-4 (an old direction is
+  // dropped for the new one), where the squared form loses 8 digits per step.
+  // H's column k = M^T E[:, k] / s_k needs s_k well above zero.
+  const bool hk_ok = k2 == k && S.s2[k] > 1e-6 * S.s2[0];
+  if (hk_ok && k >= olo && k < ohi) {
+    const double* Ek = prow(1, k);
+    if (warp == 0) {
+      double aEk = 0;
+      for (int i = lane; i < n; i += 32) aEk += S.av[i] * Ek[i];
+      aEk = warp_sum(aEk);
+      if (lane == 0) S.bred[0] = aEk;
+    }
+    __syncthreads();
+    const double aEk = S.bred[0], isk = 1.0 / S.s2[k];
+    for (int x = tid; x < C * n; x += NT) {
+      const int r = x / n, i = x % n;
+      *cl.map_shared_rank(S.cH + i, r) = (S.Dg[i] * Ek[i] + S.bv[i] * aEk) * isk;
+      if (edge) *cl.map_shared_rank(S.cE + i, r) = Ek[i];
+    }
+  }
   __syncthreads();
   // partial column sums over this CTA's kept columns (local smem):
-  //  0: sum_t H[i][t] dH_t          (A_H d_H)
-  //  1: sum_t E[i][t] dE_t          (A_E d_E)
-  //  2: sum_t c_t w_t H[i][t]       (row fix, side A: c = ex, w = sqrt(s))
-  //  3: sum_t c_t w_t B[i][t]       (row fix, side B: edge c = ey, w = sqrt(s), B = E;
+  //  0: sum_t c_t w_t H[i][t]       (row fix, side A: c = ex, w = sqrt(s))
+  //  1: sum_t c_t w_t B[i][t]       (row fix, side B: edge c = ey, w = sqrt(s), B = E;
   //                                  node c = vrow, w = 1/sqrt(s), B = H)
   {
     const int tk = min(ohi, k);
     for (int i = tid; i < k; i += NT) {
-      double p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+      double p2 = 0, p3 = 0;
       for (int t = olo; t < tk; ++t) {
         const double Hi = prow(2, t)[i], Ei = prow(1, t)[i];
         const double rs = sqrt(S.s2[t]);
-        p0 += Hi * S.dH[t];
-        p1 += Ei * S.dE[t];
         p2 += S.exv[t] * rs * Hi;
         p3 += edge ? S.eyv[t] * rs * Ei : S.eyv[t] / rs * Hi;
       }
-      S.partL[0][i] = p0;
-      S.partL[1][i] = p1;
-      S.partL[2][i] = p2;
-      S.partL[3][i] = p3;
+      S.partL[0][i] = p2;
+      S.partL[1][i] = p3;
     }
     if (warp == 0) {
       double q0 = 0, q1 = 0;
@@ -1329,11 +1345,11 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     int lo, hi;
     block_range(k, C, rank, lo, hi);
     const int w = hi - lo;
-    for (int x = tid; x < 4 * w; x += NT) {
+    for (int x = tid; x < 2 * w; x += NT) {
       const int q = x / w, i = lo + x % w;
       double s = 0;
       for (int r = 0; r < C; ++r) s += *cl.map_shared_rank(&S.partL[q][i], r);
-      double* dst = q == 0 ? S.AHdH : q == 1 ? S.AEdE : q == 2 ? S.yA1 : S.yB1;
+      double* dst = q == 0 ? S.yA1 : S.yB1;
       for (int r = 0; r < C; ++r) *cl.map_shared_rank(dst + i, r) = s;
     }
   }
@@ -1368,39 +1384,35 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     if (eynz && (!edge || st.c_val != 0.0)) put(sB, st.c_row);
   }
   PROF_MARK(7);
-  double nH = 0, nE = 0;
-  for (int t = tid; t < min(k2, k); t += NT) {
-    nH += S.dH[t] * S.dH[t];
-    nE += S.dE[t] * S.dE[t];
-  }
-  nH = block_sum(S, nH);
-  nE = block_sum(S, nE);
-  const double gH = 1.0 - nH;
-  const double gE = edge && k2 == k ? S.dE[k] * S.dE[k] : 1.0 - nE;
-  // Closed-form inverses need 1 - |d|^2 well away from 0; otherwise the step
-  // stays lazy but P^-1 is recomputed exactly (Gauss-Jordan) and a rebase is
-  // requested (the reference folds eagerly when its LU is unreliable,
-  // factor_state.cpp:168-177; a rebase is the grid-wide equivalent here).
-  // Eager folds remain for rank changes (k2 != k).
+  // Closed-form inverses need h well away from 0 (and H's column k, i.e.
+  // s_k > 0); otherwise the step stays lazy but P^-1 is recomputed exactly
+  // (Gauss-Jordan) and a rebase is requested (the reference folds eagerly
+  // when its LU is unreliable, factor_state.cpp:168-177; a rebase is the
+  // grid-wide equivalent here). Eager folds remain for rank changes (k2 != k).
   const bool lazy = k2 == k;
-  const bool exact = lazy && !(gH > 1e-10 && (!edge || gE > 1e-10));
+  const double hH = hk_ok ? S.cH[k] : 0.0, hE = edge && hk_ok ? S.cE[k] : 1.0;
+  // (the stable form's error ~ eps / |h| is what an exact inversion of the
+  // ill-conditioned block costs as well; only a numerically singular block,
+  // |h| <= 1e-12, where the reference's LU pivot test fails too, is inverted
+  // exactly and folded away)
+  const bool exact = lazy && !(hk_ok && fabs(hH) > 1e-12 && fabs(hE) > 1e-12);
   const int npp = 1 - S.pp[sA], nppB = 1 - S.pp[sB];
   double* PTA_n = A.PT[sA][npp];
   double* PTB_n = A.PT[sB][nppB];
   double* QA_n = A.Q[sA][npp];
   double* QB_n = A.Q[sB][nppB];
   if (lazy) {
-    const double igH = 1.0 / gH, igE = 1.0 / gE;
+    const double ihH = 1.0 / hH, ihE = 1.0 / hE;
     const int fbuf = edge ? 2 : 1, gbuf = edge ? 1 : 2;
     if (!exact) {
     // ---- 5. row fixes from the OLD inverse: y = (ex F^-1) P_old^-1 ----------
     //   ex F^-1 [m] = (1/sqrt(sig_m)) (sum_t ex_t sqrt(s_t) H[m][t]
-    //                                  + (A_H d_H)[m] / gH * sum_t ex_t sqrt(s_t) dH_t)
+    //                                  - c_H[m] / h_H * sum_t ex_t sqrt(s_t) dH_t)
     for (int m = tid; m < k; m += NT) {
       const double rsm = sqrt(S.sig[m]);
-      S.yA1[m] = (S.yA1[m] + S.AHdH[m] * igH * sA_) / rsm;
-      S.yB1[m] = edge ? (S.yB1[m] + S.AEdE[m] * igE * sB_) / rsm
-                      : (S.yB1[m] + S.AHdH[m] * igH * sB_) * rsm;
+      S.yA1[m] = (S.yA1[m] - S.cH[m] * ihH * sA_) / rsm;
+      S.yB1[m] = edge ? (S.yB1[m] - S.cE[m] * ihE * sB_) / rsm
+                      : (S.yB1[m] - S.cH[m] * ihH * sB_) * rsm;
     }
     __syncthreads();
     {
@@ -1425,16 +1437,16 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       }
     }
     // ---- inverse rows (private, in place) ----------------------------------
-    //   F^-1[t][m] = sqrt(s_t) (H[m][t] + dH_t (A_H d_H)[m]/gH) / sqrt(sig_m)
-    //   edge: G^-1[t][m] = sqrt(s_t) (E[m][t] + dE_t (A_E d_E)[m]/gE) / sqrt(sig_m)
-    //   node: G^-1[t][m] = (H[m][t] + dH_t (A_H d_H)[m]/gH) sqrt(sig_m) / sqrt(s_t)
+    //   F^-1[t][m] = sqrt(s_t) (H[m][t] - dH_t c_H[m] / h_H) / sqrt(sig_m)
+    //   edge: G^-1[t][m] = sqrt(s_t) (E[m][t] - dE_t c_E[m] / h_E) / sqrt(sig_m)
+    //   node: G^-1[t][m] = (H[m][t] - dH_t c_H[m] / h_H) sqrt(sig_m) / sqrt(s_t)
     for (int x = tid; x < (kohi - olo) * k; x += NT) {
       const int t = olo + x / k, m = x % k;
       const double rst = sqrt(S.s2[t]), rsm = sqrt(S.sig[m]);
-      const double ahinv = prow(2, t)[m] + S.dH[t] * S.AHdH[m] * igH;
+      const double ahinv = prow(2, t)[m] - S.dH[t] * S.cH[m] * ihH;
       double gi;
       if (edge)
-        gi = rst * (prow(1, t)[m] + S.dE[t] * S.AEdE[m] * igE) / rsm;
+        gi = rst * (prow(1, t)[m] - S.dE[t] * S.cE[m] * ihE) / rsm;
       else
         gi = ahinv * rsm / rst;
       prow(fbuf, t)[m] = rst * ahinv / rsm;  // edge: over H (read above); node: over E
@@ -1459,7 +1471,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       cl.sync();  // new P^T rows visible
       if (rank < 2) {
         const bool ok = gj_inverse_cta(rank == 0 ? PTA_n : PTB_n, rank == 0 ? QA_n : QB_n, k, ld,
-                                       S.yA1, S.yB1, S.AHdH, S.AEdE);
+                                       S.yA1, S.yB1, S.cH, S.cE);
         if (!ok && tid == 0) {
           A.ctl->err = 8;  // SingularProjection (factor_state.cpp:21-36)
           A.ctl->err_event = ev_index;
@@ -1518,6 +1530,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       const double by = sqrt(p2o) * sqrt(q2o);
       const double rk = sqrt((double)k);
       A.ctl->cond_est = bx / rk;
+      A.ctl->cond_est_y = by / rk;
       // P_X as engine.cpp:38-40; P_Y as well (its rows are fp64-slotted the
       // same way and P_Y^-1 is maintained by products too)
       if (fmax(bx, by) / rk > A.rebase_cond) A.ctl->need_rebase = 1;
@@ -1616,7 +1629,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       A.ctl->k = k2;
       A.ctl->rank1 += 1;
       A.ctl->folds += 1;
-      A.ctl->cond_est = 1.0;
+      A.ctl->cond_est = A.ctl->cond_est_y = 1.0;
       A.ctl->dirty_n[0] = A.ctl->dirty_n[1] = 0;  // folded (fp64 slots read), P = I
     }
   }
