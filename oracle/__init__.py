@@ -59,6 +59,7 @@ def lib():
                                                     f64p, f64p, C.c_double, f64p, f64p, f64p,
                                                     f64p, f64p, f64p, f64p, i64p]
         L.oracle_engine_row_log_enable.argtypes = [C.c_void_p, C.c_int]
+        L.oracle_engine_set_fp32_base.argtypes = [C.c_void_p, C.c_int]
         L.oracle_engine_row_log.argtypes = [C.c_void_p, i64p, C.c_int64]
         L.oracle_engine_row_log.restype = C.c_int64
         L.oracle_engine_save_state.argtypes = [C.c_void_p, C.c_char_p]
@@ -242,6 +243,11 @@ class OracleEngine:
 
     def rebase(self):
         lib().oracle_engine_rebase(self.h)
+
+    def set_fp32_base(self, on=True):
+        """The device's storage model: base rows rounded to fp32 at every
+        fold (rebase / eager fold), lazily solved rows fp64 until then."""
+        lib().oracle_engine_set_fp32_base(self.h, int(on))
 
     def row_log_enable(self, on=True):
         """Record the row sets of every ProjectionUpdate's dX / dY from now on

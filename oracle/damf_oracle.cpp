@@ -508,6 +508,7 @@ AppliedDelta FactorState::apply_update(const ProjectionUpdate& u) {
     ++eager_folds;
     xb_ = matmul(xb_, px_new);
     yb_ = matmul(yb_, py_new);
+    if (fp32_base) round_base();
     for (Index t = 0; t < u.dX.nnz_rows(); ++t)
       for (Index j = 0; j < k2; ++j) xb_(u.dX.idx[t], j) += u.dX.vals(t, j);
     for (Index t = 0; t < u.dY.nnz_rows(); ++t)
@@ -551,7 +552,13 @@ Mat FactorState::rebase() {  // factor_state.cpp:215-222
   yb_ = matmul(yb_, py_);
   px_ = Mat::eye(rank());
   py_ = Mat::eye(rank());
+  if (fp32_base) round_base();
   return tx;
+}
+
+void FactorState::round_base() {  // harness fp32 storage mode
+  for (double& v : xb_.a) v = static_cast<double>(static_cast<float>(v));
+  for (double& v : yb_.a) v = static_cast<double>(static_cast<float>(v));
 }
 
 double FactorState::cond_estimate() const {  // factor_state.cpp:224-249

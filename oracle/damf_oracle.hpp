@@ -245,6 +245,12 @@ class FactorState {
   double ortho_defect_y() const;
   // Counters used by the parity harness (not in the reference).
   std::uint64_t eager_folds = 0;
+  // Harness mode (not in the reference): the device's storage model -- base
+  // rows rounded to fp32 whenever a fold writes them (rebase, eager fold),
+  // rows written through the lazy solve kept in fp64 until then -- so
+  // storage-precision effects can be told apart from logic differences.
+  bool fp32_base = false;
+  void round_base();
 
  private:
   Mat xb_, yb_, px_, py_;

@@ -399,6 +399,14 @@ void oracle_stream_events(void* hp, int32_t* kind, int64_t* u, int64_t* v, doubl
 
 // ---- harness: modified-row log (see Engine::row_log) -----------------------
 extern "C" {
+// fp32 base-row storage model (FactorState::fp32_base); rounds the current
+// base rows once when switched on.
+void oracle_engine_set_fp32_base(void* hp, int on) {
+  auto* h = static_cast<OEngine*>(hp);
+  auto& fs = const_cast<FactorState&>(h->eng.state());
+  fs.fp32_base = on != 0;
+  if (on) fs.round_base();
+}
 // Start (on != 0) or stop logging; starting clears the log and the step count.
 void oracle_engine_row_log_enable(void* hp, int on) {
   auto* h = static_cast<OEngine*>(hp);

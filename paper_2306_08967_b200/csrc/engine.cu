@@ -221,6 +221,15 @@ __global__ void base_rows64_kernel(const float* base, int d, const int32_t* slot
   }
 }
 
+__global__ void count_sum_kernel(const int32_t* cnt, int64_t n, unsigned long long* out) {
+  unsigned long long s = 0;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    s += (unsigned long long)cnt[x];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
 __global__ void set_slots_kernel(int32_t* slot, const int64_t* rows, long long ns) {
   for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
        s += (long long)gridDim.x * blockDim.x)
@@ -760,6 +769,9 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   c0.rows_x = n;
   c0.rows_y = n;
   c0.cond_est = 1.0;
+  c0.cond_est_y = 1.0;
+  c0.ppr_skip = -1;
+  c0.stop_event = -1;
   *h->h_ctl = c0;
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, h->st));
   // ---- graph (slack CSR)
@@ -1298,6 +1310,40 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
   int64_t rebases = 0;
   int64_t i = 0;
   int64_t n_before = h->n;
+  const bool split_mode = ppr && event_cluster_size() == 16;
+  // the PPR absorb / push of one event on its own (after a rebase it waited for)
+  auto event_ppr = [&](int64_t e) -> int {
+    const bool fused_e = h->n_cap <= (1 << 20) || (mode & DAMF_APPLY_DEFER_PUSH);
+    if (fused_e && split_mode) {
+      ea.e_begin = e;
+      ea.e_end = e + 1;
+      CK(launch_ppr_kernel(ea, h->st));
+      h->launches += 1;
+    } else {
+      const EventDesc& ed = h->ev.h[e];
+      PprArgs pa = ppr_args(h);
+      pa.k = h->k;
+      CK(launch_ppr_absorb(pa, h->touched.d + ed.touched_off, (int)ed.touched_cnt, h->st));
+      h->launches += 1;
+      if (push_each)
+        if (int r = run_push(h, 8 * h->nsm, timing ? h->t_end + e : nullptr)) return r;
+    }
+    return 0;
+  };
+  int64_t host_ppr_skip = -1;  // the whole-GPU path records it on the host
+  auto pending_ppr = [&]() -> int {
+    const int64_t e = host_ppr_skip >= 0 ? host_ppr_skip : h->h_ctl->ppr_skip;
+    host_ppr_skip = -1;
+    if (!ppr || e < 0) return 0;
+    h->h_ctl->ppr_skip = -1;
+    h->h_ctl->stop_event = -1;
+    CK(cudaMemcpyAsync(&h->ctl->stop_event, &h->h_ctl->stop_event, sizeof(long long),
+                       cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(&h->ctl->ppr_skip, &h->h_ctl->ppr_skip, sizeof(long long), cudaMemcpyHostToDevice,
+                       h->st));
+    if (int r = event_ppr(e)) return r;
+    return sync_ctl(h);
+  };
   while (i < ok_count) {
     // events up to the next rebase_every boundary (engine.cpp:37-40)
     int64_t j = ok_count;
@@ -1343,26 +1389,18 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         ea.e_begin = e;
         ea.e_end = e + 1;
         CK(launch_event_kernel(ea, h->st));
-        h->launches += 1 + (ed_absorb_nonempty(h, e) ? 1 : 0);
-        // rows appended by AddNode are visible to the enhancer from here
-        const EventDesc& ed = h->ev.h[e];
-        const int64_t n_prev = h->n;
-        if (ed.kind == DAMF_ADD_NODE) h->n = ed.u + 1;
-        PprArgs pa = ppr_args(h);
-        pa.k = h->k;
-        CK(launch_ppr_absorb(pa, h->touched.d + ed.touched_off, (int)ed.touched_cnt, h->st));
-        if (push_each) {
-          if (int r = run_push(h, 8 * h->nsm, timing ? h->t_end + e : nullptr)) return r;
-        }
+        h->launches += 1;
         if (int r = sync_ctl(h)) return r;
-        if (h->h_ctl->err) {
-          h->n = n_prev;
-          break;
-        }
+        if (h->h_ctl->err) break;
+        // rows appended by AddNode are visible to the enhancer from here
+        if (h->ev.h[e].kind == DAMF_ADD_NODE) h->n = h->ev.h[e].u + 1;
         if (h->h_ctl->need_rebase) {
+          // absorb / push after the fold (see damf_ppr_kernel)
+          host_ppr_skip = e;
           h->h_ctl->stop_event = e + 1;
           break;
         }
+        if (int r = event_ppr(e)) return r;
       }
     }
     if (int r = sync_ctl(h)) return r;
@@ -1381,6 +1419,8 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     if (stopped || (h->cfg.rebase_every > 0 && h->since_rebase >= h->cfg.rebase_every)) {
       if (int r = damf_gpu_rebase(h)) return r;
       ++rebases;
+      if (int r = pending_ppr()) return r;
+      if (h->h_ctl->err) break;
     }
     i = done;
   }
@@ -1418,6 +1458,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
   if (!status && h->h_ctl->need_rebase) {
     if (int r = damf_gpu_rebase(h)) return r;
     ++rebases;
+    if (int r = pending_ppr()) return r;
   }
   if (log_rows) {
     // rebases inside the call do not touch the log; the mirror is fresh here
@@ -2043,13 +2084,16 @@ int damf_gpu_diagnostics(damf_gpu* h, damf_diag* o) {
   o->n = h->n;
   o->k = h->k;
   o->d = h->d;
-  int64_t arcs = 0;
-  {
-    std::vector<int32_t> cnt(h->n);
-    CK(cudaMemcpy(cnt.data(), h->out.cnt, h->n * 4, cudaMemcpyDeviceToHost));
-    for (auto c : cnt) arcs += c;
-  }
-  o->arcs = arcs;
+  unsigned long long* dsum = nullptr;
+  CK(cudaMalloc(&dsum, 8));
+  CK(cudaMemsetAsync(dsum, 0, 8, h->st));
+  count_sum_kernel<<<h->nsm * 4, 256, 0, h->st>>>(h->out.cnt, h->n, dsum);
+  CK(cudaGetLastError());
+  unsigned long long arcs = 0;
+  CK(cudaMemcpyAsync(&arcs, dsum, 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(dsum);
+  o->arcs = (int64_t)arcs;
   o->events_applied = (int64_t)h->events_applied;
   o->events_since_rebase = h->since_rebase;
   o->cond_estimate = h->h_ctl->cond_est;

@@ -1237,7 +1237,20 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   PROF_MARK(5);
   const double* lamF = edge ? S.lamB : S.lamA;
   // ---- truncation (update_engine.cpp:39-52, svd.cpp:37-38) ----------------
-  for (int t = tid; t < n; t += NT) S.s2[t] = sqrt(fmax(edge ? lamF[t] : lamF[n - 1 - t], 0.0));
+  // sigma = sqrt(lambda) of M M^T: lambda carries an absolute error of a few
+  // eps lambda_max, so singular values below ~sqrt(64 eps) sigma_1 (1.2e-7
+  // sigma_1) are indistinguishable from zero here and are treated as zero.
+  // The reference's direct SVD resolves them down to its 1e-12 sigma_1 floor
+  // (update_engine.cpp:41-44); values in between arise from its in-span
+  // clamp (R >= 1e-12, update_engine.cpp:154-155) and contribute < 1.2e-7 of
+  // |M| (a documented deviation: the device's rank may then be lower).
+  {
+    const double lmax = fmax(edge ? lamF[0] : lamF[n - 1], 0.0);
+    for (int t = tid; t < n; t += NT) {
+      const double l = edge ? lamF[t] : lamF[n - 1 - t];
+      S.s2[t] = l > 64.0 * EPS * lmax ? sqrt(l) : 0.0;
+    }
+  }
   __syncthreads();
   int k2 = allow_grow ? n : k;
   while (k2 > 0 && S.s2[k2 - 1] <= 0.0) --k2;
@@ -1389,13 +1402,18 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   // (Gauss-Jordan) and a rebase is requested (the reference folds eagerly
   // when its LU is unreliable, factor_state.cpp:168-177; a rebase is the
   // grid-wide equivalent here). Eager folds remain for rank changes (k2 != k).
-  const bool lazy = k2 == k;
   const double hH = hk_ok ? S.cH[k] : 0.0, hE = edge && hk_ok ? S.cE[k] : 1.0;
   // (the stable form's error ~ eps / |h| is what an exact inversion of the
   // ill-conditioned block costs as well; only a numerically singular block,
-  // |h| <= 1e-12, where the reference's LU pivot test fails too, is inverted
-  // exactly and folded away)
-  const bool exact = lazy && !(hk_ok && fabs(hH) > 1e-12 && fabs(hE) > 1e-12);
+  // |h| <= 1e-12, where the reference's LU pivot test fails too, needs more:
+  // the reference folds eagerly then (factor_state.cpp:168-177). States up to
+  // 2^20 rows fold in the cluster (the eager branch below); larger ones take
+  // an exact Gauss-Jordan P^-1 and fold over the whole GPU right after the
+  // event (a requested rebase).)
+  const bool singular_block = k2 == k && !(hk_ok && fabs(hH) > 1e-12 && fabs(hE) > 1e-12);
+  const bool small_state = max(A.ctl->rows_x, A.ctl->rows_y) <= (1ll << 20);
+  const bool lazy = k2 == k && !(singular_block && small_state);
+  const bool exact = lazy && singular_block;
   const int npp = 1 - S.pp[sA], nppB = 1 - S.pp[sB];
   double* PTA_n = A.PT[sA][npp];
   double* PTB_n = A.PT[sB][nppB];
@@ -2000,6 +2018,14 @@ __global__ void __launch_bounds__(PPR_NT, 1) damf_ppr_kernel(EventKernelArgs A) 
   for (int64_t e = A.e_begin; e < A.e_end; ++e) {
     const long long stop = *(volatile long long*)&A.ctl->stop_event;
     if (*(volatile int*)&A.ctl->err || (stop >= 0 && stop <= e)) break;
+    // this event's factor update requested a rebase: Z_b / r_b are fp32 base
+    // coordinates, so the absorb and push wait until the host has folded
+    // everything to P = I (a rebase is query-transparent for the enhancer,
+    // enhancer.cpp:196-206); the host relaunches this kernel for event e
+    if (*(volatile int*)&A.ctl->need_rebase) {
+      if (rank == 0 && threadIdx.x == 0) A.ctl->ppr_skip = e;
+      break;
+    }
     const EventDesc ev = A.ev[e];
     ppr_event<C, PSmem<C>, PPR_NT>(A, S, cl, ev);
     if (A.t_end && rank == 0 && threadIdx.x == 0) A.t_end[e] = globaltimer();
