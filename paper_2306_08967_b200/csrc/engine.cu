@@ -27,6 +27,9 @@ namespace {
 // a full table requests a rebase): 2 rows per side per edge event, so a
 // table outlasts the reference's 50,000-event rebase period
 constexpr long long kDirtyCap = 1 << 17;
+// DevCtl followed by the 8 push counters (pushes, rounds, round base, ...)
+constexpr size_t kCtlOff = (sizeof(dgpu::DevCtl) + 63) & ~size_t(63);
+constexpr size_t kCtlBytes = kCtlOff + 8 * sizeof(long long);
 
 #define CK(expr)                                                                       \
   do {                                                                                 \
@@ -306,6 +309,11 @@ struct damf_gpu {
   double* smax = nullptr;
   long long* pstats = nullptr;  // pushes, rounds, round base
   long long* h_pstats = nullptr;
+  Staged<char> pack;  // every descriptor array of one apply, one H2D copy
+  EventDesc* d_ev = nullptr;
+  StepDesc* d_steps = nullptr;
+  int64_t *d_sp_rows = nullptr, *d_nb_ids = nullptr, *d_touched = nullptr;
+  double *d_sp_vals = nullptr, *d_nb_w = nullptr;
   Staged<EventDesc> ev;
   Staged<StepDesc> steps;
   Staged<int64_t> sp_rows, nb_ids, touched;
@@ -357,12 +365,12 @@ int fail(damf_gpu* h, int code, const std::string& msg) {
 
 EventKernelArgs event_args(damf_gpu* h) {
   EventKernelArgs a{};
-  a.ev = h->ev.d;
-  a.steps = h->steps.d;
-  a.sp_rows = h->sp_rows.d;
-  a.sp_vals = h->sp_vals.d;
-  a.nb_ids = h->nb_ids.d;
-  a.nb_w = h->nb_w.d;
+  a.ev = h->d_ev;
+  a.steps = h->d_steps;
+  a.sp_rows = h->d_sp_rows;
+  a.sp_vals = h->d_sp_vals;
+  a.nb_ids = h->d_nb_ids;
+  a.nb_w = h->d_nb_w;
   a.ctl = h->ctl;
   a.d = h->d;
   a.ld = h->ld;
@@ -381,7 +389,7 @@ EventKernelArgs event_args(damf_gpu* h) {
   a.listF = h->listF;
   a.listG = h->listG;
   a.listL = h->listL;
-  a.touched = h->touched.d;
+  a.touched = h->d_touched;
   a.pstats = h->pstats;
   for (int s = 0; s < 2; ++s)
     for (int p = 0; p < 2; ++p) {
@@ -475,8 +483,7 @@ PprArgs ppr_args(damf_gpu* h) {
 bool ed_absorb_nonempty(damf_gpu* h, int64_t e) { return h->ev.h[e].touched_cnt > 0; }
 
 int sync_ctl(damf_gpu* h) {
-  CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->st));
-  CK(cudaMemcpyAsync(h->h_pstats, h->pstats, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(h->h_ctl, h->ctl, kCtlBytes, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   h->k = h->h_ctl->k;
   h->round_base = (int)h->h_pstats[2];
@@ -563,9 +570,9 @@ void damf_gpu_destroy(damf_gpu* h) {
   if (!h) return;
   cudaStreamSynchronize(h->st);
   for (void* p : h->allocs) cudaFree(p);
-  if (h->h_ctl) cudaFreeHost(h->h_ctl);
+  if (h->h_ctl) cudaFreeHost(h->h_ctl);  // h_pstats lives in the same block
   if (h->h_pst) cudaFreeHost(h->h_pst);
-  if (h->h_pstats) cudaFreeHost(h->h_pstats);
+  h->pack.release();
   h->ev.release();
   h->steps.release();
   h->sp_rows.release();
@@ -700,11 +707,24 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev);
   CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
-  CK(cudaMallocHost(&h->h_ctl, sizeof(DevCtl)));
-  CK(cudaMallocHost(&h->h_pstats, 8 * sizeof(long long)));
+  // the control block and the push counters share one allocation (device and
+  // pinned host) so a single copy refreshes both (sync_ctl)
+  {
+    char* hb = nullptr;
+    CK(cudaMallocHost(&hb, kCtlBytes));
+    std::memset(hb, 0, kCtlBytes);
+    h->h_ctl = reinterpret_cast<DevCtl*>(hb);
+    h->h_pstats = reinterpret_cast<long long*>(hb + kCtlOff);
+  }
   const int64_t n = g->n, ncap = h->n_cap, d = h->d, ld = h->ld;
   // ---- factor state
-  CK(dalloc(h, &h->ctl, 1));
+  {
+    char* db = nullptr;
+    CK(dalloc(h, &db, kCtlBytes));
+    CK(cudaMemsetAsync(db, 0, kCtlBytes, h->st));
+    h->ctl = reinterpret_cast<DevCtl*>(db);
+    h->pstats = reinterpret_cast<long long*>(db + kCtlOff);
+  }
   for (int sd = 0; sd < 2; ++sd) {
     CK(dalloc(h, &h->dirty[sd], (size_t)kDirtyCap));
     CK(dalloc(h, &h->rows64[sd], (size_t)kDirtyCap * ((h->d + 1 + 3) & ~3)));
@@ -731,8 +751,7 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
   CK(cudaMemcpyAsync(h->sigma, sigma, k * 8, cudaMemcpyHostToDevice, h->st));
   CK(dalloc(h, &h->ws, (size_t)ld * ld + (size_t)4 * 16 * 20 * ld));
   CK(dalloc(h, &h->smax, 1));
-  CK(dalloc(h, &h->pstats, 8));
-  CK(cudaMemsetAsync(h->pstats, 0, 8 * sizeof(long long), h->st));
+
   {
     // P (row-major k x k on host) -> device, transpose into PT, invert into Q.
     double* tmp = nullptr;
@@ -1258,13 +1277,38 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
   if (need_w && !h->out.wts)
     if (int r = ensure_weights(h)) return r;
   // ---- upload
-  CK(h->ev.upload(h->st));
-  CK(h->steps.upload(h->st));
-  CK(h->sp_rows.upload(h->st));
-  CK(h->sp_vals.upload(h->st));
-  CK(h->nb_ids.upload(h->st));
-  CK(h->nb_w.upload(h->st));
-  CK(h->touched.upload(h->st));
+  {
+    // one pinned staging block and one copy for all descriptor arrays (a
+    // batch of one event costs one H2D call, not seven)
+    size_t off = 0;
+    auto place = [&](size_t bytes) {
+      const size_t o = off;
+      off += (bytes + 15) & ~size_t(15);
+      return o;
+    };
+    const size_t o_ev = place(h->ev.n * sizeof(EventDesc)), o_st = place(h->steps.n * sizeof(StepDesc));
+    const size_t o_sr = place(h->sp_rows.n * 8), o_sv = place(h->sp_vals.n * 8);
+    const size_t o_ni = place(h->nb_ids.n * 8), o_nw = place(h->nb_w.n * 8);
+    const size_t o_tc = place(h->touched.n * 8);
+    CK(h->pack.ensure(off + 16));
+    char* hp = h->pack.h;
+    std::memcpy(hp + o_ev, h->ev.h, h->ev.n * sizeof(EventDesc));
+    std::memcpy(hp + o_st, h->steps.h, h->steps.n * sizeof(StepDesc));
+    std::memcpy(hp + o_sr, h->sp_rows.h, h->sp_rows.n * 8);
+    std::memcpy(hp + o_sv, h->sp_vals.h, h->sp_vals.n * 8);
+    std::memcpy(hp + o_ni, h->nb_ids.h, h->nb_ids.n * 8);
+    std::memcpy(hp + o_nw, h->nb_w.h, h->nb_w.n * 8);
+    std::memcpy(hp + o_tc, h->touched.h, h->touched.n * 8);
+    if (off) CK(cudaMemcpyAsync(h->pack.d, hp, off, cudaMemcpyHostToDevice, h->st));
+    char* dp = h->pack.d;
+    h->d_ev = reinterpret_cast<EventDesc*>(dp + o_ev);
+    h->d_steps = reinterpret_cast<StepDesc*>(dp + o_st);
+    h->d_sp_rows = reinterpret_cast<int64_t*>(dp + o_sr);
+    h->d_sp_vals = reinterpret_cast<double*>(dp + o_sv);
+    h->d_nb_ids = reinterpret_cast<int64_t*>(dp + o_ni);
+    h->d_nb_w = reinterpret_cast<double*>(dp + o_nw);
+    h->d_touched = reinterpret_cast<int64_t*>(dp + o_tc);
+  }
   const bool timing = mode & DAMF_APPLY_TIME_EVENTS;
   if (timing && (size_t)ok_count > h->t_cap) {
     if (h->t_begin) cudaFree(h->t_begin);
@@ -1323,7 +1367,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
       const EventDesc& ed = h->ev.h[e];
       PprArgs pa = ppr_args(h);
       pa.k = h->k;
-      CK(launch_ppr_absorb(pa, h->touched.d + ed.touched_off, (int)ed.touched_cnt, h->st));
+      CK(launch_ppr_absorb(pa, h->d_touched + ed.touched_off, (int)ed.touched_cnt, h->st));
       h->launches += 1;
       if (push_each)
         if (int r = run_push(h, 8 * h->nsm, timing ? h->t_end + e : nullptr)) return r;
@@ -1360,10 +1404,10 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
     // for 8-CTA clusters.
     const bool split = fused && event_cluster_size() == 16;
     // no stop recorded yet for this launch group (the kernels stop at an
-    // event that requests a rebase and skip everything after it)
+    // event that requests a rebase and skip everything after it): the
+    // group's first event kernel clears it before any CTA looks at it
     h->h_ctl->stop_event = -1;
-    CK(cudaMemcpyAsync(&h->ctl->stop_event, &h->h_ctl->stop_event, sizeof(long long),
-                       cudaMemcpyHostToDevice, h->st));
+    ea.reset_stop = 1;
     if (split) {
       // one-event factor kernel, then the push kernel for that event
       ea.fused_ppr = 0;
@@ -1371,6 +1415,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         ea.e_begin = e;
         ea.e_end = e + 1;
         CK(launch_event_kernel(ea, h->st));
+        ea.reset_stop = 0;
         CK(launch_ppr_kernel(ea, h->st));
         h->launches += 2;
       }
@@ -1379,6 +1424,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
       ea.e_end = j;
       ea.fused_ppr = fused ? 1 : 0;
       CK(launch_event_kernel(ea, h->st));
+      ea.reset_stop = 0;
       h->launches += 1;
     } else {
       // whole-GPU push per event (large graphs): the host reads the control
@@ -1389,6 +1435,7 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
         ea.e_begin = e;
         ea.e_end = e + 1;
         CK(launch_event_kernel(ea, h->st));
+        ea.reset_stop = 0;
         h->launches += 1;
         if (int r = sync_ctl(h)) return r;
         if (h->h_ctl->err) break;
@@ -1712,15 +1759,18 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
   // (benign rows) and, above kPreciseCond, the dirty rows (written through
   // P^-1 since the last fold) are recomputed in fp64 and patched in; without
   // a usable dirty list (PPR state, overflow) the whole fold is fp64.
-  // A one-shot query tolerates the fast path's ~sqrt(k) 2^-22 relative error
-  // on typical rows up to a moderate cond(P) (rows in P's small singular
-  // directions lose ~log10(cond) digits); above kPreciseCond every row takes
-  // fp64 products. Side-table rows are always folded from fp64.
-  constexpr double kPreciseCond = 1e4;
+  // Two tiers, as for a rebase but without the cond switch: the rows whose
+  // base values carry cond(P)-sized cancelling components are exactly the
+  // side-table rows (written through P^-1 since the last fold), patched from
+  // their fp64 values with fp64 products; every other row was set by a fold
+  // and is benign for the fast path (~sqrt(k) 2^-22 relative). Without a
+  // usable table (overflow, PPR state Z_b above cond 100, k > 128) every row
+  // takes fp64 products.
+  constexpr double kPreciseCond = 100.0;
   const int side = which == DAMF_Y ? 1 : (which == DAMF_Z && !h->alpha1) ? -1 : 0;
   const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
   const double cond = side == 1 ? h->h_ctl->cond_est_y : h->h_ctl->cond_est;
-  if (cond <= kPreciseCond) {
+  if (cond <= kPreciseCond || (nd >= 0 && nd <= kDirtyCap && h->k <= 128)) {
     CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
   } else {
     CK(launch_materialize_precise(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));

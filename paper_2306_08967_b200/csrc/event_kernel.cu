@@ -2054,9 +2054,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     }
     for (int i = 0; i < 3; ++i) S.gprof[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (A.reset_stop && rank == 0) A.ctl->stop_event = -1;
   }
   __syncthreads();
-  cl.sync();  // counters zeroed before any CTA can append to them
+  cl.sync();  // counters zeroed (and the stop cleared) before any CTA looks at them
   for (int64_t e = A.e_begin; e < A.e_end; ++e) {
     // (split mode launches one event per kernel: an earlier launch of the
     // batch that stopped for a rebase or failed turns this one into a no-op)

@@ -19,6 +19,7 @@ struct EventKernelArgs {
   unsigned long long* t_begin;  // per-event %globaltimer stamps (or null)
   unsigned long long* t_end;
   int mode;                 // DAMF_APPLY_* bits
+  int reset_stop;           // first kernel of a launch group: clear ctl->stop_event
   int64_t* rowlog;          // (step, side 0=X / 1=Y, row) per modified base row, or null
   long long rowlog_cap;     // triples
   // factor state
