@@ -612,7 +612,17 @@ def stream_latencies(eng, ev, batch, max_events):
     rebases = 0
     m = min(len(ev), max_events)
     torch.cuda.synchronize()
-    for a in range(0, m, batch):
+    if batch == 1:
+        # single events through Engine::apply's one-event call
+        for a in range(m):
+            u, v = int(ev.u[a]), int(ev.v[a])
+            t0 = time.perf_counter()
+            st = eng.apply_edge(int(ev.kind[a]), u, v, 1.0, ge.APPLY_TIME_EVENTS)
+            t_wall += time.perf_counter() - t0
+            dev_ms += st.device_ms
+            rebases += st.rebases
+            lat.extend(eng.latencies_us().tolist())
+    for a in range(0, m if batch > 1 else 0, batch):
         part = ev.slice(a, min(m, a + batch))
         t0 = time.perf_counter()
         st = eng.apply(part, mode=ge.APPLY_TIME_EVENTS)

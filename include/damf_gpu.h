@@ -199,6 +199,13 @@ int damf_gpu_sync(damf_gpu* h);
 int damf_gpu_apply(damf_gpu* h, const damf_event_batch* batch, int32_t mode,
                    damf_apply_stats* stats);
 
+/* Engine::apply(GraphEvent::add_edge(u, v, w)) / remove_edge(u, v)
+ * (engine.cpp:22-41, graph.hpp:14-47) for ONE edge event, without building
+ * a damf_event_batch: kind = DAMF_ADD_EDGE or DAMF_REMOVE_EDGE (w ignored for
+ * removals). Same semantics and errors as a batch of one. */
+int damf_gpu_apply_edge(damf_gpu* h, int32_t kind, int64_t u, int64_t v, double w, int32_t mode,
+                        damf_apply_stats* stats);
+
 /* Batched scoring. flags: DAMF_SCORE_ENHANCED scores
  * <Z[u], Y[v]> instead of <X[u], Y[v]> (Engine::score, engine.cpp:49-52);
  * DAMF_SCORE_SYMMETRIC_MAX takes max(s(u,v), s(v,u)) as pair_score does for

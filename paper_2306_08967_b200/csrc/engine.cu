@@ -1552,6 +1552,17 @@ int damf_gpu_apply(damf_gpu* h, const damf_event_batch* b, int32_t mode, damf_ap
   return status;
 }
 
+int damf_gpu_apply_edge(damf_gpu* h, int32_t kind, int64_t u, int64_t v, double w, int32_t mode,
+                        damf_apply_stats* stats) {
+  damf_event_batch b{};
+  b.count = 1;
+  b.kind = &kind;
+  b.u = &u;
+  b.v = &v;
+  b.w = &w;
+  return damf_gpu_apply(h, &b, mode, stats);
+}
+
 int64_t damf_gpu_row_log(damf_gpu* h, int64_t* out, int64_t max) {
   const int64_t m = (int64_t)h->rowlog_h.size() / 3;
   for (int64_t i = 0; i < 3 * std::min(m, max); ++i) out[i] = h->rowlog_h[i];

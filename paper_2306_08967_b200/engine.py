@@ -55,9 +55,10 @@ class Csr(C.Structure):
 
 
 class EventBatch(C.Structure):
-    _fields_ = [("count", C.c_int64), ("kind", i32p), ("u", i64p), ("v", i64p), ("w", f64p),
-                ("in_off", i64p), ("in_ids", i64p), ("in_w", f64p), ("out_off", i64p),
-                ("out_ids", i64p), ("out_w", f64p)]
+    # pointer fields as void*: set from integer addresses (cheaper per call
+    # than typed ctypes pointers)
+    _fields_ = [("count", C.c_int64)] + [(f, C.c_void_p) for f in (
+        "kind", "u", "v", "w", "in_off", "in_ids", "in_w", "out_off", "out_ids", "out_w")]
 
 
 class ApplyStats(C.Structure):
@@ -98,6 +99,8 @@ def lib():
         L.damf_gpu_destroy.argtypes = [vp]
         L.damf_gpu_sync.argtypes = [vp]
         L.damf_gpu_apply.argtypes = [vp, C.POINTER(EventBatch), C.c_int32, C.POINTER(ApplyStats)]
+        L.damf_gpu_apply_edge.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, C.c_double, C.c_int32,
+                                          C.POINTER(ApplyStats)]
         L.damf_gpu_event_latencies.argtypes = [vp, f64p, C.c_int64]
         L.damf_gpu_event_latencies.restype = C.c_int64
         L.damf_gpu_row_log.argtypes = [vp, i64p, C.c_int64]
@@ -132,21 +135,16 @@ def _p(a, t):
     return a.ctypes.data_as(t) if a is not None else None
 
 
+_BATCH_FIELDS = (("kind", np.int32), ("u", np.int64), ("v", np.int64), ("w", np.float64),
+                 ("in_off", np.int64), ("in_ids", np.int64), ("in_w", np.float64),
+                 ("out_off", np.int64), ("out_ids", np.int64), ("out_w", np.float64))
+
+
 def make_batch(ev):
     """Build a damf_event_batch from an object with kind/u/v/w/in_*/out_* arrays."""
-    arrs = dict(kind=np.ascontiguousarray(ev.kind, np.int32),
-                u=np.ascontiguousarray(ev.u, np.int64), v=np.ascontiguousarray(ev.v, np.int64),
-                w=np.ascontiguousarray(ev.w, np.float64),
-                in_off=np.ascontiguousarray(ev.in_off, np.int64),
-                in_ids=np.ascontiguousarray(ev.in_ids, np.int64),
-                in_w=np.ascontiguousarray(ev.in_w, np.float64),
-                out_off=np.ascontiguousarray(ev.out_off, np.int64),
-                out_ids=np.ascontiguousarray(ev.out_ids, np.int64),
-                out_w=np.ascontiguousarray(ev.out_w, np.float64))
-    b = EventBatch(len(arrs["kind"]), _p(arrs["kind"], i32p), _p(arrs["u"], i64p),
-                   _p(arrs["v"], i64p), _p(arrs["w"], f64p), _p(arrs["in_off"], i64p),
-                   _p(arrs["in_ids"], i64p), _p(arrs["in_w"], f64p), _p(arrs["out_off"], i64p),
-                   _p(arrs["out_ids"], i64p), _p(arrs["out_w"], f64p))
+    arrs = {f: np.ascontiguousarray(getattr(ev, f), t) for f, t in _BATCH_FIELDS}
+    b = EventBatch(len(arrs["kind"]), *(arrs[f].__array_interface__["data"][0]
+                                        for f, _ in _BATCH_FIELDS))
     return b, arrs  # keep arrs alive while b is used
 
 
@@ -260,6 +258,14 @@ class Engine:
         del keep
         self._check(st, s.failed_index)
         return s.as_dict()
+
+    def apply_edge(self, kind, u, v, w=1.0, mode=0):
+        """Engine::apply(GraphEvent::add_edge(u, v, w) / remove_edge(u, v)) for
+        one event (damf_gpu_apply_edge): no batch arrays to marshal."""
+        s = ApplyStats()
+        st = lib().damf_gpu_apply_edge(self.h, kind, u, v, w, mode, C.byref(s))
+        self._check(st, s.failed_index)
+        return s
 
     def latencies_us(self):
         n = lib().damf_gpu_event_latencies(self.h, None, 0)
