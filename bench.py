@@ -262,8 +262,10 @@ def cfg5_materialize(eng, n, d, hbm, peak_kind):
     return {"kernel": "materialize_tc128 (X = X_b P_X, n = 67,108,864, d = 128, 3 x TF32)",
             "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(gbs / hbm, 4),
-            "traffic": ncu_traffic("r2_mat_cfg5_raw.csv", "materialize_tc128"),
-            "traffic_source": "profiles/r2_mat_cfg5_raw.csv (ncu --set full, same launch)",
+            "traffic": ncu_metric_traffic("r2_mat_cfg5_launches.csv", "materialize_tc128"),
+            "traffic_source": "profiles/r2_mat_cfg5_launches.csv (ncu --metrics dram__bytes_read.sum,"
+                              "dram__bytes_write.sum on the same kernel at the same shape, "
+                              "tools/prof_r2.py mat5)",
             "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(bytes_),
             "launch_ms": round(t, 4), "launch_ms_all": [round(x, 4) for x in ms]}
 
@@ -411,6 +413,32 @@ def ncu_traffic(fname, kernel_substr):
             tot += float(row[i].replace(",", "")) * scale.get(units[i], 1.0)
         return int(tot)
     return None
+
+
+def ncu_metric_traffic(fname, kernel_substr):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the first launch of
+    `kernel_substr` in a committed `ncu --metrics ... --csv` launch list
+    (one row per metric) under profiles/, or None."""
+    import csv
+    path = os.path.join(ROOT, "profiles", fname)
+    if not os.path.exists(path):
+        return None
+    lines = [l for l in open(path) if l.startswith('"')]
+    rows = list(csv.reader(lines))
+    head = rows[0]
+    tot, seen = 0.0, None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows[1:]:
+        rec = dict(zip(head, r))
+        if kernel_substr not in rec["Kernel Name"]:
+            continue
+        if seen is None:
+            seen = rec["ID"]
+        if rec["ID"] != seen:
+            break
+        if rec["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(rec["Metric Value"].replace(",", "")) * scale.get(rec["Metric Unit"], 1.0)
+    return int(tot) if seen is not None else None
 
 
 def bench_cfg2(args):

@@ -1,7 +1,8 @@
 """Dev driver for ncu captures (round 2): one hot kernel family per mode.
   cfg5ev  : config-5-like state (R-MAT scale 20, orthonormal U/V,
-            sigma_i = i^-1/2, d = 128), 40 warm-up insertions, then one
-            damf_event_kernel<16,0> launch over 50 insertions
+            sigma_i = i^-1/2, d = 128), then one
+            damf_event_kernel<16,0> launch over 50 insertions after 200 (past the
+            rebase transient)
   cfg2ev  : config-2 stream, split mode: 20 events = 20 damf_event_kernel<16,0>
             + 20 damf_ppr_kernel<16> launches after 200 warm-up events
   mat5    : Z = X F at the config-5 shape (n = 2^26, d = 128)"""
@@ -18,10 +19,12 @@ from paper_2306_08967_b200 import workloads as W
 mode = sys.argv[1]
 if mode == "cfg5ev":
     from test_gpu_configs import cfg5_like
-    e, su, sv = cfg5_like(20, 128, 90, seed=4)
-    e.apply(W.EventList.edges(1, su[:40], sv[:40]))
+    e, su, sv = cfg5_like(20, 128, 250, seed=4)
+    st = e.apply(W.EventList.edges(1, su[:200], sv[:200]))  # past the rebase transient
     torch.cuda.synchronize()
-    print(e.apply(W.EventList.edges(1, su[40:90], sv[40:90])))
+    # one event-kernel launch per launch group: a rebase ends a group
+    print("event-kernel launches before the captured one:", st["rebases"] + 1)
+    print(e.apply(W.EventList.edges(1, su[200:250], sv[200:250])))
 elif mode == "cfg2ev":
     w = W.cfg2()
     off, tgt = W.undirected_csr(w["n"], *w["init"])
