@@ -2187,6 +2187,19 @@ int damf_gpu_ppr_trace(damf_gpu* h, int64_t* out, int cap) {
   return r;
 }
 
+// Dev (DAMF_PROF builds): the slow-secular-root dump kept in the d > 128
+// workspace: 8 header doubles, then up to 8 records of 600 doubles.
+int damf_gpu_debug_dump(damf_gpu* h, double* out, int64_t count) {
+  double* src = h->ws + (size_t)h->ld * h->ld;
+  if (count < 0) {  // reset
+    CK(cudaMemset(src, 0, 16));
+    return 0;
+  }
+  const int64_t m = std::min<int64_t>(count, 8 + 8 * 800);
+  CK(cudaMemcpy(out, src, m * 8, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int damf_gpu_profile_counters(damf_gpu* h, uint64_t* out16) {
   if (int r = sync_ctl(h)) return r;
   for (int i = 0; i < 32; ++i) out16[i] = h->h_ctl->prof[i];

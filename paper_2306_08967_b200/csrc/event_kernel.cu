@@ -586,6 +586,21 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
       g = Aq < 0.0 ? 2.0 * Bq / (Aq - sq) : -(Aq + sq) / (2.0 * C);
     }
     if (g > lo && g < hi) tau = g;
+  } else if (K >= 2) {
+    // last root: the two-pole model at poles K-2 and K-1 with the other
+    // terms frozen at tau = 0, i.e. the positive root of
+    // C t^2 - (C dl + a + b) t + b dl = 0 (dl = d_{K-2} - d_{K-1} < 0); kept
+    // only when it falls inside the bracket (C > 0)
+    double sm = 0;
+    for (int i = gl; i < K - 2; i += 16) sm += kz2[i] / (kd[i] - kd[K - 1]);
+    sm = gsum(sm, gm);
+    const double C = 1.0 / rho + sm, dl = kd[K - 2] - kd[K - 1], a = kz2[K - 2], b = kz2[K - 1];
+    if (C > 0.0) {
+      const double Bm = C * dl + a + b;
+      const double sq = sqrt(fmax(Bm * Bm - 4.0 * C * b * dl, 0.0));
+      const double g = Bm > 0.0 ? (Bm + sq) / (2.0 * C) : (2.0 * b * dl) / (Bm - sq);
+      if (g > lo && g < hi) tau = g;
+    }
   }
   int it = 0;
   for (; it < 120; ++it) {
@@ -633,14 +648,24 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
         }
       }
     } else {
-      const double q1 = dpsi * D1 * D1;
-      const double c = 1.0 + psi - dpsi * D1 + phi;
-      if (c > 0.0) {
-        nt = tau + D1 + q1 / c;
+      // last root: Newton on 1/P with P = 1 - f = -(psi + phi) > 0 -- exact
+      // for a single pole at any position, so it also converges fast when the
+      // weight sits in a cluster of poles below the last one (the cfg-5
+      // spectrum after many unit insertions), where a model anchored at the
+      // last pole creeps in linearly
+      const double P = -(psi + phi), dP = dpsi + dphi;
+      if (P > 0.0 && dP > 0.0) {
+        nt = tau + (P * P - P) / dP;
         ok = true;
       }
     }
-    if (!ok || !(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
+    if (!ok || !(nt > lo && nt < hi)) {
+      // safeguard: bisect, geometrically when the bracket spans many decades
+      // of distance from the origin pole (a root hugging it), else in value
+      const bool pos = hi > 0.0;
+      const double a = fmax(pos ? lo : -hi, 4.0 * EPS * fmax(fabs(dorg), 1e-300)), b = pos ? hi : -lo;
+      nt = b > 1e9 * a ? (pos ? sqrt(a * b) : -sqrt(a * b)) : 0.5 * (lo + hi);
+    }
     if (nt == tau || hi - lo <= 2.0 * EPS * fmax(fabs(lo), fabs(hi))) {
       tau = nt;
       break;
@@ -661,7 +686,7 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
 template <int C>
 DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const double* z,
                       double rho, int n, int elo, int ehi, double* QT, int ldq, int row_off,
-                      double* lamOut, unsigned long long* A_prof) {
+                      double* lamOut, unsigned long long* A_prof, double* S_dump = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cl.block_rank();
   const bool neg = rho < 0.0;
@@ -757,6 +782,24 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   __syncthreads();
   EPROF(16);
   const int K = S.K;
+#if DAMF_PROF
+  // dev: dump the first 8 deflated secular problems after a reset
+  // (damf_gpu_debug_dump with count < 0): K, rho, sum z^2, kd[K], kz2[K]
+  if (S_dump != nullptr) {
+    if (rank == 0 && threadIdx.x == 0) {
+      const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(S_dump), 1ull);
+      S_dump[1] = slot < 8 ? (double)(slot + 1) : 0.0;
+      if (slot < 8) {
+        double* o = S_dump + 8 + slot * 800;
+        o[0] = K; o[1] = rhoN;
+        double z2 = 0;
+        for (int i = 0; i < K; ++i) { o[8 + i] = S.kd[i]; o[8 + 260 + i] = S.kz2[i]; z2 += S.kz2[i]; }
+        o[2] = z2;
+      }
+    }
+    cl.sync();
+  }
+#endif
   double sz2 = 0;
   for (int j = tid; j < K; j += NT) sz2 += S.kz2[j];
   sz2 = block_sum(S, sz2);
@@ -770,9 +813,21 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
     double t;
     int o;
     const int its = secular_root(S.kd, S.kz2, K, rhoN, sz2, j, t, o);
+#if DAMF_PROF
+    const int o_ = o;
+#endif
     if (DAMF_PROF && gl == 0 && rank == 0) atomicAdd(&A_prof[13], (unsigned long long)its);
     if (DAMF_PROF && gl == 0 && rank == 0) atomicAdd(&A_prof[14], 1ull);
     if (DAMF_PROF && gl == 0) atomicMax(&A_prof[15], (unsigned long long)its);
+    if (DAMF_PROF && gl == 0 && its >= 10) atomicAdd(&A_prof[31], 1ull);
+#if DAMF_PROF
+    // dev: record the iteration count of every root of the dumped problems
+    if (gl == 0 && S_dump != nullptr) {
+      const long long slot = (long long)S_dump[1] - 1;  // this eigensolve's record (set below)
+      if (slot >= 0 && slot < 8) S_dump[8 + slot * 800 + 530 + j] = its;
+    }
+    (void)o_;
+#endif
     if (gl < C) {
       *cl.map_shared_rank(S.tau + j, gl) = t;
       *cl.map_shared_rank(S.org + j, gl) = o;
@@ -1193,7 +1248,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   PROF_MARK(1);
   // ---- 3. eigen step A: D^2 + rho z z^T -> Q1^T rows (L2, shared) ---------
   eig_rank1<C>(S, cl, S.dd, S.zz, edge ? lp : 1.0, n, olo, ohi, A.ws_Q1T, ld, 0, S.lamA,
-               A.ctl->prof);
+               A.ctl->prof, DAMF_PROF && d <= 128 ? A.ws_priv : nullptr);
   PROF_MARK(2);
   if (edge) {
     // z2 = Q1^T u_minus for this CTA's columns, broadcast
@@ -1208,7 +1263,8 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   PROF_MARK(3);
   if (edge) {
     // ---- eigen step B: Lambda1 + lm z2 z2^T -> Q2^T rows (private) ---------
-    eig_rank1<C>(S, cl, S.lamA, S.zz, lm, n, olo, ohi, PB[0], pld, olo, S.lamB, A.ctl->prof);
+    eig_rank1<C>(S, cl, S.lamA, S.zz, lm, n, olo, ohi, PB[0], pld, olo, S.lamB, A.ctl->prof,
+                 DAMF_PROF && d <= 128 ? A.ws_priv : nullptr);
     PROF_MARK(4);
     // E columns t (rows of E^T, private): E^T[t] = sum_e Q2^T[t][e] Q1^T[e]
     {
