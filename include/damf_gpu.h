@@ -298,7 +298,8 @@ void* damf_gpu_stream(damf_gpu* h);
 int damf_gpu_push_counters(damf_gpu* h, int64_t* out4);
 
 /* Developer profiling: cumulative SM cycles per phase of the per-event
- * kernel (cluster rank 0), 32 slots (see event_kernel.cu PROF_MARK). */
+ * kernel, 128 slots (see event_kernel.cu PROF_MARK; nonzero only in
+ * -DDAMF_PROF=1 builds). */
 int damf_gpu_profile_counters(damf_gpu* h, uint64_t* out16);
 
 /* Development: per-round trace of the last whole-GPU push, 4 int64 per round

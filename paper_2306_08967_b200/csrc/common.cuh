@@ -33,7 +33,7 @@ struct DevCtl {
   long long dirty_n[2];               // rows of X_b / Y_b written through P^-1 since the last fold
   long long rowlog_n;                 // entries in the modified-row log (DAMF_APPLY_LOG_ROWS)
   long long ppr_skip;                 // event whose PPR absorb / push waits for a rebase (-1: none)
-  unsigned long long prof[32];        // per-phase SM cycles (rank 0), dev profiling
+  unsigned long long prof[128];       // per-phase SM cycles, dev profiling (DAMF_PROF builds)
 };
 
 // Slack-per-row CSR (K9): row u occupies ids[off[u] .. off[u]+cnt[u]) inside a

@@ -2202,7 +2202,7 @@ int damf_gpu_debug_dump(damf_gpu* h, double* out, int64_t count) {
 
 int damf_gpu_profile_counters(damf_gpu* h, uint64_t* out16) {
   if (int r = sync_ctl(h)) return r;
-  for (int i = 0; i < 32; ++i) out16[i] = h->h_ctl->prof[i];
+  for (int i = 0; i < 128; ++i) out16[i] = h->h_ctl->prof[i];
   return 0;
 }
 

@@ -62,6 +62,14 @@ constexpr int PLD = 132;           // private-matrix row stride (d <= 128 in sme
 constexpr int PCAP = 2048;         // fused-PPR candidate list entries kept in shared memory
 constexpr int GBUF_D = 4224;       // GEMM staging slot: 32 rows x 132 doubles (33 KB)
 
+// One row GEMM of a staged call: Out[o0 + r][:] = Coef[r][:] In (see rows_gemm_staged).
+struct GemmJob {
+  double* Out;
+  const double* Coef;
+  const double* In;
+  double* fro;
+};
+
 template <int C>
 struct Smem {
   static constexpr int PROWS = (128 + C - 1) / C + 1;  // owned rows (+ the discarded one)
@@ -73,13 +81,16 @@ struct Smem {
   double tau[NPAD], zhat[NPAD], lamA[NPAD], lamB[NPAD];
   double s2[NPAD], exv[NPAD], eyv[NPAD], dH[NPAD], dE[NPAD];
   double cH[NPAD], cE[NPAD], yA1[NPAD], yB1[NPAD];  // dropped columns of H / E (top k)
+  // sqrt(sigma_i), 1/sqrt(sigma_i) of the old spectrum and sqrt(s_t), 1/sqrt(s_t)
+  // of the new one, computed once per step (every closed form scales by them;
+  // an IEEE sqrt / division is ~100-130 dependent cycles on this chip)
+  double rsig[NPAD], irsig[NPAD], rs2[NPAD], irs2[NPAD];
   int rot_p[NPAD], rot_q[NPAD];
   double rot_c[NPAD], rot_s[NPAD];
   double partL[2][kMaxD];         // this CTA's partial column sums
   double partS[4];                // this CTA's partial scalars
   double pnorm[C][4];
   double priv[4][PROWS * PLD];    // owned rows of Q2T/F, E/G^-1, H/F^-1, G
-  double vscr[NW][NPAD];          // per-warp eigenvector scratch (rare deflation path)
   double bred[NW];
   long long found[C][2];          // graph row-scan results
   int lcnt3[3];                   // fused PPR: rows in this CTA's candidate lists (round mod 3)
@@ -89,13 +100,16 @@ struct Smem {
   union alignas(16) {
     int plist[3][PCAP];           // fused PPR: candidate lists (round mod 3); overflow in global
     double gbuf[2][GBUF_D];       // GEMM operand staging: two slots of chunk rows x ld doubles
+    double vscr[NW][NPAD];        // per-warp row scratch (deflation rotations, eager folds)
   };
   int K, nrot, need;
   int k, pp[2];
   int err;
   unsigned long long gbar[2];     // GEMM staging: bulk-copy completion per slot
   unsigned gq[2];                 // completed phases per slot
-  long long gprof[3];             // DAMF_PROF: staged-GEMM wait / DMMA / barrier cycles
+  GemmJob gjobs[4];               // the staged GEMM's job list (uniform reads from shared memory)
+  double gfro[4];                 // ... and its Frobenius norms
+  long long gprof[8];             // DAMF_PROF: staged-GEMM wait / DMMA / call / prologue / bar / issue / epilogue / tail
 };
 static_assert(sizeof(Smem<16>) <= 232448, "event kernel shared memory above the 227 KB opt-in limit");
 
@@ -264,12 +278,7 @@ DAMF_D void rows_gemm(Smem<C>& S, double* Out, int ldo, int o0, const double* Co
 // copy of the next chunk -- also across GEMMs -- overlaps the DMMAs of this
 // one and each GEMM pays one L2 latency instead of one per K-chunk per warp.
 // nt <= 8 * MT rows, J <= 64 * TPW columns (8 warps x TPW 8-column tiles).
-struct GemmJob {
-  double* Out;
-  const double* Coef;
-  const double* In;
-  double* fro;
-};
+
 DAMF_D unsigned ctarank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -297,8 +306,13 @@ DAMF_D void stage_chunk(Smem<C>& S, int slot, const double* src, unsigned bytes)
 // KF > 0: shapes fixed at compile time (M = J = KF, ldi = ldc = KF + 4, the
 // k = 128 update GEMMs), so the chunk loops unroll without predicates.
 template <int C, int MT, int TPW, int KF>
-__device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0,
-                                              int ldc_, int nt, int ldi_, int M_, int J_) {
+__device__ __noinline__ void rows_gemm_staged(int nj, int ldo, int o0, int ldc_, int nt, int ldi_,
+                                              int M_, int J_) {
+  // the block's shared window, re-derived here so that its accesses compile to
+  // LDS / STS (a reference parameter of a non-inlined function is generic)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<C>& S = *reinterpret_cast<Smem<C>*>(smem_raw);
+  const GemmJob* jobs = S.gjobs;
   const int ldc = KF ? KF + 4 : ldc_, ldi = KF ? KF + 4 : ldi_, M = KF ? KF : M_, J = KF ? KF : J_;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ar = lane >> 2, ac = lane & 3;
@@ -323,6 +337,9 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
     issue(0);
     if (T > 1) issue(1);
   }
+#if DAMF_PROF
+  if (threadIdx.x == 0 && ctarank() == 0) S.gprof[3] += clock64() - _gs;
+#endif
   int bc[TPW];
   bool bok[TPW];
 #pragma unroll
@@ -355,7 +372,11 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
     if (threadIdx.x == 0 && ctarank() == 0) S.gprof[0] += _g1 - _g0;
 #endif
     const double* sb = S.gbuf[slot];
-    const double* Coef = jobs[j].Coef;
+    // KF: the coefficient rows are this CTA's private rows in shared memory
+    const double* Coef = KF ? reinterpret_cast<const double*>(
+                                  smem_raw + (reinterpret_cast<const unsigned char*>(jobs[j].Coef) -
+                                              reinterpret_cast<const unsigned char*>(&S)))
+                            : jobs[j].Coef;
     const int m0 = c * CR, rows = (KF && KF % CR == 0) ? CR : min(CR, M - m0);
     for (int mm = 0; mm < rows; mm += 16) {
       // operands of four k-steps loaded before their DMMAs
@@ -384,8 +405,16 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
     if (threadIdx.x == 0 && ctarank() == 0) S.gprof[1] += _g2 - _g1;
 #endif
     __syncthreads();  // every warp is done with this slot
+#if DAMF_PROF
+    long long _g3 = clock64();
+    if (threadIdx.x == 0 && ctarank() == 0) S.gprof[4] += _g3 - _g2;
+#endif
 
     if (threadIdx.x == 0 && t + 2 < T) issue(t + 2);
+#if DAMF_PROF
+    long long _g4 = clock64();
+    if (threadIdx.x == 0 && ctarank() == 0) S.gprof[5] += _g4 - _g3;
+#endif
     if (c == nch - 1) {
       double* Out = jobs[j].Out;
 #pragma unroll
@@ -408,9 +437,15 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
           }
         }
       }
-      if (jobs[j].fro) *jobs[j].fro = block_sum(S, frob);
+      if (jobs[j].fro) S.gfro[j] = block_sum(S, frob);
     }
+#if DAMF_PROF
+    if (threadIdx.x == 0 && ctarank() == 0) S.gprof[6] += clock64() - _g4;
+#endif
   }
+#if DAMF_PROF
+  const long long _g5 = clock64();
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {
     S.gq[0] = q0 + (unsigned)((T + 1) >> 1);
@@ -418,7 +453,10 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
   }
   __syncthreads();
 #if DAMF_PROF
-  if (threadIdx.x == 0 && ctarank() == 0) S.gprof[2] += clock64() - _gs;
+  if (threadIdx.x == 0 && ctarank() == 0) {
+    S.gprof[2] += clock64() - _gs;
+    S.gprof[7] += clock64() - _g5;
+  }
 #endif
 }
 
@@ -426,17 +464,25 @@ __device__ __noinline__ void rows_gemm_staged(Smem<C>& S, const GemmJob* jobs, i
 template <int C>
 DAMF_D void rows_gemms(Smem<C>& S, const GemmJob* jobs, int nj, int ldo, int o0, int ldc, int nt,
                        int ldi, int M, int J) {
-  if (nt <= 8 && M == 128 && J == 128 && ldi == 132 && ldc == 132)
-    rows_gemm_staged<C, 1, 2, 128>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
-  else if (nt <= 8 && J <= 128)
-    rows_gemm_staged<C, 1, 2, 0>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
-  else if (nt <= 16 && J <= 128)
-    rows_gemm_staged<C, 2, 2, 0>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
-  else if (nt <= 16 && J <= 256)
-    rows_gemm_staged<C, 2, 4, 0>(S, jobs, nj, ldo, o0, ldc, nt, ldi, M, J);
-  else
+  if (nt > 16 || J > 256) {
     for (int j = 0; j < nj; ++j)
       rows_gemm<C>(S, jobs[j].Out, ldo, o0, jobs[j].Coef, ldc, nt, jobs[j].In, ldi, M, J, jobs[j].fro);
+    return;
+  }
+  if (threadIdx.x < nj) S.gjobs[threadIdx.x] = jobs[threadIdx.x];
+  __syncthreads();
+  if (nt <= 8 && M == 128 && J == 128 && ldi == 132 && ldc == 132 &&
+      jobs[0].Coef >= &S.priv[0][0] && jobs[0].Coef < &S.priv[4][0])
+    rows_gemm_staged<C, 1, 2, 128>(nj, ldo, o0, ldc, nt, ldi, M, J);
+  else if (nt <= 8 && J <= 128)
+    rows_gemm_staged<C, 1, 2, 0>(nj, ldo, o0, ldc, nt, ldi, M, J);
+  else if (nt <= 16 && J <= 128)
+    rows_gemm_staged<C, 2, 2, 0>(nj, ldo, o0, ldc, nt, ldi, M, J);
+  else
+    rows_gemm_staged<C, 2, 4, 0>(nj, ldo, o0, ldc, nt, ldi, M, J);
+  // (the staged call ends with a block barrier: gfro is complete)
+  for (int j = 0; j < nj; ++j)
+    if (jobs[j].fro) *jobs[j].fro = S.gfro[j];
 }
 
 // ---------------------------------------------- exact inverse (one CTA)
@@ -535,20 +581,117 @@ DAMF_D bool gj_inverse_cta(const double* PT, double* Q, int k, int ld, double* p
 }
 
 // ------------------------------------------------------------ secular solver
+// Branch-free reciprocal: MUFU.RCP64H seed (about 20 bits) and two Newton
+// steps, ~1 ulp. The IEEE division nvcc emits carries a slow-path branch per
+// call, which serialises the divisions of a secular pass (one per pole per
+// lane, each ~150 cycles of dependent latency); these interleave. The seed
+// flushes subnormal inputs to zero, so callers re-run a pass with IEEE
+// divisions when its result is not finite (never seen outside tests).
+DAMF_D double frcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  return r;
+}
+
+// One pass of the secular sums at lambda = dorg + tau over the K poles, by a
+// 16-lane group (4 poles per lane in flight): psi = sum_{i<=j} z_i^2 / (d_i -
+// lambda), phi = sum_{i>j}, and the derivative sums (all before the rho factor).
+template <bool FAST>
+DAMF_D void secular_pass(const double* kd, const double* kz2, int K, double dorg, double tau, int j,
+                         int gl, unsigned gm, double& psi, double& phi, double& dpsi, double& dphi) {
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  int i = gl;
+  for (; i + 48 < K; i += 64) {
+    double r[4], z[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double den = (kd[i + 16 * u] - dorg) - tau;
+      z[u] = kz2[i + 16 * u];
+      r[u] = FAST ? frcp(den) : 1.0 / den;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double t = z[u] * r[u], dt = t * r[u];
+      const bool left = i + 16 * u <= j;
+      a0 += left ? t : 0.0;
+      a1 += left ? 0.0 : t;
+      a2 += left ? dt : 0.0;
+      a3 += left ? 0.0 : dt;
+    }
+  }
+  {
+    // tail: up to 4 more poles per lane, the same way with a guard
+    double r[4], z[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int ii = i + 16 * u;
+      const bool in = ii < K;
+      const double den = in ? (kd[ii] - dorg) - tau : 1.0;
+      z[u] = in ? kz2[ii] : 0.0;
+      r[u] = FAST ? frcp(den) : 1.0 / den;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double t = z[u] * r[u], dt = t * r[u];
+      const bool left = i + 16 * u <= j;
+      a0 += left ? t : 0.0;
+      a1 += left ? 0.0 : t;
+      a2 += left ? dt : 0.0;
+      a3 += left ? 0.0 : dt;
+    }
+  }
+  // four butterflies interleaved (independent shuffle chains)
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    const double b0 = __shfl_xor_sync(gm, a0, o, 16), b1 = __shfl_xor_sync(gm, a1, o, 16);
+    const double b2 = __shfl_xor_sync(gm, a2, o, 16), b3 = __shfl_xor_sync(gm, a3, o, 16);
+    a0 += b0;
+    a1 += b1;
+    a2 += b2;
+    a3 += b3;
+  }
+  psi = a0;
+  phi = a1;
+  dpsi = a2;
+  dphi = a3;
+}
+
+// The IEEE-division fallback, out of line (cold).
+__device__ __noinline__ void secular_pass_ieee(const double* kd, const double* kz2, int K, double dorg,
+                                               double tau, int j, int gl, unsigned gm, double& psi,
+                                               double& phi, double& dpsi, double& dphi) {
+  secular_pass<false>(kd, kz2, K, dorg, tau, j, gl, gm, psi, phi, dpsi, dphi);
+}
+
 // Root j of 1 + rho * sum_i kz2[i] / (kd[i] - lambda) = 0 (kd ascending,
-// rho > 0, sum kz2 <= 1), one warp. Returns tau and the origin pole o with
-// lambda = kd[o] + tau, so lambda - kd[i] is formed as tau - (kd[i]-kd[o]).
+// rho > 0, sum kz2 <= 1), one 16-lane group. Returns tau and the origin pole
+// o with lambda = kd[o] + tau, so lambda - kd[i] is formed as
+// tau - (kd[i]-kd[o]).
 DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, double sumz2,
                         int j, double& tau_out, int& org_out) {
   const int gl = threadIdx.x & 15;
   const unsigned gm = 0xFFFFu << (threadIdx.x & 16);
   int o;
   double lo, hi;
+  double tau;
   if (j < K - 1) {
-    const double mid = 0.5 * (kd[j + 1] - kd[j]);
-    double s = 0;
-    for (int i = gl; i < K; i += 16) s += kz2[i] / ((kd[i] - kd[j]) - mid);
-    s = gsum(s, gm);
+    // f at the midpoint of (d_j, d_j+1) picks the origin pole; the same sum
+    // gives LAPACK dlaed4's initial guess: the two nearest poles exact, the
+    // other terms frozen at the midpoint (C), i.e. the root of
+    // C + z_j^2/(d_j - l) + z_{j+1}^2/(d_{j+1} - l) = 0 (a quadratic); keeps
+    // the slow roots (tiny z, root hugging a pole) from starting at the midpoint
+    const double del = kd[j + 1] - kd[j], mid = 0.5 * del;
+    double ps, ph, d1, d2;
+    secular_pass<true>(kd, kz2, K, kd[j], mid, j, gl, gm, ps, ph, d1, d2);
+    double s = ps + ph;
+    if (!isfinite(s)) {
+      secular_pass_ieee(kd, kz2, K, kd[j], mid, j, gl, gm, ps, ph, d1, d2);
+      s = ps + ph;
+    }
     if (1.0 + rho * s >= 0.0) {
       o = j;
       lo = 0.0;
@@ -558,23 +701,8 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
       lo = -mid;
       hi = 0.0;
     }
-  } else {
-    o = j;
-    lo = 0.0;
-    hi = rho * sumz2 * (1.0 + 4.0 * EPS);
-  }
-  const double dorg = kd[o];
-  double tau = 0.5 * (lo + hi);
-  if (j < K - 1) {
-    // initial guess as in LAPACK dlaed4: the two nearest poles exact, the
-    // other terms frozen at the midpoint (C), i.e. the root of
-    // C + z_j^2/(d_j - l) + z_{j+1}^2/(d_{j+1} - l) = 0 (a quadratic); keeps
-    // the slow roots (tiny z, root hugging a pole) from starting at the midpoint
-    const double del = kd[j + 1] - kd[j], mid = 0.5 * del;
-    double sm = 0;  // sum at the midpoint over all terms (recomputed, cheap)
-    for (int i = gl; i < K; i += 16) sm += kz2[i] / ((kd[i] - kd[j]) - mid);
-    sm = gsum(sm, gm);
-    const double C = 1.0 / rho + sm + kz2[j] / mid - kz2[j + 1] / mid;
+    tau = 0.5 * (lo + hi);
+    const double C = 1.0 / rho + s + kz2[j] / mid - kz2[j + 1] / mid;
     double g;
     if (o == j) {
       const double Aq = C * del + kz2[j] + kz2[j + 1], Bq = kz2[j] * del;
@@ -586,43 +714,42 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
       g = Aq < 0.0 ? 2.0 * Bq / (Aq - sq) : -(Aq + sq) / (2.0 * C);
     }
     if (g > lo && g < hi) tau = g;
-  } else if (K >= 2) {
-    // last root: the two-pole model at poles K-2 and K-1 with the other
-    // terms frozen at tau = 0, i.e. the positive root of
-    // C t^2 - (C dl + a + b) t + b dl = 0 (dl = d_{K-2} - d_{K-1} < 0); kept
-    // only when it falls inside the bracket (C > 0)
-    double sm = 0;
-    for (int i = gl; i < K - 2; i += 16) sm += kz2[i] / (kd[i] - kd[K - 1]);
-    sm = gsum(sm, gm);
-    const double C = 1.0 / rho + sm, dl = kd[K - 2] - kd[K - 1], a = kz2[K - 2], b = kz2[K - 1];
-    if (C > 0.0) {
-      const double Bm = C * dl + a + b;
-      const double sq = sqrt(fmax(Bm * Bm - 4.0 * C * b * dl, 0.0));
-      const double g = Bm > 0.0 ? (Bm + sq) / (2.0 * C) : (2.0 * b * dl) / (Bm - sq);
-      if (g > lo && g < hi) tau = g;
+  } else {
+    o = j;
+    lo = 0.0;
+    hi = rho * sumz2 * (1.0 + 4.0 * EPS);
+    tau = 0.5 * (lo + hi);
+    if (K >= 2) {
+      // last root: the two-pole model at poles K-2 and K-1 with the other
+      // terms frozen at tau = 0, i.e. the positive root of
+      // C t^2 - (C dl + a + b) t + b dl = 0 (dl = d_{K-2} - d_{K-1} < 0); kept
+      // only when it falls inside the bracket (C > 0)
+      double sm = 0;
+      for (int i = gl; i < K - 2; i += 16) sm += kz2[i] * frcp(kd[i] - kd[K - 1]);
+      sm = gsum(sm, gm);
+      const double C = 1.0 / rho + sm, dl = kd[K - 2] - kd[K - 1], a = kz2[K - 2], b = kz2[K - 1];
+      if (C > 0.0) {
+        const double Bm = C * dl + a + b;
+        const double sq = sqrt(fmax(Bm * Bm - 4.0 * C * b * dl, 0.0));
+        const double g = Bm > 0.0 ? (Bm + sq) / (2.0 * C) : (2.0 * b * dl) / (Bm - sq);
+        if (g > lo && g < hi) tau = g;
+      }
     }
   }
+  const double dorg = kd[o];
   int it = 0;
   for (; it < 120; ++it) {
-    double psi = 0, phi = 0, dpsi = 0, dphi = 0, aerr = 0;
-    for (int i = gl; i < K; i += 16) {
-      const double rdel = 1.0 / ((kd[i] - dorg) - tau);
-      const double t = kz2[i] * rdel;
-      const double dt = t * rdel;
-      if (i <= j) {
-        psi += t;
-        dpsi += dt;
-      } else {
-        phi += t;
-        dphi += dt;
-      }
-      aerr += fabs(t);
-    }
-    psi = rho * gsum(psi, gm);
-    phi = rho * gsum(phi, gm);
-    dpsi = rho * gsum(dpsi, gm);
-    dphi = rho * gsum(dphi, gm);
-    aerr = rho * gsum(aerr, gm);
+    double psi, phi, dpsi, dphi;
+    secular_pass<true>(kd, kz2, K, dorg, tau, j, gl, gm, psi, phi, dpsi, dphi);
+    if (!isfinite(psi + phi + dpsi + dphi))
+      secular_pass_ieee(kd, kz2, K, dorg, tau, j, gl, gm, psi, phi, dpsi, dphi);
+    // poles at or below the root contribute negative terms, poles above it
+    // positive ones: sum |t| = phi - psi
+    const double aerr = rho * (phi - psi);
+    psi *= rho;
+    phi *= rho;
+    dpsi *= rho;
+    dphi *= rho;
     const double f = 1.0 + psi + phi;
     if (f < 0.0)
       lo = fmax(lo, tau);
@@ -809,6 +936,9 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   const int grp = tid >> 4, gl = tid & 15;
   const unsigned gm = 0xFFFFu << (tid & 16);
   constexpr int NG = NT / 16;
+#if DAMF_PROF
+  const long long _r0 = clock64();
+#endif
   for (int j = lo + grp; j < hi; j += NG) {
     double t;
     int o;
@@ -820,6 +950,7 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
     if (DAMF_PROF && gl == 0 && rank == 0) atomicAdd(&A_prof[14], 1ull);
     if (DAMF_PROF && gl == 0) atomicMax(&A_prof[15], (unsigned long long)its);
     if (DAMF_PROF && gl == 0 && its >= 10) atomicAdd(&A_prof[31], 1ull);
+    if (DAMF_PROF && gl == 0) atomicAdd(&A_prof[64 + rank], (unsigned long long)its);
 #if DAMF_PROF
     // dev: record the iteration count of every root of the dumped problems
     if (gl == 0 && S_dump != nullptr) {
@@ -834,15 +965,34 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
     }
   }
   EPROF(17);
+#if DAMF_PROF
+  // per-rank: this CTA's root loop (all groups done) and its wait at the barrier
+  __syncthreads();
+  const long long _r1 = clock64();
   cl.sync();
+  if (threadIdx.x == 0) {
+    A_prof[32 + rank] += (unsigned long long)(_r1 - _r0);
+    A_prof[48 + rank] += (unsigned long long)(clock64() - _r1);
+  }
+#else
+  cl.sync();
+#endif
   EPROF(18);
   // --- Gu-Eisenstat z-hat: zhat_i^2 = prod_j (lam_j - d_i) / prod_{j!=i} (d_j - d_i) / rho
   for (int i = lo + grp; i < hi; i += NG) {
     const double di = S.kd[i];
     double p = 1.0;
-    for (int j = gl; j < K; j += 16) {
-      const double lmd = S.tau[j] - (di - S.kd[S.org[j]]);  // lambda_j - d_i
-      p *= (j == i) ? lmd / rhoN : lmd / (S.kd[j] - di);
+    for (int j0 = gl; j0 < K; j0 += 64) {
+      // four ratios in flight per lane (branch-free reciprocals)
+      double lmd[4], r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + 16 * u;
+        const bool in = j < K;
+        lmd[u] = in ? S.tau[j] - (di - S.kd[S.org[j]]) : 1.0;  // lambda_j - d_i
+        r[u] = frcp(in ? (j == i ? rhoN : S.kd[j] - di) : 1.0);
+      }
+      p *= (lmd[0] * r[0]) * (lmd[1] * r[1]) * ((lmd[2] * r[2]) * (lmd[3] * r[3]));
     }
     p = gprod(p, gm);
     const double zh = copysign(sqrt(fmax(p, 0.0)), S.kz[i]);
@@ -902,13 +1052,31 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
       if (item < K) {
         const double dj = S.kd[S.org[item]], tj = S.tau[item];
         double nn = 0;
-        for (int t = gl; t < K; t += 16) {
-          const double y = S.zhat[t] / ((S.kd[t] - dj) - tj);
-          nn += y * y;
+        for (int t0 = gl; t0 < K; t0 += 64) {
+          double y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + 16 * u;
+            const bool in = t < K;
+            y[u] = (in ? S.zhat[t] : 0.0) * frcp(in ? (S.kd[t] - dj) - tj : 1.0);
+          }
+          nn += (y[0] * y[0] + y[1] * y[1]) + (y[2] * y[2] + y[3] * y[3]);
         }
-        const double inv = 1.0 / sqrt(gsum(nn, gm));
-        for (int t = gl; t < K; t += 16)
-          row[n - 1 - S.kidx[t]] = S.zhat[t] / ((S.kd[t] - dj) - tj) * inv;
+        const double inv = rsqrt(gsum(nn, gm));
+        for (int t0 = gl; t0 < K; t0 += 64) {
+          double y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + 16 * u;
+            const bool in = t < K;
+            y[u] = (in ? S.zhat[t] : 0.0) * frcp(in ? (S.kd[t] - dj) - tj : 1.0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + 16 * u;
+            if (t < K) row[n - 1 - S.kidx[t]] = y[u] * inv;
+          }
+        }
       } else if (gl == 0) {
         row[n - 1 - (item - K)] = 1.0;
       }
@@ -1149,7 +1317,10 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       s += A.sp_vals[st.b_off + t] * row_val(A, sA, baseA, A.sp_rows[st.b_off + t], j);
     S.gA[j] = s;
     S.gB[j] = edge ? st.c_val * row_val(A, sB, baseB, st.c_row, j) : 0.0;
-    S.sig[j] = A.sigma[j];
+    const double sg = A.sigma[j], rs = sqrt(sg);
+    S.sig[j] = sg;
+    S.rsig[j] = rs;
+    S.irsig[j] = 1.0 / rs;
   }
   __syncthreads();
   {
@@ -1161,8 +1332,8 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
         sa += S.gA[i] * PTA[(int64_t)j * ld + i];
         if (edge) sb += S.gB[i] * PTB[(int64_t)j * ld + i];
       }
-      sa = warp_sum(sa) / sqrt(S.sig[j]);
-      sb = warp_sum(sb) / sqrt(S.sig[j]);
+      sa = warp_sum(sa) * S.irsig[j];
+      sb = warp_sum(sb) * S.irsig[j];
       if (lane < C) {
         *cl.map_shared_rank(S.wA + j, lane) = sa;
         *cl.map_shared_rank(S.wB + j, lane) = sb;
@@ -1304,7 +1475,11 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     const double lmax = fmax(edge ? lamF[0] : lamF[n - 1], 0.0);
     for (int t = tid; t < n; t += NT) {
       const double l = edge ? lamF[t] : lamF[n - 1 - t];
-      S.s2[t] = l > 64.0 * EPS * lmax ? sqrt(l) : 0.0;
+      const double sv = l > 64.0 * EPS * lmax ? sqrt(l) : 0.0;
+      const double rsv = sqrt(sv);
+      S.s2[t] = sv;
+      S.rs2[t] = rsv;
+      S.irs2[t] = sv > 0.0 ? 1.0 / rsv : 0.0;
     }
   }
   __syncthreads();
@@ -1319,7 +1494,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     double* Ht = prow(2, t);
     double* Ft = prow(0, t);
     double* Gt = prow(3, t);
-    const double st_ = S.s2[t], rst = sqrt(st_), ist = 1.0 / st_, irst = 1.0 / rst;
+    const double rst = S.rs2[t], irst = S.irs2[t], ist = irst * irst;
     double aE = 0;
     for (int i = lane; i < n; i += 32) aE += S.av[i] * Et[i];
     aE = warp_sum(aE);
@@ -1330,9 +1505,9 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       Ht[i] = Hi;
       bH += S.bv[i] * Hi;
       if (i < k) {
-        const double rs = sqrt(S.sig[i]);
-        Ft[i] = rs * Hi * irst;                             // F column t (A side)
-        Gt[i] = edge ? rs * e_i * irst : Hi * rst / rs;     // G column t (B side)
+        const double rs = S.rsig[i];
+        Ft[i] = rs * Hi * irst;                                   // F column t (A side)
+        Gt[i] = edge ? rs * e_i * irst : Hi * rst * S.irsig[i];   // G column t (B side)
       }
     }
     bH = warp_sum(bH);
@@ -1385,9 +1560,9 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
       double p2 = 0, p3 = 0;
       for (int t = olo; t < tk; ++t) {
         const double Hi = prow(2, t)[i], Ei = prow(1, t)[i];
-        const double rs = sqrt(S.s2[t]);
+        const double rs = S.rs2[t];
         p2 += S.exv[t] * rs * Hi;
-        p3 += edge ? S.eyv[t] * rs * Ei : S.eyv[t] / rs * Hi;
+        p3 += edge ? S.eyv[t] * rs * Ei : S.eyv[t] * S.irs2[t] * Hi;
       }
       S.partL[0][i] = p2;
       S.partL[1][i] = p3;
@@ -1395,9 +1570,9 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     if (warp == 0) {
       double q0 = 0, q1 = 0;
       for (int t = olo + lane; t < tk; t += 32) {
-        const double rs = sqrt(S.s2[t]);
+        const double rs = S.rs2[t];
         q0 += S.exv[t] * rs * S.dH[t];
-        q1 += edge ? S.eyv[t] * rs * S.dE[t] : S.eyv[t] / rs * S.dH[t];
+        q1 += edge ? S.eyv[t] * rs * S.dE[t] : S.eyv[t] * S.irs2[t] * S.dH[t];
       }
       q0 = warp_sum(q0);
       q1 = warp_sum(q1);
@@ -1483,9 +1658,9 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     //   ex F^-1 [m] = (1/sqrt(sig_m)) (sum_t ex_t sqrt(s_t) H[m][t]
     //                                  - c_H[m] / h_H * sum_t ex_t sqrt(s_t) dH_t)
     for (int m = tid; m < k; m += NT) {
-      const double rsm = sqrt(S.sig[m]);
-      S.yA1[m] = (S.yA1[m] - S.cH[m] * ihH * sA_) / rsm;
-      S.yB1[m] = edge ? (S.yB1[m] - S.cE[m] * ihE * sB_) / rsm
+      const double rsm = S.rsig[m], irsm = S.irsig[m];
+      S.yA1[m] = (S.yA1[m] - S.cH[m] * ihH * sA_) * irsm;
+      S.yB1[m] = edge ? (S.yB1[m] - S.cE[m] * ihE * sB_) * irsm
                       : (S.yB1[m] - S.cH[m] * ihH * sB_) * rsm;
     }
     __syncthreads();
@@ -1516,14 +1691,14 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
     //   node: G^-1[t][m] = (H[m][t] - dH_t c_H[m] / h_H) sqrt(sig_m) / sqrt(s_t)
     for (int x = tid; x < (kohi - olo) * k; x += NT) {
       const int t = olo + x / k, m = x % k;
-      const double rst = sqrt(S.s2[t]), rsm = sqrt(S.sig[m]);
+      const double rst = S.rs2[t], rsm = S.rsig[m], irsm = S.irsig[m];
       const double ahinv = prow(2, t)[m] - S.dH[t] * S.cH[m] * ihH;
       double gi;
       if (edge)
-        gi = rst * (prow(1, t)[m] - S.dE[t] * S.cE[m] * ihE) / rsm;
+        gi = rst * (prow(1, t)[m] - S.dE[t] * S.cE[m] * ihE) * irsm;
       else
-        gi = ahinv * rsm / rst;
-      prow(fbuf, t)[m] = rst * ahinv / rsm;  // edge: over H (read above); node: over E
+        gi = ahinv * rsm * S.irs2[t];
+      prow(fbuf, t)[m] = rst * ahinv * irsm;  // edge: over H (read above); node: over E
       prow(gbuf, t)[m] = gi;                 // edge: over E (read above); node: over H
     }
     __syncthreads();
@@ -2108,7 +2283,7 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
                        (unsigned)__cvta_generic_to_shared(&S.gbar[i])));
       S.gq[i] = 0;
     }
-    for (int i = 0; i < 3; ++i) S.gprof[i] = 0;
+    for (int i = 0; i < 8; ++i) S.gprof[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (A.reset_stop && rank == 0) A.ctl->stop_event = -1;
   }
@@ -2243,7 +2418,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
   }
 #if DAMF_PROF
   if (rank == 0 && threadIdx.x == 0)
+  {
     for (int i = 0; i < 3; ++i) A.ctl->prof[28 + i] += (unsigned long long)S.gprof[i];
+    for (int i = 3; i < 8; ++i) A.ctl->prof[96 + i] += (unsigned long long)S.gprof[i];
+  }
 #endif
 }
 

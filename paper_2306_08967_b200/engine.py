@@ -407,7 +407,7 @@ class Engine:
                     pulled_arcs=int(out[3]))
 
     def profile_counters(self):
-        out = np.zeros(32, np.uint64)
+        out = np.zeros(128, np.uint64)
         self._check(lib().damf_gpu_profile_counters(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64))))
         return out
 

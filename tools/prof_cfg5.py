@@ -32,6 +32,11 @@ en = ["eig.prep", "eig.roots", "eig.sync1", "eig.zhat", "eig.sync2", "eig.order"
 out["eig_us_per_event"] = {nm: round(pc[16 + i] / clk / nev, 2) for i, nm in enumerate(en)}
 out["staged_gemm_us_per_event"] = {nm: round(pc[28 + i] / clk / nev, 2)
                                    for i, nm in enumerate(["wait", "dmma", "whole_call"])}
+gn = ["prologue", "bar_after_dmma", "issue_next", "epilogue", "tail"]
+out["staged_gemm_detail_us_per_event"] = {nm: round(pc[99 + i] / clk / nev, 2) for i, nm in enumerate(gn)}
+out["roots_us_per_event_by_rank"] = [round(pc[32 + r] / clk / nev, 1) for r in range(16)]
+out["sync1_us_per_event_by_rank"] = [round(pc[48 + r] / clk / nev, 1) for r in range(16)]
+out["root_iters_per_event_by_rank"] = [round(pc[64 + r] / nev, 1) for r in range(16)]
 out["root_iters_mean"] = float(pc[13] / max(pc[14], 1))
 out["root_iters_max"] = int(e.profile_counters()[15])
 out["roots_with_10plus_iters_per_event"] = float(pc[31] / nev)
