@@ -2195,7 +2195,7 @@ int damf_gpu_debug_dump(damf_gpu* h, double* out, int64_t count) {
     CK(cudaMemset(src, 0, 16));
     return 0;
   }
-  const int64_t m = std::min<int64_t>(count, 8 + 8 * 800);
+  const int64_t m = std::min<int64_t>(count, 8 + 8 * 800 + 16 * 260);
   CK(cudaMemcpy(out, src, m * 8, cudaMemcpyDeviceToHost));
   return 0;
 }

@@ -37,11 +37,19 @@
 #ifndef DAMF_PROF_RANK
 #define DAMF_PROF_RANK 0  // CTA whose clock feeds the phase counters (dev profiling)
 #endif
-// Phase counters (ctl->prof) cost a global read-modify-write on the
-// critical path of every phase; they are compiled in only with -DDAMF_PROF=1
-// (tools/prof_events.py builds that way).
+// Phase counters are compiled in only with -DDAMF_PROF=1 (tools/prof_cfg5.py,
+// tools/prof_events.py): they accumulate in shared memory (a global
+// read-modify-write per phase would sit in front of every cluster barrier's
+// release) and are flushed to ctl->prof when the kernel ends.
 #ifndef DAMF_PROF
 #define DAMF_PROF 0
+#endif
+#if DAMF_PROF
+#define DAMF_PROF_PTR(S) (S).lprof
+#define DAMF_PROF_ADD(S, slot, v) (S).lprof[slot] += (unsigned long long)(v)
+#else
+#define DAMF_PROF_PTR(S) nullptr
+#define DAMF_PROF_ADD(S, slot, v) (void)0
 #endif
 
 namespace cg = cooperative_groups;
@@ -102,7 +110,7 @@ struct Smem {
     double gbuf[2][GBUF_D];       // GEMM operand staging: two slots of chunk rows x ld doubles
     double vscr[NW][NPAD];        // per-warp row scratch (deflation rotations, eager folds)
   };
-  int K, nrot, need;
+  int K, nrot, need, heavy;
   int k, pp[2];
   int err;
   unsigned long long gbar[2];     // GEMM staging: bulk-copy completion per slot
@@ -110,6 +118,11 @@ struct Smem {
   GemmJob gjobs[4];               // the staged GEMM's job list (uniform reads from shared memory)
   double gfro[4];                 // ... and its Frobenius norms
   long long gprof[8];             // DAMF_PROF: staged-GEMM wait / DMMA / call / prologue / bar / issue / epilogue / tail
+#if DAMF_PROF
+  unsigned long long lprof[128];  // phase counters of this CTA (flushed at kernel end)
+  unsigned long long tlog[64][4]; // %globaltimer: roots begin, group 0 done, CTA done (arrive), barrier release
+  int tlog_n;
+#endif
 };
 static_assert(sizeof(Smem<16>) <= 232448, "event kernel shared memory above the 227 KB opt-in limit");
 
@@ -667,17 +680,54 @@ __device__ __noinline__ void secular_pass_ieee(const double* kd, const double* k
   secular_pass<false>(kd, kz2, K, dorg, tau, j, gl, gm, psi, phi, dpsi, dphi);
 }
 
+// Root in (L, U) of the three-pole model c + sa/(pa-x) + sb/(pb-x) + sh/(ph-x)
+// with pa <= L < U <= pb and ph outside [pa, pb]: safeguarded Newton on
+// G(x) = F(x) (pa-x)(pb-x), which is smooth on the bracket and decreasing
+// through its only zero there. Scalar work (every lane the same); a model
+// step only, so a loose tolerance.
+DAMF_D double solve3(double c, double pa, double sa, double pb, double sb, double ph, double sh,
+                     double L, double U, double x0) {
+  double lo = L, hi = U;
+  double x = (x0 >= L && x0 <= U) ? x0 : 0.5 * (L + U);
+#pragma unroll 1
+  for (int it = 0; it < 8; ++it) {
+    const double rh = frcp(ph - x);
+    const double B = c + sh * rh, a = pa - x, b = pb - x;
+    const double g = B * a * b + sa * b + sb * a;
+    const double dg = sh * rh * rh * a * b - B * (a + b) - sa - sb;
+    if (g > 0.0)
+      lo = fmax(lo, x);
+    else if (g < 0.0)
+      hi = fmin(hi, x);
+    else
+      return x;
+    double xn = dg != 0.0 ? x - g * frcp(dg) : 0.5 * (lo + hi);
+    if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
+    const bool done = fabs(xn - x) <= 1e-8 * fmax(fabs(xn), fabs(x));
+    x = xn;
+    if (done) break;
+  }
+  return x;
+}
+
 // Root j of 1 + rho * sum_i kz2[i] / (kd[i] - lambda) = 0 (kd ascending,
-// rho > 0, sum kz2 <= 1), one 16-lane group. Returns tau and the origin pole
+// rho > 0, sum kz2 <= 1), one 16-lane group. h: index of a pole that holds
+// more than half of the weight (or -1). The interval that receives that
+// pole's own moved eigenvalue (the zero of 1/rho + z_h^2/(d_h - l) + rest)
+// has a root the two-pole model converges to slowly (the background changes
+// sign inside the interval; 7 iterations on the config-5 stream); there the
+// heavy pole is kept exact in the model, both in the initial guess and in
+// the iteration (solve3), which takes it to 1-2 iterations. Returns tau and the origin pole
 // o with lambda = kd[o] + tau, so lambda - kd[i] is formed as
 // tau - (kd[i]-kd[o]).
 DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, double sumz2,
-                        int j, double& tau_out, int& org_out) {
+                        int j, int h, double& tau_out, int& org_out) {
   const int gl = threadIdx.x & 15;
   const unsigned gm = 0xFFFFu << (threadIdx.x & 16);
   int o;
   double lo, hi;
   double tau;
+  bool use3 = false;
   if (j < K - 1) {
     // f at the midpoint of (d_j, d_j+1) picks the origin pole; the same sum
     // gives LAPACK dlaed4's initial guess: the two nearest poles exact, the
@@ -703,6 +753,15 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
     }
     tau = 0.5 * (lo + hi);
     const double C = 1.0 / rho + s + kz2[j] / mid - kz2[j + 1] / mid;
+    if (h >= 0 && h != j && h != j + 1) {
+      const double C3 = C - kz2[h] * frcp((kd[h] - kd[j]) - mid);
+      const double pa = kd[j] - kd[o], pb = kd[j + 1] - kd[o], ph = kd[h] - kd[o];
+      use3 = (C3 + kz2[h] * frcp(ph - pa)) * (C3 + kz2[h] * frcp(ph - pb)) < 0.0;
+      if (use3) {
+        const double g3 = solve3(C3, pa, kz2[j], pb, kz2[j + 1], ph, kz2[h], fmax(lo, pa), fmin(hi, pb), tau);
+        if (g3 > lo && g3 < hi) tau = g3;
+      }
+    }
     double g;
     if (o == j) {
       const double Aq = C * del + kz2[j] + kz2[j + 1], Bq = kz2[j] * del;
@@ -713,7 +772,7 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
       const double sq = sqrt(fabs(Aq * Aq + 4.0 * Bq * C));
       g = Aq < 0.0 ? 2.0 * Bq / (Aq - sq) : -(Aq + sq) / (2.0 * C);
     }
-    if (g > lo && g < hi) tau = g;
+    if (!use3 && g > lo && g < hi) tau = g;
   } else {
     o = j;
     lo = 0.0;
@@ -759,7 +818,23 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
     const double D1 = (kd[j] - dorg) - tau;
     double nt;
     bool ok = false;
-    if (j < K - 1) {
+    if (use3) {
+      // heavy pole exact, the rest of each side interpolated at its nearest pole
+      const double Dh = (kd[h] - dorg) - tau, rh = frcp(Dh), sh = rho * kz2[h];
+      const double th = sh * rh, dth = th * rh;
+      if (h <= j) {
+        psi -= th;
+        dpsi -= dth;
+      } else {
+        phi -= th;
+        dphi -= dth;
+      }
+      const double D2 = (kd[j + 1] - dorg) - tau;
+      const double q1 = dpsi * D1 * D1, q2 = dphi * D2 * D2;
+      const double c = 1.0 + psi - dpsi * D1 + phi - dphi * D2;
+      nt = tau + solve3(c, D1, q1, D2, q2, Dh, sh, fmax(lo - tau, D1), fmin(hi - tau, D2), 0.0);
+      ok = true;
+    } else if (j < K - 1) {
       const double D2 = (kd[j + 1] - dorg) - tau;
       const double q1 = dpsi * D1 * D1, q2 = dphi * D2 * D2;
       const double c = 1.0 + psi - dpsi * D1 + phi - dphi * D2;
@@ -929,7 +1004,12 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
 #endif
   double sz2 = 0;
   for (int j = tid; j < K; j += NT) sz2 += S.kz2[j];
+  if (tid == 0) S.heavy = -1;
   sz2 = block_sum(S, sz2);
+  // the pole that holds more than half of the weight, if any (at most one)
+  for (int j = tid; j < K; j += NT)
+    if (S.kz2[j] > 0.5 * sz2) S.heavy = j;
+  __syncthreads();
   // --- roots (this CTA's block of K)
   int lo, hi;
   block_range(K, C, rank, lo, hi);
@@ -938,11 +1018,12 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   constexpr int NG = NT / 16;
 #if DAMF_PROF
   const long long _r0 = clock64();
+  const unsigned long long _t0 = globaltimer();
 #endif
   for (int j = lo + grp; j < hi; j += NG) {
     double t;
     int o;
-    const int its = secular_root(S.kd, S.kz2, K, rhoN, sz2, j, t, o);
+    const int its = secular_root(S.kd, S.kz2, K, rhoN, sz2, j, S.heavy, t, o);
 #if DAMF_PROF
     const int o_ = o;
 #endif
@@ -967,12 +1048,21 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   EPROF(17);
 #if DAMF_PROF
   // per-rank: this CTA's root loop (all groups done) and its wait at the barrier
+  const unsigned long long _t1 = globaltimer();
   __syncthreads();
   const long long _r1 = clock64();
+  const unsigned long long _t2 = globaltimer();
   cl.sync();
   if (threadIdx.x == 0) {
     A_prof[32 + rank] += (unsigned long long)(_r1 - _r0);
     A_prof[48 + rank] += (unsigned long long)(clock64() - _r1);
+    if (S.tlog_n < 64) {
+      S.tlog[S.tlog_n][0] = _t0;
+      S.tlog[S.tlog_n][1] = _t1;
+      S.tlog[S.tlog_n][2] = _t2;
+      S.tlog[S.tlog_n][3] = globaltimer();
+      S.tlog_n += 1;
+    }
   }
 #else
   cl.sync();
@@ -1210,7 +1300,7 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
   do {                                                                    \
     if (DAMF_PROF && rank == DAMF_PROF_RANK && threadIdx.x == 0) {        \
       const long long _t = clock64();                                     \
-      A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
+      DAMF_PROF_ADD(S, slot, _t - _pt);                                   \
       _pt = _t;                                                           \
     }                                                                     \
   } while (0)
@@ -1220,7 +1310,7 @@ DAMF_D void erase_at(const DevCSR& g, int64_t u, long long pos) {
   do {                                                                    \
     if (DAMF_PROF && rank == DAMF_PROF_RANK && threadIdx.x == 0) {        \
       const long long _t = clock64();                                     \
-      A.ctl->prof[slot] += (unsigned long long)(_t - _pt);                \
+      DAMF_PROF_ADD(S, slot, _t - _pt);                                   \
       _pt = _t;                                                           \
     }                                                                     \
   } while (0)
@@ -1419,7 +1509,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   PROF_MARK(1);
   // ---- 3. eigen step A: D^2 + rho z z^T -> Q1^T rows (L2, shared) ---------
   eig_rank1<C>(S, cl, S.dd, S.zz, edge ? lp : 1.0, n, olo, ohi, A.ws_Q1T, ld, 0, S.lamA,
-               A.ctl->prof, DAMF_PROF && d <= 128 ? A.ws_priv : nullptr);
+               DAMF_PROF_PTR(S), DAMF_PROF && d <= 128 ? A.ws_priv : nullptr);
   PROF_MARK(2);
   if (edge) {
     // z2 = Q1^T u_minus for this CTA's columns, broadcast
@@ -1434,7 +1524,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   PROF_MARK(3);
   if (edge) {
     // ---- eigen step B: Lambda1 + lm z2 z2^T -> Q2^T rows (private) ---------
-    eig_rank1<C>(S, cl, S.lamA, S.zz, lm, n, olo, ohi, PB[0], pld, olo, S.lamB, A.ctl->prof,
+    eig_rank1<C>(S, cl, S.lamA, S.zz, lm, n, olo, ohi, PB[0], pld, olo, S.lamB, DAMF_PROF_PTR(S),
                  DAMF_PROF && d <= 128 ? A.ws_priv : nullptr);
     PROF_MARK(4);
     // E columns t (rows of E^T, private): E^T[t] = sum_e Q2^T[t][e] Q1^T[e]
@@ -2216,6 +2306,24 @@ DAMF_D void ppr_event(const EventKernelArgs& A, SMT& S, cg::cluster_group& cl,
 }
 
 
+#if DAMF_PROF
+// Flush this CTA's phase counters: rank 0 owns the phase slots, every rank its
+// own per-rank slots (32 / 48 / 64 + rank); slot 15 is a maximum.
+template <class SMT>
+DAMF_D void prof_flush(const EventKernelArgs& A, SMT& S, int rank) {
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < 128; ++i) {
+    const bool per_rank = i >= 32 && i < 96;
+    if (per_rank ? ((i & 15) == rank) : rank == 0) {
+      if (i == 15)
+        atomicMax(&A.ctl->prof[i], S.lprof[i]);
+      else
+        atomicAdd(&A.ctl->prof[i], S.lprof[i]);
+    }
+  }
+}
+#endif
+
 // ------------------------------------------------------------------ push kernel
 // The per-event push as its own cluster kernel (split mode): launched after a
 // one-event factor kernel, with its own register budget and twice the warps
@@ -2231,6 +2339,9 @@ struct PSmem {
   long long found[C][2];
   int lcnt3[3];
   int plist[3][PCAP];
+#if DAMF_PROF
+  unsigned long long lprof[128];
+#endif
 };
 template <int C>
 __global__ void __launch_bounds__(PPR_NT, 1) damf_ppr_kernel(EventKernelArgs A) {
@@ -2243,6 +2354,9 @@ __global__ void __launch_bounds__(PPR_NT, 1) damf_ppr_kernel(EventKernelArgs A) 
     S.pp[0] = A.ctl->pp[0];
     S.pp[1] = A.ctl->pp[1];
     for (int i = 0; i < 3; ++i) S.lcnt3[i] = 0;
+#if DAMF_PROF
+    for (int i = 0; i < 128; ++i) S.lprof[i] = 0;
+#endif
   }
   __syncthreads();
   cl.sync();
@@ -2261,6 +2375,9 @@ __global__ void __launch_bounds__(PPR_NT, 1) damf_ppr_kernel(EventKernelArgs A) 
     ppr_event<C, PSmem<C>, PPR_NT>(A, S, cl, ev);
     if (A.t_end && rank == 0 && threadIdx.x == 0) A.t_end[e] = globaltimer();
   }
+#if DAMF_PROF
+  prof_flush(A, S, rank);
+#endif
 }
 
 // ------------------------------------------------------------------ kernel
@@ -2284,6 +2401,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
       S.gq[i] = 0;
     }
     for (int i = 0; i < 8; ++i) S.gprof[i] = 0;
+#if DAMF_PROF
+    for (int i = 0; i < 128; ++i) S.lprof[i] = 0;
+    S.tlog_n = 0;
+#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (A.reset_stop && rank == 0) A.ctl->stop_event = -1;
   }
@@ -2417,10 +2538,17 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     }
   }
 #if DAMF_PROF
-  if (rank == 0 && threadIdx.x == 0)
-  {
-    for (int i = 0; i < 3; ++i) A.ctl->prof[28 + i] += (unsigned long long)S.gprof[i];
-    for (int i = 3; i < 8; ++i) A.ctl->prof[96 + i] += (unsigned long long)S.gprof[i];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) S.lprof[28 + i] += (unsigned long long)S.gprof[i];
+    for (int i = 3; i < 8; ++i) S.lprof[96 + i] += (unsigned long long)S.gprof[i];
+  }
+  prof_flush(A, S, rank);
+  // barrier timeline of this launch's first 64 eigen-solves (d <= 128: ws_priv is free)
+  if (threadIdx.x == 0 && A.d <= 128) {
+    double* o = A.ws_priv + 8 + 8 * 800 + rank * 260;
+    o[0] = S.tlog_n;
+    for (int i = 0; i < S.tlog_n; ++i)
+      for (int q = 0; q < 4; ++q) o[4 + 4 * i + q] = (double)(S.tlog[i][q] & 0xFFFFFFFFFFFFull);
   }
 #endif
 }

@@ -50,3 +50,25 @@ if os.environ.get("DAMF_DUMP"):
     ge.lib().damf_gpu_debug_dump(e.h, buf.ctypes.data, len(buf))
     np.save(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out", "slow_roots.npy"), buf)
     print("dumped", int(buf[0]))
+
+if os.environ.get("DAMF_TLOG"):
+    import ctypes as C
+    n = 8 + 8 * 800 + 16 * 260
+    buf = np.zeros(n)
+    ge.lib().damf_gpu_debug_dump.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    ge.lib().damf_gpu_debug_dump(e.h, buf.ctypes.data, n)
+    T = buf[8 + 8 * 800:].reshape(16, 260)
+    m = int(T[:, 0].min())
+    L = T[:, 4:4 + 4 * m].reshape(16, m, 4)
+    print("solve: [last CTA arrival - first roots begin] [release - last arrival] (us); slowest rank; its group-0 time")
+    for s in (13, 19, 23):
+        t0 = L[:, s, 0].min()
+        print("solve", s, "per rank [begin, group0 done, cta done, release] us")
+        for r in range(16):
+            print("  rank", r, [round((x - t0) / 1e3, 2) for x in L[r, s]])
+    for s in range(8, min(m, 24)):
+        t0 = L[:, s, 0].min()
+        arr = L[:, s, 2]
+        rel = L[:, s, 3]
+        print(s, round((arr.max() - t0) / 1e3, 2), round((rel.min() - arr.max()) / 1e3, 2), int(arr.argmax()),
+              [round((x - t0) / 1e3, 1) for x in arr])
