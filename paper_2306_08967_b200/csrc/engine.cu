@@ -475,6 +475,7 @@ PprArgs ppr_args(damf_gpu* h) {
   a.cand = nullptr;
   a.ncand = -1;
   a.push_guard = 1000000000LL;  // enhancer.cpp:8
+  a.narcs_hint = h->arcs;
   a.stats = h->pstats;
   a.ctl = h->ctl;
   return a;

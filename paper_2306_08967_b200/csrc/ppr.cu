@@ -1,10 +1,11 @@
 // K6-K8: the dynamic Personalized-PageRank enhancer (enhancer.cpp:26-206).
 //
 // State (base coordinates, sharing P_X with the factors): Z_b, r_b fp32
-// n x d, plus key[u] = |r_b[u]|_inf / max(deg u, 1) (fp32), kept current by
-// every kernel that writes r_b, which replaces the reference's FIFO + lazy
-// max-heap (enhancer.cpp:108-157): the push scans keys against the
-// threshold alpha*eps/s_max at every call.
+// n x d, plus key[u] >= |r_b[u]|_inf / max(deg u, 1) (fp32): exact after an
+// absorb, a pull round or an evaluation of the row, an upper bound after
+// scatter contributions (each adds its largest possible effect). It replaces
+// the reference's FIFO + lazy max-heap (enhancer.cpp:108-157): a row under
+// the threshold alpha*eps/s_max by its bound needs no look at r.
 //
 // The push is frontier-synchronous (Jacobi rounds) instead of FIFO
 // Gauss-Seidel. Each round chooses its direction from the frontier's
@@ -14,8 +15,9 @@
 //     with plain stores; only chunked heavy rows combine their partial sums
 //     with vector float reductions (red.global.add.v4.f32).
 //   scatter (sparse rounds): r[v] += (1-alpha) w / deg(v) * delta[u] for
-//     v in in(u) with float reductions, and the first toucher of v (atomicExch
-//     on mark[v]) appends v to the next candidate list.
+//     v in in(u) with float reductions; a target whose key bound crosses the
+//     threshold is appended to the next candidate list by its first toucher
+//     (atomicExch on mark[v]).
 // Work is handed out through per-warp static batches plus 32 atomic queue
 // heads. Floating-point reductions make the fp32 summation order, and with it
 // the last bits of r / Z and the push count, vary from run to run; the
@@ -671,25 +673,24 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
   int R = resume ? A.pst->R : (int)A.stats[2];  // device-resident round stamp base (monotonic)
   if (blockIdx.x == 0)
     for (int i = threadIdx.x; i < WQ_SC + 16 * QS; i += PT_) wq[i] = 0;
-  int nH, nchunks;
-  long long narcs;
-  if (resume) {
-    nH = A.pst->nH;
-    nchunks = A.pst->nchunks;
-    narcs = A.pst->narcs;
-    g.sync();  // counters zeroed
-  } else {
-  // ---- heavy rows (> HEAVY out-arcs): list, chunk prefix, chunk -> row
-  nH = grid_compact(
-      g, n,
-      [&](int i, int& v) {
-        v = i;
-        return A.out.cnt[i] > HEAVY;
-      },
-      A.heavy, A.blk);
-  nchunks = grid_scan(
-      g, nH, [&](int h) { return (A.out.cnt[A.heavy[h]] + CH - 1) / CH; }, A.hoff, A.blk);
-  {
+  // The heavy-row lists (rows above HEAVY out-arcs: list, chunk prefix, chunk
+  // -> row) and the exact arc count serve dense pull rounds only; a push that
+  // starts from a candidate list builds them the first time a round turns
+  // dense (three passes over every row's arc count, ~0.3 ms at 8.4 M rows --
+  // a fifth of the push after 1,000 insertions, which never pulls).
+  int nH = 0, nchunks = 0;
+  long long narcs = A.narcs_hint;
+  bool have_heavy = resume;
+  auto build_heavy = [&]() {
+    nH = grid_compact(
+        g, n,
+        [&](int i, int& v) {
+          v = i;
+          return A.out.cnt[i] > HEAVY;
+        },
+        A.heavy, A.blk);
+    nchunks = grid_scan(
+        g, nH, [&](int h) { return (A.out.cnt[A.heavy[h]] + CH - 1) / CH; }, A.hoff, A.blk);
     for (int h = blockIdx.x * PT_ + threadIdx.x; h < nH; h += gridDim.x * PT_) {
       A.hidx[A.heavy[h]] = h;
       for (int c = A.hoff[h]; c < A.hoff[h + 1]; ++c) A.cidx[c] = h;
@@ -698,15 +699,25 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
     for (int i = blockIdx.x * PT_ + threadIdx.x; i < n; i += gridDim.x * PT_) arcs += A.out.cnt[i];
     for (int o = 16; o > 0; o >>= 1) arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
     if (lane == 0 && arcs) atomicAdd(&sc[SC_ARCS * QS], arcs);
+    g.sync();
+    narcs = (long long)*(volatile unsigned long long*)&sc[SC_ARCS * QS];
+    have_heavy = true;
+  };
+  if (resume) {
+    nH = A.pst->nH;
+    nchunks = A.pst->nchunks;
+    narcs = A.pst->narcs;
   }
-  g.sync();
-  narcs = (long long)*(volatile unsigned long long*)&sc[SC_ARCS * QS];
-  }
+  g.sync();  // counters zeroed
+  if (!resume && A.ncand < 0) build_heavy();  // whole-graph scan: dense rounds are the rule
   // ---- rounds
   bool cand_all = resume || A.ncand < 0;
   int ncand = cand_all ? n : A.ncand;
   const int* candL = cand_all ? nullptr : A.cand;
-  bool fresh = false;  // candidates' keys must be recomputed from r
+  // candidates' keys must be recomputed from r: after a scatter round, and for
+  // a caller's candidate list (one group per candidate spreads a short list
+  // over the whole grid; the key scan hands a warp 32 of them)
+  bool fresh = !cand_all;
   long long pushes = resume ? A.pst->pushes : 0;
   long long c_aff = 0, c_arcs = 0, c_pulled = 0;  // lane-0 accounting
   int rounds = resume ? A.pst->rounds : 0;
@@ -882,7 +893,11 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
       if (blockIdx.x == 0 && threadIdx.x == 0) A.ctl->err = 9;  // NonConvergence
       break;
     }
-    const bool dense = S * 64 > narcs;
+    bool dense = S * 64 > narcs;
+    if (dense && !have_heavy) {  // (grid-uniform: S and narcs are)
+      build_heavy();
+      dense = S * 64 > narcs;
+    }
     if (tl && A.trace && rounds <= 1024) {
       long long* t = A.trace + 4 * (rounds - 1);
       t[0] = nF;
@@ -939,19 +954,34 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
           float x[CL::NE];
           CL::load(A.delta + (int64_t)u * d, gl, k, x);
           if (lane == 0) c_arcs += end - beg;
+          // |delta_u|_inf: what this push can add to a target's key (below)
+          float dmax = 0.0f;
+#pragma unroll
+          for (int e = 0; e < CL::NE; ++e)
+            if (CL::col(gl, e) < k) dmax = fmaxf(dmax, fabsf(x[e]));
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(gm, dmax, o, G));
           for (int p0 = beg; p0 < end; p0 += 32) {
             const int p = p0 + lane;
             const bool ok = p < end;
             int v = 0;
             float coef = 0.0f;
+            bool t = false;
             if (ok) {
               v = inC.ids[ib + p];
               const double w = inC.wts ? inC.wts[ib + p] : 1.0;
-              coef = (float)(om * w / fmax(A.deg[v], 1.0));
+              const double dg = fmax(A.deg[v], 1.0);
+              coef = (float)(om * w / dg);
+              // key[v] is kept as an upper bound of |r_v|_inf / max(deg v, 1):
+              // this contribution raises it by at most |coef| |delta|_inf / dg.
+              // Only a target whose bound crosses the threshold is a candidate
+              // of the next round (a target under it cannot be over it), and
+              // its first toucher appends it. The candidate threshold sits 1 %
+              // lower: fp32 rounding of many small increments stays inside it.
+              const float inc = (float)(fabs(om * w) / (dg * dg) * (double)dmax * (1.0 + 1e-4));
+              const float kb = atomicAdd(&A.key[v], inc) + inc;
+              t = kb > 0.99f * thr && __ldcg(&A.mark[v]) != R && atomicExch(&A.mark[v], R) != R;
             }
-            // first toucher appends v; a plain L2 read first keeps the many
-            // pushers of a hub's neighbours off the same returning atomic
-            const bool t = ok && __ldcg(&A.mark[v]) != R && atomicExch(&A.mark[v], R) != R;
             const unsigned tm = __ballot_sync(0xffffffffu, t);
             if (tm) {
               unsigned long long b0 = 0;
@@ -1010,7 +1040,7 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
     candL = A.items[cur];
     cur ^= 1;
   }
-  if (!split_exit)
+  if (!split_exit && have_heavy)
     for (int h = blockIdx.x * PT_ + threadIdx.x; h < nH; h += gridDim.x * PT_) A.hidx[A.heavy[h]] = -1;
   // accounting (bench algorithmic bytes): lane-0 counters of groups/warps
   for (int o = 16; o > 0; o >>= 1) {

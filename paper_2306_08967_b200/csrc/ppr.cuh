@@ -57,6 +57,7 @@ struct PprArgs {
   const int* cand;    // candidate rows for the first frontier (ncand >= 0)
   int ncand;          // -1: scan all rows
   long long push_guard;
+  long long narcs_hint; // arcs of the initial graph: picks the round direction until the exact count is built
   long long* stats;   // [pushes, rounds, next round base, sum|F|, sum|L|,
                       //  sum outdeg(L), matched arcs] (bench accounting)
   unsigned long long* t_end;
