@@ -501,7 +501,7 @@ double* live_Q(damf_gpu* h, int side) { return h->Q[side][h->h_ctl->pp[side]]; }
 // kernel with more warps per SM; the cooperative kernel exits before such a
 // round and is relaunched after it (one small host read per dense round).
 int run_push(damf_gpu* h, int grid, unsigned long long* t_end, int split = 0,
-             const int32_t* cand = nullptr, int ncand = -1) {
+             const int32_t* cand = nullptr, int ncand = -1, bool read_ctl = false) {
   h->launches += 2;
   CK(launch_smax(h->PT[0][0], h->PT[0][1], h->ctl, h->ld, h->smax, h->st));
   PprArgs a = ppr_args(h);
@@ -516,7 +516,14 @@ int run_push(damf_gpu* h, int grid, unsigned long long* t_end, int split = 0,
     CK(launch_ppr_push(a, std::min(grid, gmax), h->st));
     if (!split) break;
     CK(cudaMemcpyAsync(h->h_pst, h->pst, sizeof(PprState), cudaMemcpyDeviceToHost, h->st));
+    // (split calls end with a control-block read: the same round trip)
+    if (read_ctl) CK(cudaMemcpyAsync(h->h_ctl, h->ctl, kCtlBytes, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    if (read_ctl) {
+      h->k = h->h_ctl->k;
+      h->round_base = (int)h->h_pstats[2];
+      h->ctl_fresh = true;
+    }
     if (!h->h_pst->pull_pending) break;
     h->h_pst->pull_pending = 0;
     CK(cudaMemcpyAsync(&h->pst->pull_pending, &h->h_pst->pull_pending, sizeof(int),
@@ -998,9 +1005,11 @@ int damf_gpu_ppr_init(damf_gpu* h, damf_apply_stats* stats) {
 }
 
 int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
-  if (h) h->ctl_fresh = false;
   if (h->alpha1) return 0;
-  if (int r = sync_ctl(h)) return r;
+  // (after an apply the host mirror of the control block is current)
+  if (!h->ctl_fresh)
+    if (int r = sync_ctl(h)) return r;
+  h->ctl_fresh = false;
   const long long p0 = h->h_pstats[0], r0 = h->h_pstats[1];
   const int32_t* cand = nullptr;
   int ncand = -1;
@@ -1014,8 +1023,7 @@ int damf_gpu_ppr_push(damf_gpu* h, damf_apply_stats* stats) {
   }
   h->pend.clear();
   h->pend_valid = false;
-  if (int r = run_push(h, 1 << 20, nullptr, 1, cand, ncand)) return r;
-  if (int r = sync_ctl(h)) return r;
+  if (int r = run_push(h, 1 << 20, nullptr, 1, cand, ncand, true)) return r;
   if (h->h_ctl->err) return fail(h, h->h_ctl->err, "push_to_tolerance: push budget exceeded");
   h->pend_valid = true;
   if (stats) {

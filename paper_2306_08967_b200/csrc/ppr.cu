@@ -448,7 +448,7 @@ struct Grabber {
         i(0) {
     const long long per = (long long)nw * SB;
     dlo = (int)(total / (2 * per) * per);
-    if (total <= per) dlo = total;  // small: all static
+    if (total <= 4 * per) dlo = total;  // small: all static (a few strided batches per warp, no grabs)
     len = (total - dlo + NQ - 1) / NQ;
   }
   // warp-uniform; returns false when every item is taken
@@ -1170,31 +1170,40 @@ __global__ void ppr_init_kernel(PprArgs A) {
 
 // proj_row_bound (factor_state.cpp:251-259) from PT (P transposed):
 // col1 = max_j sum_i |P_ij| = max_j sum_i |PT[j][i]|; rowinf = max_i sum_j |P_ij|.
-__global__ void smax_kernel(const double* PT0, const double* PT1, const DevCtl* ctl, int ld,
-                            double* out) {
-  __shared__ double cmax[PT_], rmax[PT_];
+__global__ void __launch_bounds__(1024) smax_kernel(const double* PT0, const double* PT1,
+                                                    const DevCtl* ctl, int ld, double* out) {
+  // one CTA of 32 warps: row sums by warps (coalesced, 4-8 rows per warp),
+  // column sums by threads over a quarter of the rows each; fixed orders
+  __shared__ double cmax[32], part[4][kMaxD], rmax[kMaxD];
   const int k = ctl->k;
   const double* PT = ctl->pp[0] ? PT1 : PT0;
-  double c1 = 0, ri = 0;
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double c1 = 0;
+  for (int j = warp; j < k; j += 32) {
     double s = 0;
-    for (int i = 0; i < k; ++i) s += fabs(PT[(int64_t)j * ld + i]);
+    for (int i = lane; i < k; i += 32) s += fabs(PT[(int64_t)j * ld + i]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     c1 = fmax(c1, s);
   }
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+  if (lane == 0) cmax[warp] = c1;
+  {
+    const int i = threadIdx.x % kMaxD, q = threadIdx.x / kMaxD;  // kMaxD = 256: q in [0, 4)
+    const int per = (k + 3) / 4, j0 = q * per, j1 = min(k, j0 + per);
     double s = 0;
-    for (int j = 0; j < k; ++j) s += fabs(PT[(int64_t)j * ld + i]);
-    ri = fmax(ri, s);
+    if (i < k)
+      for (int j = j0; j < j1; ++j) s += fabs(PT[(int64_t)j * ld + i]);
+    part[q][i] = s;
   }
-  cmax[threadIdx.x] = c1;
-  rmax[threadIdx.x] = ri;
+  __syncthreads();
+  if (threadIdx.x < kMaxD) {
+    const int i = threadIdx.x;
+    rmax[i] = i < k ? ((part[0][i] + part[1][i]) + (part[2][i] + part[3][i])) : 0.0;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     double a = 0, b = 0;
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      a = fmax(a, cmax[t]);
-      b = fmax(b, rmax[t]);
-    }
+    for (int t = 0; t < 32; ++t) a = fmax(a, cmax[t]);
+    for (int t = 0; t < k; ++t) b = fmax(b, rmax[t]);
     *out = k == 0 ? 1.0 : fmax(a, sqrt(a * b));
   }
 }
@@ -1283,7 +1292,7 @@ cudaError_t launch_ppr_init(const PprArgs& a, int nsm, cudaStream_t s) {
 
 cudaError_t launch_smax(const double* PT0, const double* PT1, const DevCtl* ctl, int ld,
                         double* out, cudaStream_t s) {
-  smax_kernel<<<1, PT_, 0, s>>>(PT0, PT1, ctl, ld, out);
+  smax_kernel<<<1, 1024, 0, s>>>(PT0, PT1, ctl, ld, out);
   return cudaGetLastError();
 }
 
