@@ -476,6 +476,10 @@ PprArgs ppr_args(damf_gpu* h) {
   a.ncand = -1;
   a.push_guard = 1000000000LL;  // enhancer.cpp:8
   a.narcs_hint = h->arcs;
+  {
+    static const int fp = [] { const char* e = getenv("DAMF_PPR_FORCE_PULL"); return e && *e == '1' ? 1 : 0; }();
+    a.force_pull = fp;
+  }
   a.stats = h->pstats;
   a.ctl = h->ctl;
   return a;

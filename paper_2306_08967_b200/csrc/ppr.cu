@@ -893,10 +893,11 @@ __global__ void __launch_bounds__(PT_, ((VEC ? 4 * PER : PER) >= 16) ? 2 : 3) pp
       if (blockIdx.x == 0 && threadIdx.x == 0) A.ctl->err = 9;  // NonConvergence
       break;
     }
-    bool dense = S * 64 > narcs;
+    // (force_pull: diagnostic switch, every round in the atomics-free pull form)
+    bool dense = S * 64 > narcs || A.force_pull;
     if (dense && !have_heavy) {  // (grid-uniform: S and narcs are)
       build_heavy();
-      dense = S * 64 > narcs;
+      dense = S * 64 > narcs || A.force_pull;
     }
     if (tl && A.trace && rounds <= 1024) {
       long long* t = A.trace + 4 * (rounds - 1);

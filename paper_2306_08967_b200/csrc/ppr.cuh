@@ -57,6 +57,7 @@ struct PprArgs {
   const int* cand;    // candidate rows for the first frontier (ncand >= 0)
   int ncand;          // -1: scan all rows
   long long push_guard;
+  int force_pull;       // diagnostic (DAMF_PPR_FORCE_PULL=1): pull rounds only, for the scatter-vs-pull A/B
   long long narcs_hint; // arcs of the initial graph: picks the round direction until the exact count is built
   long long* stats;   // [pushes, rounds, next round base, sum|F|, sum|L|,
                       //  sum outdeg(L), matched arcs] (bench accounting)
