@@ -75,7 +75,7 @@ def host_info():
                 break
     except Exception:
         pass
-    return {"nproc": os.cpu_count(), "cpu": cpu}
+    return {"nproc": os.cpu_count(), "cpu": cpu, "oracle_build": ORACLE_BUILD["flags"]}
 
 
 class ClockSampler:
@@ -270,6 +270,30 @@ def cfg5_materialize(eng, n, d, hbm, peak_kind):
             "launch_ms": round(t, 4), "launch_ms_all": [round(x, 4) for x in ms]}
 
 
+ORACLE_BUILD = {"flags": "-O3 (portable build from make)"}
+
+
+def oracle_module():
+    """The CPU oracle for the baseline legs, compiled once per bench run with
+    -O3 -march=native on the host that is about to be timed (BASELINE.md section 4);
+    falls back to the portable in-tree build if the compiler is missing."""
+    if "oracle" not in sys.modules and not os.environ.get("DAMF_ORACLE_LIB"):
+        import subprocess
+        import tempfile
+        out = os.path.join(tempfile.mkdtemp(prefix="damf_oracle_"), "libdamf_oracle_native.so")
+        cmd = ["g++", "-O3", "-march=native", "-std=c++17", "-fPIC", "-shared", "-o", out,
+               os.path.join(ROOT, "oracle", "damf_oracle.cpp"),
+               os.path.join(ROOT, "oracle", "oracle_capi.cpp")]
+        try:
+            subprocess.run(cmd, check=True, capture_output=True, timeout=300)
+            os.environ["DAMF_ORACLE_LIB"] = out
+            ORACLE_BUILD["flags"] = "g++ -O3 -march=native, built on this host for this run"
+        except Exception as ex:  # noqa: BLE001
+            print(f"[bench] native oracle build failed ({ex}); using the portable build", file=sys.stderr)
+    import oracle
+    return oracle
+
+
 def cfg5_oracle(su, sv, n, d, sig, budget_s, max_events=None, first=0):
     """The fp64 oracle (1 thread) applying config 5's insertions in order
     from the same initial factors as the device (the fp32 rows
@@ -280,7 +304,7 @@ def cfg5_oracle(su, sv, n, d, sig, budget_s, max_events=None, first=0):
     stream's endpoints (their rows, the graph among them); Engine::apply --
     graph mutation, two rank-1 updates, cond_estimate, the rebase policy -- is
     timed per event with steady_clock like damf_cli.cpp:145-151."""
-    import oracle
+    oracle = oracle_module()
     from paper_2306_08967_b200 import workloads as W
     m = len(su) if max_events is None else min(max_events, len(su))
     first = min(first, m)
@@ -484,7 +508,7 @@ def bench_cfg2(args):
     del eng
     torch.cuda.empty_cache()
     if state:
-        import oracle
+        oracle = oracle_module()
         t2 = time.time()
         oe = oracle.OracleEngine.load_state(state)
         load_s = time.time() - t2
@@ -719,7 +743,7 @@ def cpu_legs(args):
     (enhancer.cpp:26-47) on an R-MAT scale-16 ef-24 graph at d = 128 with the
     device's init_propagate on the same graph and signal."""
     import torch
-    import oracle
+    oracle = oracle_module()
     from paper_2306_08967_b200 import engine as ge
     from paper_2306_08967_b200 import workloads as W
     out = {}

@@ -14,7 +14,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "build", "libdamf_oracle.so")
+# DAMF_ORACLE_LIB: another build of the same sources (bench.py's CPU legs compile
+# one with -O3 -march=native on the host they time; tests use the portable one)
+_LIB_PATH = os.environ.get("DAMF_ORACLE_LIB") or os.path.join(_HERE, "build", "libdamf_oracle.so")
 _lib = None
 
 i64p = C.POINTER(C.c_int64)

@@ -617,6 +617,41 @@ template <bool FAST>
 DAMF_D void secular_pass(const double* kd, const double* kz2, int K, double dorg, double tau, int j,
                          int gl, unsigned gm, double& psi, double& phi, double& dpsi, double& dphi) {
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  if (FAST && K <= 144) {
+    // k = 128 (K = 129 poles, the common case) and below: all of a lane's poles
+    // (up to 9) in flight at once -- one load / reciprocal latency per pass
+    // instead of one per batch of four -- and two accumulator sets
+    double r[9], z[9];
+#pragma unroll
+    for (int u = 0; u < 9; ++u) {
+      const int ii = gl + 16 * u;
+      const bool in = ii < K;
+      const double den = in ? (kd[ii] - dorg) - tau : 1.0;
+      z[u] = in ? kz2[ii] : 0.0;
+      r[u] = frcp(den);
+    }
+    double b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+#pragma unroll
+    for (int u = 0; u < 9; ++u) {
+      const double t = z[u] * r[u], dt = t * r[u];
+      const bool left = gl + 16 * u <= j;
+      if (u & 1) {
+        b0 += left ? t : 0.0;
+        b1 += left ? 0.0 : t;
+        b2 += left ? dt : 0.0;
+        b3 += left ? 0.0 : dt;
+      } else {
+        a0 += left ? t : 0.0;
+        a1 += left ? 0.0 : t;
+        a2 += left ? dt : 0.0;
+        a3 += left ? 0.0 : dt;
+      }
+    }
+    a0 += b0;
+    a1 += b1;
+    a2 += b2;
+    a3 += b3;
+  } else {
   int i = gl;
   for (; i + 48 < K; i += 64) {
     double r[4], z[4];
@@ -656,6 +691,7 @@ DAMF_D void secular_pass(const double* kd, const double* kz2, int K, double dorg
       a2 += left ? dt : 0.0;
       a3 += left ? 0.0 : dt;
     }
+  }
   }
   // four butterflies interleaved (independent shuffle chains)
 #pragma unroll
@@ -720,8 +756,8 @@ DAMF_D double solve3(double c, double pa, double sa, double pb, double sb, doubl
 // the iteration (solve3), which takes it to 1-2 iterations. Returns tau and the origin pole
 // o with lambda = kd[o] + tau, so lambda - kd[i] is formed as
 // tau - (kd[i]-kd[o]).
-DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, double sumz2,
-                        int j, int h, double& tau_out, int& org_out) {
+DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, double irho,
+                        double sumz2, int j, int h, double& tau_out, int& org_out) {
   const int gl = threadIdx.x & 15;
   const unsigned gm = 0xFFFFu << (threadIdx.x & 16);
   int o;
@@ -752,7 +788,8 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
       hi = 0.0;
     }
     tau = 0.5 * (lo + hi);
-    const double C = 1.0 / rho + s + kz2[j] / mid - kz2[j + 1] / mid;
+    const double rmid = frcp(mid);
+    const double C = irho + s + kz2[j] * rmid - kz2[j + 1] * rmid;
     if (h >= 0 && h != j && h != j + 1) {
       const double C3 = C - kz2[h] * frcp((kd[h] - kd[j]) - mid);
       const double pa = kd[j] - kd[o], pb = kd[j + 1] - kd[o], ph = kd[h] - kd[o];
@@ -766,11 +803,11 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
     if (o == j) {
       const double Aq = C * del + kz2[j] + kz2[j + 1], Bq = kz2[j] * del;
       const double sq = sqrt(fabs(Aq * Aq - 4.0 * Bq * C));
-      g = Aq > 0.0 ? 2.0 * Bq / (Aq + sq) : (Aq - sq) / (2.0 * C);
+      g = Aq > 0.0 ? 2.0 * Bq * frcp(Aq + sq) : (Aq - sq) * frcp(2.0 * C);
     } else {
       const double Aq = C * del - kz2[j] - kz2[j + 1], Bq = kz2[j + 1] * del;
       const double sq = sqrt(fabs(Aq * Aq + 4.0 * Bq * C));
-      g = Aq < 0.0 ? 2.0 * Bq / (Aq - sq) : -(Aq + sq) / (2.0 * C);
+      g = Aq < 0.0 ? 2.0 * Bq * frcp(Aq - sq) : -(Aq + sq) * frcp(2.0 * C);
     }
     if (!use3 && g > lo && g < hi) tau = g;
   } else {
@@ -786,7 +823,7 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
       double sm = 0;
       for (int i = gl; i < K - 2; i += 16) sm += kz2[i] * frcp(kd[i] - kd[K - 1]);
       sm = gsum(sm, gm);
-      const double C = 1.0 / rho + sm, dl = kd[K - 2] - kd[K - 1], a = kz2[K - 2], b = kz2[K - 1];
+      const double C = irho + sm, dl = kd[K - 2] - kd[K - 1], a = kz2[K - 2], b = kz2[K - 1];
       if (C > 0.0) {
         const double Bm = C * dl + a + b;
         const double sq = sqrt(fmax(Bm * Bm - 4.0 * C * b * dl, 0.0));
@@ -845,7 +882,7 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
         const double sq = sqrt(disc);
         const double den = Bq + (Bq >= 0.0 ? sq : -sq);
         if (den != 0.0) {
-          nt = tau + 2.0 * Cq / den;
+          nt = tau + 2.0 * Cq * frcp(den);  // (a model step: 1 ulp of the quotient is immaterial)
           ok = true;
         }
       }
@@ -1016,6 +1053,7 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   const int grp = tid >> 4, gl = tid & 15;
   const unsigned gm = 0xFFFFu << (tid & 16);
   constexpr int NG = NT / 16;
+  const double irhoN = 1.0 / rhoN;  // (once per solve, not per root)
 #if DAMF_PROF
   const long long _r0 = clock64();
   const unsigned long long _t0 = globaltimer();
@@ -1023,7 +1061,7 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   for (int j = lo + grp; j < hi; j += NG) {
     double t;
     int o;
-    const int its = secular_root(S.kd, S.kz2, K, rhoN, sz2, j, S.heavy, t, o);
+    const int its = secular_root(S.kd, S.kz2, K, rhoN, irhoN, sz2, j, S.heavy, t, o);
 #if DAMF_PROF
     const int o_ = o;
 #endif
