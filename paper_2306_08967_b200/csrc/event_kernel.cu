@@ -111,6 +111,8 @@ struct Smem {
     double vscr[NW][NPAD];        // per-warp row scratch (deflation rotations, eager folds)
   };
   int K, nrot, need, heavy;
+  int pf_stage;                   // side-job request for the CTA without roots (prefetch_next_event)
+  long long pf_e;                 // ... the event it looks ahead to
   int k, pp[2];
   int err;
   unsigned long long gbar[2];     // GEMM staging: bulk-copy completion per slot
@@ -916,6 +918,73 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
   return it;
 }
 
+// ---- look-ahead (side job of a CTA that owns no root in a step's first solve)
+// The next event's descriptors, graph rows and base rows are first touched
+// on the critical path otherwise (EventDesc / StepDesc reads, the duplicate
+// scan, the gather: one to three dependent DRAM latencies each). With K = 129
+// roots over 16 CTAs the last CTA has none and waits ~3 us at the barrier
+// after the roots; its warp 0 spends that wait pulling the next event's lines
+// into L2. Stage 1 (first step of event e): everything addressable from the
+// next event's (u, v). Stage 2 (second step, ~80 us later, stage 1's lines
+// resident): the dependent part -- the adjacency lists behind off[u] and the
+// fp64 side-table rows behind slot[side][row]. Prefetches only: no data is
+// consumed, so an event that fails or rebases in between costs nothing.
+DAMF_D void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+DAMF_D void pf_l2_span(const void* p, int bytes, int lane0, int lane) {
+  // lanes lane0, lane0 + 1, ... take one 128-byte line each
+  const char* b = reinterpret_cast<const char*>(p);
+  const int i = lane - lane0;
+  if (i >= 0 && i * 128 < bytes + 127) pf_l2(b + i * 128);
+}
+template <int C>
+DAMF_D void prefetch_next_event(const EventKernelArgs& A, Smem<C>& S) {
+  const int lane = threadIdx.x & 31;
+  const int stage = S.pf_stage;
+  const int64_t e1 = S.pf_e;
+  const EventDesc* evp = A.ev + e1;
+  if (stage == 1 && lane == 31 && e1 + 1 < A.e_end) {
+    pf_l2(evp + 1);  // the descriptor after it (read by the next look-ahead)
+    pf_l2(reinterpret_cast<const char*>(evp + 1) + sizeof(EventDesc) - 1);
+  }
+  const int kind = evp->kind;
+  if (kind != 1 && kind != 2) return;  // edges only
+  const int64_t u = evp->u, v = evp->v;
+  const int rowb = A.d * 4;
+  if (stage == 1) {
+    if (lane == 30) {
+      pf_l2(A.steps + evp->step0);
+      pf_l2(A.steps + evp->step0 + 1);
+    }
+    const void* direct[12] = {A.out.cnt + u, A.out.off + u, A.out.cap + u, A.deg + u,
+                              A.out.cnt + v, A.out.off + v, A.out.cap + v, A.deg + v,
+                              A.slot[0] + u, A.slot[1] + v, A.slot[0] + v, A.slot[1] + u};
+    if (lane < 12) pf_l2(direct[lane]);
+    // base rows X_b[u], Y_b[v] (step 1), X_b[v], Y_b[u] (step 2): 4 lines each up to d = 128
+    if (lane >= 12 && lane < 28) {
+      const int q = (lane - 12) >> 2, l = (lane - 12) & 3;
+      const float* base = (q & 1) ? A.Yb : A.Xb;
+      const int64_t row = (q == 0 || q == 3) ? u : v;
+      for (int o = l * 128; o < rowb; o += 512) pf_l2(reinterpret_cast<const char*>(base + row * A.d) + o);
+    }
+  } else {
+    if (lane < 2) {
+      // adjacency list of u / v (the duplicate / missing-arc scan): first 4 KB
+      const int64_t r = lane == 0 ? u : v;
+      const int64_t off = A.out.off[r];
+      const int bytes = min(A.out.cnt[r], 1024) * 4;
+      for (int o = 0; o < bytes; o += 128) pf_l2(reinterpret_cast<const char*>(A.out.ids + off) + o);
+    } else if (lane < 6) {
+      // fp64 side-table rows
+      const int side = lane & 1;
+      const int64_t r = (lane == 2 || lane == 5) ? u : v;  // X_b[u], Y_b[v], X_b[v], Y_b[u]
+      const int sl = A.slot[side][r];
+      if (sl >= 0)
+        for (int o = 0; o < A.d * 8; o += 128)
+          pf_l2(reinterpret_cast<const char*>(A.rows64[side] + (int64_t)sl * A.ld) + o);
+    }
+  }
+}
+
 // Eigen-decomposition of diag(dd) + rho z z^T over n entries, cluster-wide.
 // dd must be descending when rho > 0 and ascending when rho < 0; both map to
 // the canonical ascending problem by index reversal (c = n-1-i) and, for
@@ -925,7 +994,8 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
 template <int C>
 DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const double* z,
                       double rho, int n, int elo, int ehi, double* QT, int ldq, int row_off,
-                      double* lamOut, unsigned long long* A_prof, double* S_dump = nullptr) {
+                      double* lamOut, unsigned long long* A_prof, double* S_dump = nullptr,
+                      const EventKernelArgs* Apf = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cl.block_rank();
   const bool neg = rho < 0.0;
@@ -1083,6 +1153,8 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
       *cl.map_shared_rank(S.org + j, gl) = o;
     }
   }
+  // (no roots here: look ahead to the next event instead of idling at the barrier)
+  if (Apf != nullptr && lo == hi && rank == C - 1 && warp == 0 && S.pf_stage) prefetch_next_event<C>(*Apf, S);
   EPROF(17);
 #if DAMF_PROF
   // per-rank: this CTA's root loop (all groups done) and its wait at the barrier
@@ -1547,7 +1619,7 @@ DAMF_D bool rank1_step(const EventKernelArgs& A, Smem<C>& S, cg::cluster_group& 
   PROF_MARK(1);
   // ---- 3. eigen step A: D^2 + rho z z^T -> Q1^T rows (L2, shared) ---------
   eig_rank1<C>(S, cl, S.dd, S.zz, edge ? lp : 1.0, n, olo, ohi, A.ws_Q1T, ld, 0, S.lamA,
-               DAMF_PROF_PTR(S), DAMF_PROF && d <= 128 ? A.ws_priv : nullptr);
+               DAMF_PROF_PTR(S), DAMF_PROF && d <= 128 ? A.ws_priv : nullptr, &A);
   PROF_MARK(2);
   if (edge) {
     // z2 = Q1^T u_minus for this CTA's columns, broadcast
@@ -2557,6 +2629,10 @@ __global__ void __launch_bounds__(NT, 1) damf_event_kernel(EventKernelArgs A) {
     if (!(A.mode & 1)) {
       bool fin = true;
       for (int s = 0; s < ev.nsteps && fin; ++s) {
+        if (threadIdx.x == 0) {  // (read after several block barriers inside the step)
+          S.pf_stage = e + 1 < A.e_end ? (s == 0 ? 1 : s == 1 ? 2 : 0) : 0;
+          S.pf_e = e + 1;
+        }
         const StepDesc st = A.steps[ev.step0 + s];
         fin = rank1_step<C>(A, S, cl, st, e, ev.step0 + s);
       }

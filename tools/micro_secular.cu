@@ -25,6 +25,7 @@ __global__ void k(const double* kd, const double* kz2, int K, double rho, double
     __syncthreads();
     const long long t1 = clock64();
     if (t1 - t0 < best) best = t1 - t0;
+    if (r == 0 && threadIdx.x == 0) out[30] = t1 - t0;
   }
   if ((threadIdx.x & 15) == 0 && grp < ngroups) { out[1 + grp] = its; }
   if (threadIdx.x == 0) out[0] = best;
@@ -51,9 +52,10 @@ int main() {
       for (int ng : {1, 2, 9, 16}) {
         if (j0 + ng > K) continue;
         k<<<1, 256>>>(dkd, dkz, K, 2.0, 1.0, heavy, ng, j0, dout, dt, 20);
-        long long h[20];
+        long long h[20], h30;
         cudaMemcpy(h, dout, 20 * 8, cudaMemcpyDeviceToHost);
-        printf("heavy=%3d j0=%3d groups=%2d  cycles=%6lld  its:", heavy, j0, ng, h[0]);
+        cudaMemcpy(&h30, dout + 30, 8, cudaMemcpyDeviceToHost);
+        printf("heavy=%3d j0=%3d groups=%2d  cycles=%6lld  first-rep=%6lld  its:", heavy, j0, ng, h[0], h30);
         for (int g = 0; g < ng; ++g) printf(" %lld", h[1 + g]);
         printf("\n");
       }
