@@ -725,21 +725,27 @@ __device__ __noinline__ void secular_pass_ieee(const double* kd, const double* k
 // step only, so a loose tolerance.
 DAMF_D double solve3(double c, double pa, double sa, double pb, double sb, double ph, double sh,
                      double L, double U, double x0) {
+  // ... cleared of its third pole as well: the cubic
+  //   Q(x) = (c (ph-x) + sh)(pa-x)(pb-x) + (ph-x)(sa (pb-x) + sb (pa-x)) = G(x) (ph-x),
+  // so an iteration is a handful of dependent FMAs and one reciprocal (the
+  // rational form needed two); ph - x keeps its sign on the bracket
+  const double sgn = ph > U ? 1.0 : -1.0;
   double lo = L, hi = U;
   double x = (x0 >= L && x0 <= U) ? x0 : 0.5 * (L + U);
 #pragma unroll 1
   for (int it = 0; it < 8; ++it) {
-    const double rh = frcp(ph - x);
-    const double B = c + sh * rh, a = pa - x, b = pb - x;
-    const double g = B * a * b + sa * b + sb * a;
-    const double dg = sh * rh * rh * a * b - B * (a + b) - sa - sb;
+    const double a = pa - x, b = pb - x, hh = ph - x;
+    const double B = fma(c, hh, sh), ab = a * b, m = fma(sa, b, sb * a);
+    const double q = fma(B, ab, hh * m);
+    const double dq = -(fma(c, ab, B * (a + b)) + fma(hh, sa + sb, m));
+    const double g = sgn * q;
     if (g > 0.0)
       lo = fmax(lo, x);
     else if (g < 0.0)
       hi = fmin(hi, x);
     else
       return x;
-    double xn = dg != 0.0 ? x - g * frcp(dg) : 0.5 * (lo + hi);
+    double xn = dq != 0.0 ? x - q * frcp(dq) : 0.5 * (lo + hi);
     if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
     const bool done = fabs(xn - x) <= 1e-8 * fmax(fabs(xn), fabs(x));
     x = xn;
@@ -896,7 +902,7 @@ DAMF_D int secular_root(const double* kd, const double* kz2, int K, double rho, 
       // last pole creeps in linearly
       const double P = -(psi + phi), dP = dpsi + dphi;
       if (P > 0.0 && dP > 0.0) {
-        nt = tau + (P * P - P) / dP;
+        nt = tau + (P * P - P) * frcp(dP);
         ok = true;
       }
     }
@@ -1091,7 +1097,7 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   __syncthreads();
   EPROF(16);
   const int K = S.K;
-#if DAMF_PROF
+#if DAMF_PROF >= 2  // (dump builds only: the extra cluster barrier and global traffic distort the phase timers)
   // dev: dump the first 8 deflated secular problems after a reset
   // (damf_gpu_debug_dump with count < 0): K, rho, sum z^2, kd[K], kz2[K]
   if (S_dump != nullptr) {
@@ -1140,12 +1146,14 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
     if (DAMF_PROF && gl == 0) atomicMax(&A_prof[15], (unsigned long long)its);
     if (DAMF_PROF && gl == 0 && its >= 10) atomicAdd(&A_prof[31], 1ull);
     if (DAMF_PROF && gl == 0) atomicAdd(&A_prof[64 + rank], (unsigned long long)its);
-#if DAMF_PROF
+#if DAMF_PROF >= 2
     // dev: record the iteration count of every root of the dumped problems
     if (gl == 0 && S_dump != nullptr) {
       const long long slot = (long long)S_dump[1] - 1;  // this eigensolve's record (set below)
       if (slot >= 0 && slot < 8) S_dump[8 + slot * 800 + 530 + j] = its;
     }
+#endif
+#if DAMF_PROF
     (void)o_;
 #endif
     if (gl < C) {

@@ -30,7 +30,42 @@ __global__ void k(const double* kd, const double* kz2, int K, double rho, double
   if ((threadIdx.x & 15) == 0 && grp < ngroups) { out[1 + grp] = its; }
   if (threadIdx.x == 0) out[0] = best;
 }
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {
+    // dumped problems (tools/dump_secular.py -> secular_problems.bin: records of 800 doubles:
+    // K, rho, sum z^2, ..., kd at 8, kz2 at 268): every rank's 9 roots, as in the kernel
+    FILE* f = fopen(argv[1], "rb");
+    if (!f) { printf("cannot open %s\n", argv[1]); return 1; }
+    std::vector<double> rec(800);
+    double *dkd, *dkz, *dt; long long* dout;
+    cudaMalloc(&dkd, 260 * 8); cudaMalloc(&dkz, 260 * 8); cudaMalloc(&dt, 64 * 8); cudaMalloc(&dout, 64 * 8);
+    for (int p = 0; p < 4 && fread(rec.data(), 8, 800, f) == 800; ++p) {
+      const int K = (int)rec[0];
+      int heavy = -1; for (int i = 0; i < K; ++i) if (rec[268 + i] > 0.5 * rec[2]) heavy = i;
+      cudaMemcpy(dkd, rec.data() + 8, K * 8, cudaMemcpyHostToDevice);
+      cudaMemcpy(dkz, rec.data() + 268, K * 8, cudaMemcpyHostToDevice);
+      printf("problem %d: K=%d rho=%.6f heavy=%d\n", p, K, rec[1], heavy);
+      for (int j1 : {K - 1, K - 2, K - 3, 5}) {
+        k<<<1, 256>>>(dkd, dkz, K, rec[1], rec[2], heavy, 1, j1, dout, dt, 20);
+        long long h[20];
+        cudaMemcpy(h, dout, 20 * 8, cudaMemcpyDeviceToHost);
+        printf("  single root %3d cycles=%6lld its=%lld\n", j1, h[0], h[1]);
+      }
+      const int per = (K + 15) / 16;
+      for (int r = 0; r * per < K; ++r) {
+        const int ng = std::min(per, K - r * per);
+        k<<<1, 256>>>(dkd, dkz, K, rec[1], rec[2], heavy, ng, r * per, dout, dt, 20);
+        long long h[20];
+        cudaMemcpy(h, dout, 20 * 8, cudaMemcpyDeviceToHost);
+        printf("  rank %2d roots %3d..%3d cycles=%6lld its:", r, r * per, r * per + ng - 1, h[0]);
+        for (int g = 0; g < ng; ++g) printf(" %lld", h[1 + g]);
+        printf("\n");
+      }
+    }
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+  }
+
   const int K = 129;
   std::vector<double> d(K), z(K);
   // old spectrum squared: sigma_i = i^-1/2 -> lambda = 1/i, ascending canonical order
