@@ -175,8 +175,10 @@ int damf_gpu_create_from_factors(const damf_csr* g, const damf_config* cfg, int6
  * (factor_state.cpp:84-102) — randomized t-SVD of the adjacency on the device
  * (svd.cpp:47-96: l = d + 10, 4 power iterations, the reference's Gaussian
  * stream for Omega; graphs with n <= 600 take the exact dense SVD), then
- * the factor-based constructor. DAMF_E_ZERO_MATRIX for an empty graph,
- * DAMF_E_UNSUPPORTED if the sketch is numerically rank-deficient. */
+ * the factor-based constructor. A numerically rank-deficient sketch
+ * (rank(A) < l) is orthogonalised by Gram-Schmidt with basis completion, as
+ * the reference's Householder QR does, and the rank is clamped
+ * (svd.cpp:84-89). DAMF_E_ZERO_MATRIX for an empty graph. */
 int damf_gpu_create(const damf_csr* g, const damf_config* cfg, damf_gpu** out);
 
 /* Engine(g, fs, es, cfg, events_applied, events_since_rebase)

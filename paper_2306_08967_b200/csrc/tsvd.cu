@@ -142,7 +142,11 @@ __global__ void chol_f64(const double* G, int l, double* R, double* Rinv, int* f
     if (threadIdx.x == 0) {
       double s = G[j * l + j];
       for (int i = 0; i < j; ++i) s -= R[i * l + j] * R[i * l + j];
-      if (!(s > 1e-28 * gmax)) {
+      // a residual below 1e-6 of the column's own norm (1e-12 in the Gram
+      // entries, which carry ~1e-16 of cancellation error) is a numerically
+      // dependent column: CholeskyQR cannot orthogonalise it; the caller
+      // switches to the Gram-Schmidt path (gs_qr)
+      if (!(s > 1e-12 * G[j * l + j]) || !(s > 1e-28 * gmax)) {
         bad = 1;
         s = 1.0;
       }
@@ -211,6 +215,46 @@ __global__ void tall_mm(const double* Y, int64_t n, int l, const double* __restr
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           if (rb + a < rows && c0 + b < mc) out[(r0 + rb + a) * ldo + c0 + b] = (TO)acc[a][b];
+    }
+  }
+}
+
+// ---- rank-deficient sketches: classical Gram-Schmidt, twice, column by column
+// (the reference's Householder QR, svd.cpp:75-95 via qr_orthonormalize,
+// orthogonalises any sketch and completes the basis; CholeskyQR2 needs full
+// numerical rank). Used only after chol_f64 reports a dependent column.
+// c[t] (t <= j, zeroed) += sum_r M[r][t] M[r][j]
+__global__ void gs_dots(const double* __restrict__ M, int64_t n, int l, int j, double* c) {
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+    const double mj = M[r * l + j];
+    if (t <= j) acc = fma(M[r * l + t], mj, acc);
+  }
+  if (t <= j && acc != 0.0) atomicAdd(c + t, acc);
+}
+// M[r][j] -= sum_{t<j} M[r][t] c[t]   (one warp per row)
+__global__ void gs_update(double* M, int64_t n, int l, int j, const double* __restrict__ c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = w; r < n; r += nw) {
+    double s = 0.0;
+    for (int t = lane; t < j; t += 32) s = fma(M[r * l + t], c[t], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) M[r * l + j] -= s;
+  }
+}
+// M[r][j] *= scale, or (fill) a fixed pseudo-random completion vector
+__global__ void gs_col(double* M, int64_t n, int l, int j, double scale, int fill) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (fill) {
+      unsigned long long x = (unsigned long long)r * 0x9E3779B97F4A7C15ull + (unsigned long long)(j + 1) * 0xBF58476D1CE4E5B9ull;
+      x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+      M[r * l + j] = (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    } else {
+      M[r * l + j] *= scale;
     }
   }
 }
@@ -480,7 +524,50 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
       else
         spmm_gather_f64<9><<<gs, 256, 0, st>>>(o, i, w, n, x, y, l);
     };
-    // CholeskyQR2 in place on Y (n x l); R of the factorisation into Rout
+    // Gram-Schmidt QR in place on Ym (n x l), any rank: Q gets an orthonormal
+    // basis whose leading columns span Ym's (dependent columns are replaced by
+    // completion vectors, as a Householder Q would hold), Rgs (host, l x l
+    // row-major, upper) = Q^T Ym with a zero diagonal entry per dependent column
+    double* gc = nullptr;
+    if ((err = alloc(&gc, (size_t)l + 1))) break;
+    auto gs_qr = [&](double* Ym, std::vector<double>& Rgs) -> cudaError_t {
+      Rgs.assign((size_t)l * l, 0.0);
+      std::vector<double> hc(l + 1);
+      cudaError_t e2 = cudaSuccess;
+      for (int j = 0; j < l; ++j) {
+        double orig2 = 0.0, fin2 = 0.0;
+        for (int attempt = 0; attempt < 2; ++attempt) {  // attempt 1: the completion vector
+          for (int pass = 0; pass < 3; ++pass) {         // two projections, then the final norm
+            cudaMemsetAsync(gc, 0, (size_t)(l + 1) * 8, st);
+            gs_dots<<<gs, 288, 0, st>>>(Ym, n, l, j, gc);
+            cudaMemcpyAsync(hc.data(), gc, (size_t)(j + 1) * 8, cudaMemcpyDeviceToHost, st);
+            if ((e2 = cudaStreamSynchronize(st))) return e2;
+            if (pass == 0) orig2 = hc[j];
+            if (pass == 2) {
+              fin2 = hc[j];
+              break;
+            }
+            if (attempt == 0)
+              for (int t = 0; t < j; ++t) Rgs[(size_t)t * l + j] += hc[t];
+            if (j > 0) gs_update<<<gs, 256, 0, st>>>(Ym, n, l, j, gc);
+          }
+          // dependent: what is left is rounding noise of the projections
+          const bool dep = !(fin2 > 1e-20 * orig2) || !(orig2 > 0.0);
+          if (!dep) {
+            if (attempt == 0) Rgs[(size_t)j * l + j] = std::sqrt(fin2);
+            gs_col<<<gs, 256, 0, st>>>(Ym, n, l, j, 1.0 / std::sqrt(fin2), 0);
+            break;
+          }
+          if (attempt == 1) return cudaErrorUnknown;  // (a fixed vector inside the span: not expected)
+          gs_col<<<gs, 256, 0, st>>>(Ym, n, l, j, 0.0, 1);
+        }
+      }
+      return cudaGetLastError();
+    };
+    // CholeskyQR2 in place on Y (n x l); R of the factorisation into Rout.
+    // A numerically dependent column (chol_f64's flag, read before the in-place
+    // product so that Ym is intact) sends the matrix through gs_qr instead.
+    std::vector<double> Rgs;
     auto cholqr2 = [&](double* Ym, double* Rout) -> int {
       int hf = 0;
       for (int pass = 0; pass < 2; ++pass) {
@@ -490,10 +577,23 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
           for (int j0 = 0; j0 < l; j0 += GB)
             gram_block_f64<<<gs, TT, gram_smem, st>>>(Ym, n, l, G, i0, j0);
         chol_f64<<<1, 256, 0, st>>>(G, l, pass == 0 ? Racc : R, Ri, dflag);
-        tall_mm<double><<<gs, TT, mm_smem, st>>>(Ym, n, l, Ri, l, Ym, l);
         cudaMemcpyAsync(&hf, dflag, sizeof(int), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        if (hf) return 1;
+        if (hf) {
+          if (gs_qr(Ym, Rgs) != cudaSuccess) return 1;
+          res->gs_fallbacks += 1;
+          if (Rout) {
+            // R = R_gs (pass 0) or R_gs * R_pass1 (Ym was Y R_pass1^-1 already)
+            cudaMemcpyAsync(R, Rgs.data(), (size_t)l * l * 8, cudaMemcpyHostToDevice, st);
+            if (pass == 0)
+              cudaMemcpyAsync(Rout, R, (size_t)l * l * 8, cudaMemcpyDeviceToDevice, st);
+            else
+              tall_mm<double><<<1, TT, mm_smem, st>>>(R, l, l, Racc, l, Rout, l);
+            cudaStreamSynchronize(st);
+          }
+          return 0;
+        }
+        tall_mm<double><<<gs, TT, mm_smem, st>>>(Ym, n, l, Ri, l, Ym, l);
       }
       if (Rout) {
         // R = R_pass2 * R_pass1 (upper l x l), on the device via tall_mm

@@ -22,6 +22,7 @@ struct TsvdResult {
   int k = 0;
   int status = 0;                  // 0 ok, else damf status (6 ZeroMatrix, 101 unsupported)
   int omega = 0;                   // 0: reference Gaussian stream, 1: device Philox stream
+  int gs_fallbacks = 0;            // QRs that took the Gram-Schmidt path (rank-deficient sketch)
   std::vector<double> sigma;       // k
   float* xb_dev = nullptr;         // n x k device (randomized path), caller frees
   float* yb_dev = nullptr;

@@ -309,6 +309,50 @@ def test_device_tsvd_init_matches_oracle(case):
     assert wp <= 1e-4
 
 
+@pytest.mark.parametrize("shape", ["biclique", "stars"])
+def test_device_tsvd_init_rank_deficient_sketch(shape):
+    # rank(A) < l = d + 10 on the randomized path (n > 600): CholeskyQR2 cannot
+    # orthogonalise the sketch; the reference's Householder QR can, and clamps
+    # the rank (svd.cpp:75-95). The device takes its Gram-Schmidt path and
+    # must land on the oracle's rank, sigma and products.
+    n, d = 900, 8
+    if shape == "biclique":
+        # complete bipartite K_{3,897}: rank 2
+        a = np.repeat(np.arange(3), n - 3)
+        b = np.tile(np.arange(3, n), 3)
+    else:
+        # five disjoint stars with distinct sizes: rank 10
+        a, b, nxt = [], [], 5
+        for c, sz in enumerate((40, 70, 110, 160, 220)):
+            a += [c] * sz
+            b += list(range(nxt, nxt + sz))
+            nxt += sz
+        a, b = np.array(a), np.array(b)
+    g = oracle.Graph(n, np.concatenate([a, b]).astype(np.int64),
+                     np.concatenate([b, a]).astype(np.int64), None, True)
+    oe = oracle.OracleEngine(g, d=d, alpha=1.0, seed=7)
+    off, tgt, wts = g.csr()
+    e = ge.Engine.from_graph(n, off, tgt, None, d, alpha=1.0, undirected=True, seed=7)
+    so, sg = oe.get(oe.SIGMA), e.get(ge.SIGMA)
+    print(shape, "oracle k", len(so), "device k", len(sg), "sigma", so, sg)
+    assert len(so) == len(sg) and (shape == "stars" or len(so) < d)  # biclique: rank 2 < d
+    assert sigma_rel(sg, so) <= 1e-6
+    po = oe.get(oe.X) @ oe.get(oe.Y).T
+    pg = e.get(ge.X).astype(np.float64) @ e.get(ge.Y).astype(np.float64).T
+    rel = np.linalg.norm(pg - po) / np.linalg.norm(po)
+    print(shape, "product rel", rel)
+    assert rel <= 1e-5
+    # the state is usable: a few events against the oracle
+    ev = oracle.Events.edges(1, [10, 11, 12], [20, 500, 600])
+    oe.apply(ev)
+    e.apply(W.EventList.edges(ge.ADD_EDGE, [10, 11, 12], [20, 500, 600]))
+    po = oe.get(oe.X) @ oe.get(oe.Y).T
+    pg = e.get(ge.X).astype(np.float64) @ e.get(ge.Y).astype(np.float64).T
+    rel = np.linalg.norm(pg - po) / np.linalg.norm(po)
+    print(shape, "after 3 insertions: k", e.k, oe.dims()[1], "product rel", rel)
+    assert e.k == oe.dims()[1] and rel <= 1e-4
+
+
 # ------------------------------------------------------ full-scale configs
 def compact_oracle(e, rows, off_h, tgt_h, d):
     """The fp64 oracle restricted to `rows` (sorted global ids): a factor-only
