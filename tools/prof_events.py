@@ -4,13 +4,14 @@ Phase counters need the library built with `make EXTRA=-DDAMF_PROF=1`."""
 import sys, os, time, json
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import bench
 from paper_2306_08967_b200 import engine as ge
+from paper_2306_08967_b200 import workloads as W
 
 nev = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 alphas = [float(a) for a in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1.0, 0.15]
-d = bench.build_cfg2()
-w = d["w"]
+w = W.cfg2()
+off_, tgt_ = W.undirected_csr(w["n"], *w["init"])
+d = {"n": w["n"], "off": off_, "tgt": tgt_}
 for alpha in alphas:
     e = ge.Engine.from_graph(d["n"], d["off"], d["tgt"], None, w["d"], alpha=alpha, eps=w["eps"],
                              undirected=True, seed=0, node_capacity=4096)
