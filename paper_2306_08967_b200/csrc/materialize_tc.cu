@@ -789,6 +789,302 @@ __global__ void __launch_bounds__(B256_THREADS, 1)
   }
 }
 
+// ---- d = 256 on CTA pairs (tcgen05.mma.cta_group::2) -------------------------
+// The single-CTA kernel above is bound by shared-memory bandwidth: per 32-wide
+// K slice a CTA's tensor core reads 72 KB of operands (three passes over a
+// 128 x 32 X operand and a 256 x 32 F operand) next to 48 KB of TMA writes
+// and 64 KB of split / epilogue traffic, ~80 % of 128 B/clk. A CTA pair
+// computes a 256-row tile with ONE F slice between its two SMs: each CTA
+// holds half of the slice's rows (N) and the pair's MMA reads both halves, so
+// F costs each SM half the reads and half the TMA writes. Clusters of four =
+// two pairs; CTA r of the cluster loads rows [64 r, 64 r + 64) of every slice
+// and multicasts them to the two CTAs that hold that half (pair rank r / 2).
+// Only the pair's even CTA issues MMAs; its barriers collect the arrivals of
+// both CTAs (operands split, accumulator drained), and its commits are
+// multicast to both (operand slot free, accumulator full) or to the whole
+// cluster (F slot free).
+#ifndef P256_XR_
+#define P256_XR_ 5
+#define P256_OP_ 3
+#define P256_FR_ 4
+#endif
+constexpr int P256_XR = P256_XR_;          // raw X ring (16 KB each)
+constexpr int P256_OP = P256_OP_;          // operand ring (hi 8 KB | lo 8 KB)
+constexpr int P256_FR = P256_FR_;          // F ring of half slices (hi 8 KB | lo 8 KB)
+constexpr int P256_FH = 128 * 64;          // half of one K slice of F^T (128 rows x 32 bf16)
+constexpr int P256_PR = 4;                 // forwarded-readiness ring (>= min(OP, FR))
+static_assert(P256_PR >= (P256_OP < P256_FR ? P256_OP : P256_FR), "pready ring too short");
+constexpr size_t P256_SMEM = 1024 + (size_t)P256_XR * CHUNK_BYTES + (size_t)P256_OP * 2 * 8192 +
+                             (size_t)P256_FR * 2 * P256_FH + 8 * OSTAGE + 512;
+static_assert(P256_SMEM <= 232448, "pair kernel shared memory above the opt-in limit");
+
+DAMF_D void mma_bf16_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+DAMF_D void mma_commit_mc2(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA `cta` of the cluster
+DAMF_D void mbar_arrive_cta(uint64_t* b, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(cta));
+  // (default semantics, as cutlass::arch::ClusterBarrier::arrive(cta_id): a
+  // release at cluster scope here is a full fence per call, and the one
+  // forwarding thread then paces the whole pair at ~1 us per K slice. What it
+  // forwards was made visible by its owners -- fence.proxy.async by the split
+  // warps, the TMA's complete_tx -- before this thread observed their barriers.)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+template <int CS>  // 4: two pairs sharing each F slice by multicast; 2: one pair, its own F halves
+__global__ void __launch_bounds__(B256_THREADS, 1)
+    materialize_bf16_256_pair(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap zmap,
+                              const __grid_constant__ CUtensorMap fhmap, const __grid_constant__ CUtensorMap flmap,
+                              int64_t n) {
+  constexpr int D = 256, KB = D / B256_KC;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sXR = sm;                                        // [XR][16 KB] raw fp32
+  unsigned char* sOP = sXR + P256_XR * CHUNK_BYTES;               // [OP][hi 8 KB | lo 8 KB]
+  unsigned char* sF = sOP + P256_OP * 2 * 8192;                   // [FR][hi 8 KB | lo 8 KB]
+  unsigned char* sO = sF + P256_FR * 2 * P256_FH;                 // [4 warps][2][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 4 * 2 * OSTAGE);
+  uint64_t* xfull = bars;                          // X TMA -> split (local)
+  uint64_t* xempty = xfull + P256_XR;              // split -> X producer (local, 4 warps)
+  uint64_t* ofull = xempty + P256_XR;              // split -> local (4 warps)
+  uint64_t* oempty = ofull + P256_OP;              // leader's commit -> split (both CTAs)
+  uint64_t* ffull = oempty + P256_OP;              // F TMA (two source CTAs) -> local
+  uint64_t* pready = ffull + P256_FR;              // peer: "operands and F half of slice it are in my
+                                                   // shared memory", forwarded -> leader's MMA (1)
+  uint64_t* fempty = pready + P256_PR;             // both leaders' commits -> F producers (2)
+  uint64_t* tfull = fempty + P256_FR;              // leader's commit -> epilogue (both CTAs)
+  uint64_t* tempty = tfull + 2;                    // epilogue -> local (4 warps)
+  uint64_t* ptempty = tempty + 2;                  // peer's tempty forwarded -> leader's MMA (1)
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(ptempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_rank();
+  const int leader = rank & ~1;                    // the pair's MMA-issuing CTA
+  const bool is_leader = rank == leader;
+  const uint16_t pair_mask = (uint16_t)(3u << leader);
+  const int64_t ntiles = (n + TM - 1) / TM;
+  const int64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+  auto tile_of = [&](int64_t i) { return (cid + i * ncl) * CS + rank; };
+  const int64_t iters = ntiles > cid * CS ? (ntiles - cid * CS + ncl * CS - 1) / (ncl * CS) : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P256_XR; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 4);
+    }
+    for (int s = 0; s < P256_OP; ++s) {
+      mbar_init(&ofull[s], 4);
+      mbar_init(&oempty[s], 1);
+    }
+    for (int s = 0; s < P256_FR; ++s) {
+      mbar_init(&ffull[s], 1);
+      mbar_init(&fempty[s], CS / 2);
+    }
+    for (int s = 0; s < P256_PR; ++s) mbar_init(&pready[s], 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+      mbar_init(&ptempty[a], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+  if (warp == 0) {
+    // ===== X producer: raw fp32 K slices of this CTA's tiles
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t i = 0; i < iters; ++i) {
+        const int64_t t = tile_of(i) < ntiles ? tile_of(i) : ntiles - 1;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % P256_XR;
+          if (it >= P256_XR) mbar_wait(&xempty[s], ((it / P256_XR) - 1) & 1);
+          mbar_expect_tx(&xfull[s], CHUNK_BYTES);
+          tma_load_2d(sXR + (size_t)s * CHUNK_BYTES, &xmap, kb * B256_KC, (int)(t * TM), &xfull[s]);
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ===== F producer: rows [64 rank, +64) of every F^T slice, to the two CTAs
+    // that hold that half (pair rank = rank / 2: cluster ranks rank/2 and rank/2 + 2)
+    if (lane == 0) {
+      const uint16_t fmask = (uint16_t)(5u << (rank >> 1));
+      uint32_t it = 0;
+      for (int64_t i = 0; i < iters; ++i)
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % P256_FR;
+          if (it >= P256_FR) mbar_wait(&fempty[s], ((it / P256_FR) - 1) & 1);
+          // this CTA's half of the slice: 128 rows x 64 B, hi and lo
+          mbar_expect_tx(&ffull[s], 2 * P256_FH);
+          unsigned char* fb = sF + (size_t)s * 2 * P256_FH;
+          if (CS == 4) {
+            // two source CTAs per half: this one brings rows [64 rank, +64)
+            unsigned char* fh = fb + (rank & 1) * 64 * 64;
+            tma_load_2d_mc(fh, &fhmap, kb * B256_KC, rank * 64, &ffull[s], fmask);
+            tma_load_2d_mc(fh + P256_FH, &flmap, kb * B256_KC, rank * 64, &ffull[s], fmask);
+          } else {
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              tma_load_2d(fb + h2 * 64 * 64, &fhmap, kb * B256_KC, rank * 128 + h2 * 64, &ffull[s]);
+              tma_load_2d(fb + P256_FH + h2 * 64 * 64, &flmap, kb * B256_KC, rank * 128 + h2 * 64, &ffull[s]);
+            }
+          }
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && is_leader) {
+      // ===== MMA issuer of the pair: M = 256 (128 rows per CTA), N = 256 (128 F rows per CTA)
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(D >> 3) << 17) |
+                                 ((uint32_t)((2 * TM) >> 4) << 24);
+      uint32_t it = 0, tl = 0;
+      const uint32_t obase = smem_u32(sOP), fbase = smem_u32(sF);
+      for (int64_t i = 0; i < iters; ++i, ++tl) {
+        const int a = tl & 1;
+        if (tl >= 2) {
+          mbar_wait(&tempty[a], ((tl >> 1) - 1) & 1);
+          mbar_wait(&ptempty[a], ((tl >> 1) - 1) & 1);
+        }
+        tc_fence_after();
+        const uint32_t dtm = tmem + (uint32_t)(a * D);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int so = it % P256_OP, sf = it % P256_FR;
+          mbar_wait(&ffull[sf], (it / P256_FR) & 1);
+          mbar_wait(&ofull[so], (it / P256_OP) & 1);
+          mbar_wait(&pready[it % P256_PR], (it / P256_PR) & 1);
+          tc_fence_after();
+          const uint32_t xh = obase + (uint32_t)so * 2 * 8192, xl = xh + 8192;
+          const uint32_t fh = fbase + (uint32_t)sf * 2 * P256_FH, fl = fh + P256_FH;
+#pragma unroll
+          for (int ks = 0; ks < B256_KC / 16; ++ks) {  // 16 bf16 (32 B) per MMA
+            const uint32_t ko = ks * 32;
+            const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+            mma_bf16_2cta(dtm, umma_desc_sw64(xh + ko), umma_desc_sw64(fh + ko), idesc, acc0);
+            mma_bf16_2cta(dtm, umma_desc_sw64(xh + ko), umma_desc_sw64(fl + ko), idesc, 1u);
+            mma_bf16_2cta(dtm, umma_desc_sw64(xl + ko), umma_desc_sw64(fh + ko), idesc, 1u);
+          }
+          mma_commit_mc2(&oempty[so], pair_mask);
+          mma_commit_mc2(&fempty[sf], (uint16_t)((1u << CS) - 1));
+        }
+        mma_commit_mc2(&tfull[a], pair_mask);
+      }
+    } else if (lane == 0) {
+      // ===== the peer's forwarder: one cluster-scope arrival per slice ("my
+      // operands and my F half are in place") and per drained accumulator, so
+      // that the split and epilogue warps signal locally (a release at cluster
+      // scope from every warp cost 28 % of the kernel's issue slots in fences)
+      uint32_t it = 0, tl = 0;
+      for (int64_t i = 0; i < iters; ++i, ++tl) {
+        const int a = tl & 1;
+        if (tl >= 2) {
+          mbar_wait(&tempty[a], ((tl >> 1) - 1) & 1);
+          mbar_arrive_cta(&ptempty[a], (uint32_t)leader);
+        }
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int so = it % P256_OP, sf = it % P256_FR;
+          mbar_wait(&ffull[sf], (it / P256_FR) & 1);
+          mbar_wait(&ofull[so], (it / P256_OP) & 1);
+          mbar_arrive_cta(&pready[it % P256_PR], (uint32_t)leader);
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ===== split (as in the single-CTA kernel); "operands ready" goes to the leader
+    const int r = threadIdx.x - 64;
+    const uint32_t xbase = smem_u32(sXR), obase = smem_u32(sOP);
+    uint32_t it = 0;
+    for (int64_t i = 0; i < iters; ++i)
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int sx = it % P256_XR, so = it % P256_OP;
+        mbar_wait(&xfull[sx], (it / P256_XR) & 1);
+        const uint32_t st = xbase + (uint32_t)sx * CHUNK_BYTES;
+        float4 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = lds128(st + r * 128 + ((c ^ (r & 7)) << 4));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[sx]);  // raw slot free: values are in registers
+        if (it >= P256_OP) mbar_wait(&oempty[so], ((it / P256_OP) - 1) & 1);
+        const uint32_t ob = obase + (uint32_t)so * 2 * 8192;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {  // bf16 chunk c = fp32 columns 8c .. 8c+7
+          const float4 p = v[2 * c], q = v[2 * c + 1];
+          uint4 h, l;
+          h.x = pack_bf16(p.x, p.y);
+          h.y = pack_bf16(p.z, p.w);
+          h.z = pack_bf16(q.x, q.y);
+          h.w = pack_bf16(q.z, q.w);
+          l.x = pack_bf16(p.x - __uint_as_float(h.x << 16), p.y - __uint_as_float(h.x & 0xFFFF0000u));
+          l.y = pack_bf16(p.z - __uint_as_float(h.y << 16), p.w - __uint_as_float(h.y & 0xFFFF0000u));
+          l.z = pack_bf16(q.x - __uint_as_float(h.z << 16), q.y - __uint_as_float(h.z & 0xFFFF0000u));
+          l.w = pack_bf16(q.z - __uint_as_float(h.w << 16), q.w - __uint_as_float(h.w & 0xFFFF0000u));
+          const uint32_t off = r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+          sts128(ob + off, h);
+          sts128(ob + 8192 + off, l);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ofull[so]);
+      }
+  } else {
+    // ===== epilogue: TMEM -> registers -> swizzled smem -> TMA store (this CTA's 128 rows)
+    const int q = warp & 3;
+    unsigned char* stg = sO + (size_t)(warp - 6) * 2 * OSTAGE;
+    uint32_t tl = 0, sb = 0;
+    for (int64_t i = 0; i < iters; ++i, ++tl) {
+      const int64_t t = tile_of(i);
+      const int a = tl & 1;
+      mbar_wait(&tfull[a], (tl >> 1) & 1);
+      tc_fence_after();
+      const int64_t row0 = t * TM + q * 32;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32, sb ^= 1) {
+        uint32_t rr[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * D + c0), rr);
+        unsigned char* buf = stg + sb * OSTAGE;
+        if (lane == 0) tma_store_wait_read1();
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4*>(buf + sw128(lane, 4 * v)) =
+              make_float4(__uint_as_float(rr[4 * v]), __uint_as_float(rr[4 * v + 1]),
+                          __uint_as_float(rr[4 * v + 2]), __uint_as_float(rr[4 * v + 3]));
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && row0 < n) tma_store_2d(&zmap, c0, (int)row0, buf);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  // no CTA may leave while a peer can still multicast into it or arrive on its barriers
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 template <int CS>
 cudaError_t launch_bf16_256(const CUtensorMap& map, const CUtensorMap& zm, const CUtensorMap& fh,
                             const CUtensorMap& fl, int64_t n, int64_t ntiles, cudaStream_t s, int nsm) {
@@ -833,6 +1129,50 @@ cudaError_t launch_bf16_256(const CUtensorMap& map, const CUtensorMap& zm, const
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, materialize_bf16_256<CS>, map, zm, fh, fl, n);
+}
+
+template <int CS>
+cudaError_t launch_bf16_256_pair(const CUtensorMap& map, const CUtensorMap& zm, const CUtensorMap& fh,
+                                 const CUtensorMap& fl, int64_t n, int64_t ntiles, cudaStream_t s, int nsm) {
+  const size_t smem = P256_SMEM;
+  static int grid = 0;
+  if (!grid) {
+    cudaError_t e = cudaFuncSetAttribute(materialize_bf16_256_pair<CS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    grid = nsm / CS * CS;
+    cudaLaunchConfig_t q = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    q.gridDim = dim3(grid);
+    q.blockDim = dim3(B256_THREADS);
+    q.dynamicSmemBytes = smem;
+    q.attrs = at;
+    q.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, materialize_bf16_256_pair<CS>, &q) == cudaSuccess && ncl > 0 &&
+        ncl * CS < grid)
+      grid = ncl * CS;
+  }
+  int g = grid;
+  const int64_t groups = (ntiles + CS - 1) / CS;
+  if (groups * CS < g) g = (int)(groups * CS);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(B256_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, materialize_bf16_256_pair<CS>, map, zm, fh, fl, n);
 }
 
 template <int D>
@@ -890,6 +1230,11 @@ cudaError_t launch_tc(const float* X, int64_t n, int ldx, const float* Fhi, cons
                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    // dev switch while the pair kernel is being validated: DAMF_MAT256_PAIR=1
+    static const int pair = [] { const char* e = getenv("DAMF_MAT256_PAIR"); return e ? atoi(e) : 4; }();
+    static_assert(B256_CS == 4, "the pair kernel shares the 64-row F boxes of the 4-CTA clusters");
+    if (pair == 4) return launch_bf16_256_pair<4>(map, zm, fh, fl, n, ntiles, s, nsm);
+    if (pair == 2) return launch_bf16_256_pair<2>(map, zm, fh, fl, n, ntiles, s, nsm);
     return launch_bf16_256<B256_CS>(map, zm, fh, fl, n, ntiles, s, nsm);
   }
   if (D == 128) {
