@@ -37,6 +37,11 @@ constexpr int TT = 256;
 
 // y[u] = sum_p w_p x[ids_p]: warp per row, NV column values per lane (one
 // pass over the row for l <= 32 NV), 4 neighbour rows in flight.
+// Rows above kSpmmHeavy arcs are left at zero here and accumulated by
+// spmm_heavy_f64 (one warp walking a 100 k-arc hub row set the length of the
+// whole product on R-MAT graphs: 625 GB/s of DRAM traffic at scale 22).
+constexpr int kSpmmHeavy = 256;    // rows above this many arcs go to spmm_heavy_f64
+constexpr int kSpmmChunk = 2048;   // arcs one block of spmm_heavy_f64 takes (8 warps x 256)
 template <int NV>
 __global__ void spmm_gather_f64(const int64_t* off, const int32_t* ids, const double* wts,
                                 int64_t n, const double* __restrict__ x, double* __restrict__ y,
@@ -45,7 +50,7 @@ __global__ void spmm_gather_f64(const int64_t* off, const int32_t* ids, const do
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u = warp; u < n; u += nw) {
-    const int64_t b = off[u], e = off[u + 1];
+    const int64_t b = off[u], e = off[u + 1] - off[u] > kSpmmHeavy ? off[u] : off[u + 1];
     double acc[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) acc[t] = 0.0;
@@ -87,10 +92,88 @@ __global__ void spmm_gather_f64(const int64_t* off, const int32_t* ids, const do
   }
 }
 
+// heavy[0 .. *count): rows with more than kSpmmHeavy arcs; *maxdeg = the largest of them
+__global__ void collect_heavy(const int64_t* off, int64_t n, int* heavy, int* count, int cap, int* maxdeg) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = off[u + 1] - off[u];
+    if (c > kSpmmHeavy) {
+      const int at = atomicAdd(count, 1);
+      if (at < cap) heavy[at] = (int)u;
+      atomicMax(maxdeg, (int)(c > 0x7fffffff ? 0x7fffffff : c));
+    }
+  }
+}
+// y[u] += sum over chunk blockIdx.x (kSpmmChunk arcs) of heavy row u = heavy[blockIdx.y]:
+// 8 warps x 256 arcs, four neighbour rows in flight per warp, block-reduced
+// in shared memory, one fp64 atomic per column (y[u] was left at zero).
+template <int NV>
+__global__ void __launch_bounds__(TT) spmm_heavy_f64(const int64_t* off, const int32_t* ids, const double* wts,
+                                                     const int* heavy, const double* __restrict__ x,
+                                                     double* __restrict__ y, int l) {
+  extern __shared__ double red[];  // 8 x l
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t u = heavy[blockIdx.y];
+  const int64_t rb = off[u], re = off[u + 1];
+  const int64_t cb = rb + (int64_t)blockIdx.x * kSpmmChunk;
+  if (cb >= re) return;
+  const int64_t ce = cb + kSpmmChunk < re ? cb + kSpmmChunk : re;
+  const int64_t b = cb + (int64_t)warp * (kSpmmChunk / 8);
+  const int64_t e = b + kSpmmChunk / 8 < ce ? b + kSpmmChunk / 8 : ce;
+  double acc[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) acc[t] = 0.0;
+  for (int64_t p0 = b; p0 < e; p0 += 32) {
+    const int64_t p = p0 + lane;
+    int v = 0;
+    double w = 0.0;
+    if (p < e) {
+      v = ids[p];
+      w = wts ? wts[p] : 1.0;
+    }
+    const int cnt = (int)(e - p0 < 32 ? e - p0 : 32);
+    for (int s0 = 0; s0 < cnt; s0 += 4) {
+      double xv[4][NV];
+      double ww[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int src = s0 + h < cnt ? s0 + h : 0;
+        const int vv = __shfl_sync(0xffffffffu, v, src);
+        ww[h] = s0 + h < cnt ? __shfl_sync(0xffffffffu, w, src) : 0.0;
+        const double* xr = x + (int64_t)vv * l;
+#pragma unroll
+        for (int t = 0; t < NV; ++t) {
+          const int c = lane + 32 * t;
+          xv[h][t] = c < l ? xr[c] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int t = 0; t < NV; ++t) acc[t] = fma(ww[h], xv[h][t], acc[t]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int c = lane + 32 * t;
+    if (c < l) red[warp * l + c] = acc[t];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < l; c += TT) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) sum += red[w8 * l + c];
+    if (sum != 0.0) atomicAdd(&y[u * l + c], sum);
+  }
+}
+
 // G[i0 + a][j0 + b] (a, b < GB; G zeroed) += sum_r Y[r][i0 + a] Y[r][j0 + b]:
 // one GB x GB block of the Gram matrix per launch, row tiles of Y staged in
 // shared memory, a 4 x 4 register block of G per thread, fp64 atomics at the
-// end.
+// end. Only blocks with j0 >= i0 are launched (the Cholesky reads the upper
+// triangle): six instead of nine passes over Y at l = 138. (128 x 128 blocks
+// with 8 x 8 register blocks cut the DRAM traffic threefold but not the time:
+// the ragged edge blocks of l = 138 then waste 80 % of the FMAs.)
 constexpr int GB = 64;
 __global__ void gram_block_f64(const double* __restrict__ Y, int64_t n, int l, double* G, int i0,
                                int j0) {
@@ -515,14 +598,47 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
     cudaFuncSetAttribute(tall_mm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
     cudaFuncSetAttribute(gram_block_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem);
     cudaFuncSetAttribute(tall_mm<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
+    // heavy rows of A and of A^T (collected once; order is irrelevant)
+    const int kHeavyCap = (int)std::min<int64_t>(n, 0x7fffffff);  // every row could be heavy
+    int* hvy[2] = {nullptr, nullptr};
+    int hcount[2] = {0, 0}, hmax[2] = {0, 0};
+    {
+      double* raw = nullptr;  // (freed with the other temporaries)
+      if ((err = alloc(&raw, (size_t)kHeavyCap + 8))) break;  // 2 lists of n ints + 4 counters
+      hvy[0] = reinterpret_cast<int*>(raw);
+      hvy[1] = hvy[0] + kHeavyCap;
+      int* meta = hvy[1] + kHeavyCap;  // [count, maxdeg] x 2
+      cudaMemsetAsync(meta, 0, 4 * sizeof(int), st);
+      for (int tr = 0; tr < 2; ++tr)
+        collect_heavy<<<nsm * 8, 256, 0, st>>>(tr ? g.toff : g.off, n, hvy[tr], meta + 2 * tr, kHeavyCap,
+                                               meta + 2 * tr + 1);
+      int hm[4] = {0, 0, 0, 0};
+      cudaMemcpyAsync(hm, meta, sizeof(hm), cudaMemcpyDeviceToHost, st);
+      if ((err = cudaStreamSynchronize(st))) break;
+      for (int tr = 0; tr < 2; ++tr) {
+        hcount[tr] = std::min(hm[2 * tr], kHeavyCap);
+        hmax[tr] = hm[2 * tr + 1];
+      }
+    }
+    cudaFuncSetAttribute(spmm_heavy_f64<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 288 * 8);
+    cudaFuncSetAttribute(spmm_heavy_f64<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 288 * 8);
     auto apply = [&](const double* x, double* y, bool transposed) {
       const int64_t* o = transposed ? g.toff : g.off;
       const int32_t* i = transposed ? g.tids : g.ids;
       const double* w = transposed ? g.twts : g.wts;
+      const int tr = transposed ? 1 : 0;
       if (l <= 160)
         spmm_gather_f64<5><<<gs, 256, 0, st>>>(o, i, w, n, x, y, l);
       else
         spmm_gather_f64<9><<<gs, 256, 0, st>>>(o, i, w, n, x, y, l);
+      for (int h0 = 0; h0 < hcount[tr]; h0 += 32768) {
+        const dim3 hg((unsigned)((hmax[tr] + kSpmmChunk - 1) / kSpmmChunk),
+                      (unsigned)std::min(32768, hcount[tr] - h0));
+        if (l <= 160)
+          spmm_heavy_f64<5><<<hg, TT, (size_t)8 * l * 8, st>>>(o, i, w, hvy[tr] + h0, x, y, l);
+        else
+          spmm_heavy_f64<9><<<hg, TT, (size_t)8 * l * 8, st>>>(o, i, w, hvy[tr] + h0, x, y, l);
+      }
     };
     // Gram-Schmidt QR in place on Ym (n x l), any rank: Q gets an orthonormal
     // basis whose leading columns span Ym's (dependent columns are replaced by
@@ -574,7 +690,7 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
         cudaMemsetAsync(G, 0, (size_t)l * l * 8, st);
         cudaMemsetAsync(dflag, 0, sizeof(int), st);
         for (int i0 = 0; i0 < l; i0 += GB)
-          for (int j0 = 0; j0 < l; j0 += GB)
+          for (int j0 = i0; j0 < l; j0 += GB)  // upper triangle only (chol_f64 reads nothing else)
             gram_block_f64<<<gs, TT, gram_smem, st>>>(Ym, n, l, G, i0, j0);
         chol_f64<<<1, 256, 0, st>>>(G, l, pass == 0 ? Racc : R, Ri, dflag);
         cudaMemcpyAsync(&hf, dflag, sizeof(int), cudaMemcpyDeviceToHost, st);
