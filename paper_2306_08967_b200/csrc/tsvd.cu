@@ -10,10 +10,12 @@
 // Omega is the reference's stream (mt19937_64 + Box-Muller, rng.hpp),
 // generated on the host, so the device init reproduces the reference's
 // subspace; everything else is fp64 on the device:
-//   spmm_gather_f64   y[u] = sum_{p in row u} w_p x[ids_p]   (warp per row)
-//   gram_f64          G = Y^T Y  (row tiles in shared memory, fp64 atomics)
-//   chol_f64          G = R^T R, R^-1 (one CTA)  -> CholeskyQR2
-//   tall_mm           Y <- Y M  (row tiles in shared memory; fp64 or fp32 out)
+//   spmm_gather_f64   y[u] = sum_{p in row u} w_p x[ids_p]   (warp per row; rows above
+//                     256 arcs by spmm_heavy_f64, a block per 2,048-arc chunk)
+//   gram_dmma         G = Y^T Y, upper triangle  (row tiles in shared memory, FP64
+//                     tensor cores, fp64 atomics)
+//   chol_f64          G = R^T R, R^-1 (one CTA)  -> CholeskyQR2 (gs_qr when rank-deficient)
+//   tall_mm_dmma      Y <- Y M  (row tiles in shared memory, FP64 tensor cores; fp64 or fp32 out)
 //   jacobi_svd_f64    one-sided Jacobi (round-robin pairs, one CTA)
 // Graphs with min_dim <= 600 take the reference's exact path (l = min_dim,
 // no power iterations), which is the exact truncated SVD of A: a dense
@@ -167,48 +169,127 @@ __global__ void __launch_bounds__(TT) spmm_heavy_f64(const int64_t* off, const i
   }
 }
 
-// G[i0 + a][j0 + b] (a, b < GB; G zeroed) += sum_r Y[r][i0 + a] Y[r][j0 + b]:
-// one GB x GB block of the Gram matrix per launch, row tiles of Y staged in
-// shared memory, a 4 x 4 register block of G per thread, fp64 atomics at the
-// end. Only blocks with j0 >= i0 are launched (the Cholesky reads the upper
-// triangle): six instead of nine passes over Y at l = 138. (128 x 128 blocks
-// with 8 x 8 register blocks cut the DRAM traffic threefold but not the time:
-// the ragged edge blocks of l = 138 then waste 80 % of the FMAs.)
-constexpr int GB = 64;
-__global__ void gram_block_f64(const double* __restrict__ Y, int64_t n, int l, double* G, int i0,
-                               int j0) {
-  extern __shared__ double sy[];  // RT x l
+// ---- FP64 tensor-core forms (mma.sync m8n8k4 .f64: a = A[lane>>2][lane&3],
+// b = B[lane&3][lane>>2], d{0,1} = D[lane>>2][2 (lane&3) + {0,1}]). SIMT fp64
+// FMAs run at ~6 TFLOP/s on this chip (the SIMT forms of both kernels below
+// were bound by them: 384 / 290 ms at scale 21 against 147 / 89 ms);
+// the DMMA pipe does 55 FMA/clk/SM (tools/micro_dmma.cu).
+DAMF_D void dmma884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+// padded row strides that keep the fragment loads at two wavefronts
+inline int gram_lp(int l) {  // == 8 or 24 mod 32, >= 8 ceil(l / 8)
+  int lp = 8 * ((l + 7) / 8);
+  while (lp % 32 != 8 && lp % 32 != 24) lp += 8;
+  return lp;
+}
+inline int mm_lp(int l) {  // == 4 mod 8 (odd multiple of 4), >= l rounded up to 4
+  int lp = (l + 3) & ~3;
+  if (lp % 8 == 0) lp += 4;
+  return lp;
+}
+// Upper triangle of G += Y^T Y in 8 x 8 tiles, tile q of the flat list to warp
+// q % 8; up to GT tiles per warp per launch (pass p covers tiles [p 8 GT, +8 GT)).
+constexpr int GT = 22;
+__global__ void __launch_bounds__(TT) gram_dmma(const double* __restrict__ Y, int64_t n, int l, int lp,
+                                                double* G, int pass) {
+  extern __shared__ double sy[];  // RT x lp
   constexpr int RT = 32;
-  const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;
-  const int ib = i0 + 4 * ti, jb = j0 + 4 * tj;
-  double acc[4][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nt = (l + 7) / 8, T = nt * (nt + 1) / 2;
+  const int fr = lane >> 2, fk = lane & 3;
+  // this warp's tiles: (it, jt), jt >= it, from the flat index
+  int ti[GT], tj[GT];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int q = 0; q < GT; ++q) {
+    int t = pass * 8 * GT + q * 8 + warp;
+    int it = 0;
+    if (t < T) {
+      while (t >= nt - it) {
+        t -= nt - it;
+        ++it;
+      }
+      ti[q] = it;
+      tj[q] = it + t;
+    } else {
+      ti[q] = -1;
+      tj[q] = -1;
+    }
+  }
+  double d0[GT], d1[GT];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int q = 0; q < GT; ++q) d0[q] = d1[q] = 0.0;
   for (int64_t r0 = (int64_t)blockIdx.x * RT; r0 < n; r0 += (int64_t)gridDim.x * RT) {
     const int rows = (int)(n - r0 < RT ? n - r0 : RT);
     __syncthreads();
-    for (int x = threadIdx.x; x < RT * l; x += TT) sy[x] = x / l < rows ? Y[r0 * l + x] : 0.0;
+    for (int x = threadIdx.x; x < RT * lp; x += TT) {
+      const int r = x / lp, c = x % lp;
+      sy[x] = (r < rows && c < l) ? Y[(r0 + r) * l + c] : 0.0;
+    }
     __syncthreads();
-    for (int r = 0; r < RT; ++r) {
-      double yi[4], yj[4];
+    for (int k0 = 0; k0 < RT; k0 += 4) {
+      const double* row = sy + (k0 + fk) * lp + fr;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        yi[a] = ib + a < l ? sy[r * l + ib + a] : 0.0;
-        yj[a] = jb + a < l ? sy[r * l + jb + a] : 0.0;
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(yi[a], yj[b], acc[a][b]);
+      for (int q = 0; q < GT; ++q)
+        if (ti[q] >= 0) dmma884(d0[q], d1[q], row[8 * ti[q]], row[8 * tj[q]]);
     }
   }
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int q = 0; q < GT; ++q) {
+    if (ti[q] < 0) continue;
+    const int gi = 8 * ti[q] + fr, gj = 8 * tj[q] + 2 * fk;
+    if (gi < l && gj < l && d0[q] != 0.0) atomicAdd(&G[gi * l + gj], d0[q]);
+    if (gi < l && gj + 1 < l && d1[q] != 0.0) atomicAdd(&G[gi * l + gj + 1], d1[q]);
+  }
+}
+// out[r][c] = sum_m Y[r][m] M[m][c] for c < mc (M: l x mc row-major), row tiles
+// of 64 staged in shared memory (in place when out == Y and mc <= l): warp w
+// owns rows 8 w .. 8 w + 7 of the tile and walks the columns in groups of MT8
+// 8-column tiles.
+constexpr int MT8 = 18;
+template <typename TO>
+__global__ void __launch_bounds__(TT) tall_mm_dmma(const double* Y, int64_t n, int l, int lp,
+                                                   const double* __restrict__ M, int mc, TO* out, int ldo) {
+  extern __shared__ double st[];  // 64 x lp
+  constexpr int RT = 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int l4 = (l + 3) & ~3;
+  for (int64_t r0 = (int64_t)blockIdx.x * RT; r0 < n; r0 += (int64_t)gridDim.x * RT) {
+    const int rows = (int)(n - r0 < RT ? n - r0 : RT);
+    __syncthreads();
+    for (int x = threadIdx.x; x < RT * lp; x += TT) {
+      const int r = x / lp, c = x % lp;
+      st[x] = (r < rows && c < l) ? Y[(r0 + r) * l + c] : 0.0;
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < mc; c0 += 8 * MT8) {
+      double d0[MT8], d1[MT8];
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (ib + a < l && jb + b < l) atomicAdd(&G[(ib + a) * l + jb + b], acc[a][b]);
+      for (int t = 0; t < MT8; ++t) d0[t] = d1[t] = 0.0;
+      for (int k0 = 0; k0 < l4; k0 += 4) {
+        const double a = st[(8 * warp + fr) * lp + k0 + fk];
+        const int km = k0 + fk;
+        const double* mrow = M + (int64_t)km * mc + c0 + fr;
+#pragma unroll
+        for (int t = 0; t < MT8; ++t) {
+          const double b = (km < l && c0 + 8 * t + fr < mc) ? __ldg(mrow + 8 * t) : 0.0;
+          dmma884(d0[t], d1[t], a, b);
+        }
+      }
+      const int r = 8 * warp + fr;
+      if (r < rows) {
+#pragma unroll
+        for (int t = 0; t < MT8; ++t) {
+          const int c = c0 + 8 * t + 2 * fk;
+          if (c < mc) out[(r0 + r) * ldo + c] = (TO)d0[t];
+          if (c + 1 < mc) out[(r0 + r) * ldo + c + 1] = (TO)d1[t];
+        }
+      }
+    }
+  }
 }
 
 // G = R^T R (R upper, row-major l x l, written in place of R), Rinv = R^-1.
@@ -257,49 +338,6 @@ __global__ void chol_f64(const double* G, int l, double* R, double* Rinv, int* f
     }
   }
   if (threadIdx.x == 0 && bad) *fail = 1;
-}
-
-// out[r][c] = sum_m Y[r][m] M[m][c] for c < mc (M: l x mc row-major), row
-// tiles staged in shared memory (in place when out == Y and mc <= l); each
-// thread computes a 4 x 4 output block per pass.
-template <typename TO>
-__global__ void tall_mm(const double* Y, int64_t n, int l, const double* __restrict__ M, int mc,
-                        TO* out, int ldo) {
-  extern __shared__ double st[];  // 64 x l
-  constexpr int RT = 64;
-  const int cb = (mc + 3) / 4;      // 4-column groups
-  const int nblk = (RT / 4) * cb;   // 4x4 blocks per tile
-  for (int64_t r0 = (int64_t)blockIdx.x * RT; r0 < n; r0 += (int64_t)gridDim.x * RT) {
-    const int rows = (int)(n - r0 < RT ? n - r0 : RT);
-    __syncthreads();
-    for (int x = threadIdx.x; x < RT * l; x += TT) st[x] = x / l < rows ? Y[r0 * l + x] : 0.0;
-    __syncthreads();
-    for (int bidx = threadIdx.x; bidx < nblk; bidx += TT) {
-      const int rb = 4 * (bidx / cb), c0 = 4 * (bidx % cb);
-      if (rb >= rows) continue;
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-      for (int m = 0; m < l; ++m) {
-        double ya[4], mb[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) ya[a] = st[(rb + a) * l + m];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) mb[b] = c0 + b < mc ? __ldg(M + (int64_t)m * mc + c0 + b) : 0.0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(ya[a], mb[b], acc[a][b]);
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (rb + a < rows && c0 + b < mc) out[(r0 + rb + a) * ldo + c0 + b] = (TO)acc[a][b];
-    }
-  }
 }
 
 // ---- rank-deficient sketches: classical Gram-Schmidt, twice, column by column
@@ -594,10 +632,13 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
       res->omega = 1;
     }
     const int gs = nsm * 8;
-    const size_t gram_smem = (size_t)32 * l * 8, mm_smem = (size_t)64 * l * 8;
-    cudaFuncSetAttribute(tall_mm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
-    cudaFuncSetAttribute(gram_block_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem);
-    cudaFuncSetAttribute(tall_mm<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
+    const int glp = gram_lp(l), mlp = mm_lp(l);
+    const size_t gram_smem = (size_t)32 * glp * 8, mm_smem = (size_t)64 * mlp * 8;
+    cudaFuncSetAttribute(tall_mm_dmma<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
+    cudaFuncSetAttribute(gram_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem);
+    cudaFuncSetAttribute(tall_mm_dmma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm_smem);
+    const int gram_tiles = ((l + 7) / 8) * ((l + 7) / 8 + 1) / 2;
+    const int gram_passes = (gram_tiles + 8 * GT - 1) / (8 * GT);
     // heavy rows of A and of A^T (collected once; order is irrelevant)
     const int kHeavyCap = (int)std::min<int64_t>(n, 0x7fffffff);  // every row could be heavy
     int* hvy[2] = {nullptr, nullptr};
@@ -689,9 +730,9 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
       for (int pass = 0; pass < 2; ++pass) {
         cudaMemsetAsync(G, 0, (size_t)l * l * 8, st);
         cudaMemsetAsync(dflag, 0, sizeof(int), st);
-        for (int i0 = 0; i0 < l; i0 += GB)
-          for (int j0 = i0; j0 < l; j0 += GB)  // upper triangle only (chol_f64 reads nothing else)
-            gram_block_f64<<<gs, TT, gram_smem, st>>>(Ym, n, l, G, i0, j0);
+        // upper triangle only (chol_f64 reads nothing else); one pass over Y per 176 tiles
+        for (int ps = 0; ps < gram_passes; ++ps)
+          gram_dmma<<<gs, TT, gram_smem, st>>>(Ym, n, l, glp, G, ps);
         chol_f64<<<1, 256, 0, st>>>(G, l, pass == 0 ? Racc : R, Ri, dflag);
         cudaMemcpyAsync(&hf, dflag, sizeof(int), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
@@ -704,16 +745,16 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
             if (pass == 0)
               cudaMemcpyAsync(Rout, R, (size_t)l * l * 8, cudaMemcpyDeviceToDevice, st);
             else
-              tall_mm<double><<<1, TT, mm_smem, st>>>(R, l, l, Racc, l, Rout, l);
+              tall_mm_dmma<double><<<1, TT, mm_smem, st>>>(R, l, l, mlp, Racc, l, Rout, l);
             cudaStreamSynchronize(st);
           }
           return 0;
         }
-        tall_mm<double><<<gs, TT, mm_smem, st>>>(Ym, n, l, Ri, l, Ym, l);
+        tall_mm_dmma<double><<<gs, TT, mm_smem, st>>>(Ym, n, l, mlp, Ri, l, Ym, l);
       }
       if (Rout) {
         // R = R_pass2 * R_pass1 (upper l x l), on the device via tall_mm
-        tall_mm<double><<<1, TT, mm_smem, st>>>(R, l, l, Racc, l, Rout, l);
+        tall_mm_dmma<double><<<1, TT, mm_smem, st>>>(R, l, l, mlp, Racc, l, Rout, l);
       }
       return 0;
     };
@@ -799,8 +840,8 @@ cudaError_t tsvd_init(const TsvdGraph& g, int d, uint64_t seed, cudaStream_t st,
       cudaFree(xb);
       break;
     }
-    tall_mm<float><<<gs, TT, mm_smem, st>>>(Y, n, l, Fu, k, xb, k);
-    tall_mm<float><<<gs, TT, mm_smem, st>>>(Q, n, l, Fv, k, yb, k);
+    tall_mm_dmma<float><<<gs, TT, mm_smem, st>>>(Y, n, l, mlp, Fu, k, xb, k);
+    tall_mm_dmma<float><<<gs, TT, mm_smem, st>>>(Q, n, l, mlp, Fv, k, yb, k);
     if ((err = cudaStreamSynchronize(st))) {
       cudaFree(xb);
       cudaFree(yb);
