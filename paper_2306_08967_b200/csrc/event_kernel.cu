@@ -1190,6 +1190,18 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
   for (int i = lo + grp; i < hi; i += NG) {
     const double di = S.kd[i];
     double p = 1.0;
+    if (K <= 144) {
+      // all of a lane's ratios (up to 9) in flight at once, as in secular_pass
+      double q[9];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) {
+        const int j = gl + 16 * u;
+        const bool in = j < K;
+        const double lmd = in ? S.tau[j] - (di - S.kd[S.org[j]]) : 1.0;  // lambda_j - d_i
+        q[u] = lmd * frcp(in ? (j == i ? rhoN : S.kd[j] - di) : 1.0);
+      }
+      p = ((q[0] * q[1]) * (q[2] * q[3])) * ((q[4] * q[5]) * (q[6] * q[7])) * q[8];
+    } else
     for (int j0 = gl; j0 < K; j0 += 64) {
       // four ratios in flight per lane (branch-free reciprocals)
       double lmd[4], r[4];
@@ -1260,6 +1272,27 @@ DAMF_D void eig_rank1(Smem<C>& S, cg::cluster_group& cl, const double* dd, const
       if (item < K) {
         const double dj = S.kd[S.org[item]], tj = S.tau[item];
         double nn = 0;
+        if (K <= 144) {
+          // one pass: the lane's (up to 9) components stay in registers between
+          // the norm and the scaled store
+          double y[9];
+#pragma unroll
+          for (int u = 0; u < 9; ++u) {
+            const int t = gl + 16 * u;
+            const bool in = t < K;
+            y[u] = (in ? S.zhat[t] : 0.0) * frcp(in ? (S.kd[t] - dj) - tj : 1.0);
+          }
+          nn = ((y[0] * y[0] + y[1] * y[1]) + (y[2] * y[2] + y[3] * y[3])) +
+               ((y[4] * y[4] + y[5] * y[5]) + (y[6] * y[6] + y[7] * y[7])) + y[8] * y[8];
+          const double inv = rsqrt(gsum(nn, gm));
+#pragma unroll
+          for (int u = 0; u < 9; ++u) {
+            const int t = gl + 16 * u;
+            if (t < K) row[n - 1 - S.kidx[t]] = y[u] * inv;
+          }
+          __syncwarp(gm);
+          continue;
+        }
         for (int t0 = gl; t0 < K; t0 += 64) {
           double y[4];
 #pragma unroll
