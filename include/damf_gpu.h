@@ -156,6 +156,9 @@ typedef struct damf_diag {
   int64_t total_pushes;   /* enhancer.hpp:41                               */
   int64_t device_bytes;   /* HBM held by the handle                        */
   int64_t kernel_launches;/* kernels this handle has launched (all calls)  */
+  double last_materialize_ms; /* device time of the last damf_gpu_materialize's X F
+                                 kernels (CUDA events on the handle's stream around
+                                 the launch; 0 before the first call)            */
 } damf_diag;
 
 typedef struct damf_gpu damf_gpu; /* opaque handle: owns all device memory */

@@ -323,6 +323,8 @@ struct damf_gpu {
   std::vector<double> lat_us;
   int64_t lat_pending = 0;            // events whose stamps are still on the device
   cudaEvent_t span0 = nullptr, span1 = nullptr;
+  cudaEvent_t mat0 = nullptr, mat1 = nullptr;  // around the last materialisation's X F kernels
+  double last_mat_ms = 0.0;
   int64_t* rowlog = nullptr;          // device (step, side, row) triples
   long long rowlog_cap = 0;
   std::vector<int64_t> rowlog_h;      // the last apply's log (DAMF_APPLY_LOG_ROWS)
@@ -597,6 +599,8 @@ void damf_gpu_destroy(damf_gpu* h) {
   if (h->rowlog) cudaFree(h->rowlog);
   if (h->span0) cudaEventDestroy(h->span0);
   if (h->span1) cudaEventDestroy(h->span1);
+  if (h->mat0) cudaEventDestroy(h->mat0);
+  if (h->mat1) cudaEventDestroy(h->mat1);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -1794,11 +1798,17 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
   const int side = which == DAMF_Y ? 1 : (which == DAMF_Z && !h->alpha1) ? -1 : 0;
   const long long nd = side >= 0 ? h->h_ctl->dirty_n[side] : -1;
   const double cond = side == 1 ? h->h_ctl->cond_est_y : h->h_ctl->cond_est;
+  if (!h->mat0) {
+    CK(cudaEventCreate(&h->mat0));
+    CK(cudaEventCreate(&h->mat1));
+  }
+  CK(cudaEventRecord(h->mat0, h->st));
   if (cond <= kPreciseCond || (nd >= 0 && nd <= kDirtyCap && h->k <= 128)) {
     CK(launch_materialize(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
   } else {
     CK(launch_materialize_precise(base, h->n, h->k, h->d, PT, h->ld, h->k, out, h->k, h->st, h->nsm));
   }
+  CK(cudaEventRecord(h->mat1, h->st));
   // side-table rows from their fp64 base values with fp64 products
   const long long ns = side >= 0 ? std::min<long long>(nd, kDirtyCap) : 0;
   if (ns > 0) {
@@ -1812,6 +1822,10 @@ int damf_gpu_materialize(damf_gpu* h, int32_t which, float* dst, int32_t dst_is_
     cudaFree(out);
   }
   CK(cudaStreamSynchronize(h->st));
+  {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, h->mat0, h->mat1) == cudaSuccess) h->last_mat_ms = ms;
+  }
   return 0;
 }
 
@@ -2178,6 +2192,7 @@ int damf_gpu_diagnostics(damf_gpu* h, damf_diag* o) {
   o->total_pushes = h->h_pstats[0];
   o->device_bytes = (int64_t)h->bytes;
   o->kernel_launches = h->launches;
+  o->last_materialize_ms = h->last_mat_ms;
   return 0;
 }
 

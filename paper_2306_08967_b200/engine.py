@@ -75,7 +75,7 @@ class Diag(C.Structure):
                 ("events_applied", C.c_int64), ("events_since_rebase", C.c_int64),
                 ("cond_estimate", C.c_double), ("proj_row_bound", C.c_double),
                 ("total_pushes", C.c_int64), ("device_bytes", C.c_int64),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("last_materialize_ms", C.c_double)]
 
 
 _lib = None
