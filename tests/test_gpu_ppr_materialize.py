@@ -92,6 +92,20 @@ def test_defect_bound_holds_for_batched_streams():
     assert st["pushes"] <= 6 * (oe.stat(5) - p0) + 1000
 
 
+def test_engine_materialize_reports_kernel_time():
+    # damf_diag.last_materialize_ms: device time of the X F kernels of the last
+    # damf_gpu_materialize (what bench.py's roofline divides the bytes by)
+    g = oracle.gen_random_graph(400, 3000, 5)
+    oe = oracle.OracleEngine(g, d=16, alpha=1.0, seed=5)
+    e = gpu_from_oracle(g, oe, 16, 1.0, 1e-5)
+    assert e.diag()["last_materialize_ms"] == 0.0
+    x = np.zeros((e.n, e.k), np.float32)
+    e.materialize(ge.X, dst_ptr=x.ctypes.data, on_device=False)
+    ms = e.diag()["last_materialize_ms"]
+    assert 0.0 < ms < 50.0
+    assert rel_frob(x.astype(np.float64), oe.get(oe.X)) <= 1e-5
+
+
 def test_materialize_matches_fp64():
     import torch
     rng = np.random.default_rng(3)
@@ -108,6 +122,28 @@ def test_materialize_matches_fp64():
         err = rel_frob(Z.cpu().numpy().astype(np.float64), ref)
         print(d, err)
         assert err <= 1e-5
+
+
+@pytest.mark.parametrize("n", [1, 127, 129, 513, 1000, 128 * 148 + 77, 70001])
+def test_materialize_d256_pairs_ragged_sizes(n):
+    # d = 256 runs on CTA pairs inside 4-CTA clusters (tcgen05 cta_group::2):
+    # row counts that leave a partial tile, an odd number of tiles, fewer tiles
+    # than one cluster, and more tiles than one pass of the grid
+    import torch
+    rng = np.random.default_rng(n)
+    d = 256
+    x = (rng.standard_normal((n, d)) / np.sqrt(d)).astype(np.float32)
+    q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    F = q * rng.uniform(0.5, 2.0, d)[None, :]
+    X = torch.from_numpy(x).cuda()
+    Z = torch.full((n + 1, d), 7.0, dtype=torch.float32, device="cuda")  # canary row after the end
+    ge.materialize_dev(X.data_ptr(), n, d, F, Z.data_ptr())
+    torch.cuda.synchronize()
+    z = Z.cpu().numpy()
+    assert np.all(z[n] == 7.0)
+    err = rel_frob(z[:n].astype(np.float64), x.astype(np.float64) @ F)
+    print(n, err)
+    assert err <= 1e-5
 
 
 def test_large_graph_per_event_push_keeps_defect_bound():
