@@ -2154,25 +2154,31 @@ DAMF_D void ppr_event(const EventKernelArgs& A, SMT& S, cg::cluster_group& cl,
   const int k = S.k, d = A.d;
   const double alpha = A.alpha, om = 1.0 - alpha;
   long long _pt = clock64();
-  // ---- absorb_structure_delta for the touched rows (warp per row)
-  for (int q = rank * PNW + warp; q < ev.touched_cnt; q += C * PNW) {
+  // ---- absorb_structure_delta for the touched rows: one CTA per row, the
+  // row's arcs split over its warps (one warp per row walked ~50-100 arcs four
+  // at a time: ~9 us per event, with every other warp of the cluster waiting
+  // at the next barrier), partial sums combined through the candidate-list
+  // storage, which is idle until the lists are built
+  float* scr = reinterpret_cast<float*>(&S.plist[0][0]);  // [PNW][kMaxD]
+  static_assert(sizeof(S.plist) >= (size_t)PNW * kMaxD * sizeof(float), "absorb scratch");
+  for (int q = rank; q < ev.touched_cnt; q += C) {
     const int64_t u = A.touched[ev.touched_off + q];
     float acc[kMaxD / 32];
 #pragma unroll
     for (int t = 0; t < kMaxD / 32; ++t) acc[t] = 0.0f;
     const int64_t base = A.out.off[u];
     const int c = A.out.cnt[u];
-    // neighbour ids by lanes (one coalesced load per 32 arcs), four neighbour
-    // rows in flight (one row at a time left the warp waiting on a DRAM
-    // latency per arc: ~9 us per event for two rows of ~50-100 arcs)
-    for (int p0 = 0; p0 < c; p0 += 32) {
+    const int per = (c + PNW - 1) / PNW;
+    const int pb = min(c, warp * per), pe = min(c, pb + per);
+    // neighbour ids by lanes, four neighbour rows in flight
+    for (int p0 = pb; p0 < pe; p0 += 32) {
       int vl = 0;
       float wl = 0.0f;
-      if (p0 + lane < c) {
+      if (p0 + lane < pe) {
         vl = A.out.ids[base + p0 + lane];
         wl = A.out.wts ? (float)A.out.wts[base + p0 + lane] : 1.0f;
       }
-      const int cnt = min(32, c - p0);
+      const int cnt = min(32, pe - p0);
       for (int s0 = 0; s0 < cnt; s0 += 4) {
         float zz[4][kMaxD / 32], ww[4];
 #pragma unroll
@@ -2192,20 +2198,32 @@ DAMF_D void ppr_event(const EventKernelArgs& A, SMT& S, cg::cluster_group& cl,
           for (int t = 0; t < kMaxD / 32; ++t) acc[t] = fmaf(ww[h], zz[h][t], acc[t]);
       }
     }
-    const double deg = A.deg[u];
-    float m = 0.0f;
 #pragma unroll
     for (int t = 0; t < kMaxD / 32; ++t) {
       const int j = lane + 32 * t;
-      if (j < k) {
-        float r = (float)alpha * A.Xb[u * d + j] - A.Zb[u * d + j];
-        if (deg > 0.0) r += (float)(om / deg) * acc[t];
-        A.rb[u * d + j] = r;
-        m = fmaxf(m, fabsf(r));
-      }
+      if (j < k) scr[warp * kMaxD + j] = acc[t];
+    }
+    __syncthreads();
+    const double deg = A.deg[u];
+    float m = 0.0f;
+    for (int j = tid; j < k; j += PNT) {
+      float a = 0.0f;
+#pragma unroll
+      for (int w = 0; w < PNW; ++w) a += scr[w * kMaxD + j];  // fixed order
+      float r = (float)alpha * A.Xb[u * d + j] - A.Zb[u * d + j];
+      if (deg > 0.0) r += (float)(om / deg) * a;
+      A.rb[u * d + j] = r;
+      m = fmaxf(m, fabsf(r));
     }
     m = warp_max(m);
-    if (lane == 0) A.key[u] = (float)((double)m / fmax(deg, 1.0));
+    if (lane == 0) S.bred[warp] = (double)m;
+    __syncthreads();
+    if (tid == 0) {
+      double mm = 0.0;
+      for (int w = 0; w < PNW; ++w) mm = fmax(mm, S.bred[w]);
+      A.key[u] = (float)(mm / fmax(deg, 1.0));
+    }
+    __syncthreads();
   }
   PROF_MARK(23);
   if (A.mode & 2) return;  // DAMF_APPLY_DEFER_PUSH: absorb only
