@@ -2328,6 +2328,7 @@ DAMF_D void ppr_event(const EventKernelArgs& A, SMT& S, cg::cluster_group& cl,
     // warp w's destination [off, off+cnt) never overlaps a later segment's
     // unread source because off <= w*seg)
     for (int w = 1; w < PNW; ++w) {
+      if (s_cnt[w] == 0) continue;  // (block-uniform: nothing to move, no barrier -- the usual case)
       __syncthreads();
       if (warp == w)
         for (int i = lane; i < mycnt; i += 32) out[off + i] = out[w * seg + i];
